@@ -1,0 +1,794 @@
+/*
+ * oracle/urg_oracle.c -- CPU ORACLE for the batched UrgenGo launch-policy
+ * simulation.  TEST INFRASTRUCTURE ONLY: loaded by tests/, by
+ * __graft_entry__.smoke() and by bench.py's cpu_baseline / --impl reference
+ * legs -- never by the product path (paper_2509_12207_b200/).
+ *
+ * Plain, slow, single-threaded C.  It shares no code, header or table with the
+ * CUDA path; the only common things are the seeded input records
+ * (workloads/) and the written model.  Where the paper
+ * defines an operation the code follows it literally and in its order:
+ *
+ *   - Eq. 2 urgency (§4.2) is evaluated as the literal sums
+ *     over the remaining kernels / CPU segments (no suffix-sum caches);
+ *   - the Active Kernel Buffer (§4.4.2) is an explicit list
+ *     of entries (K, U_K, S_K, C, T_K, UL_C(T_K)) per chain, an entry deleted
+ *     once its kernel completed and a covering synchronisation returned;
+ *   - each chain's stream (§2, §4.4.3) is an
+ *     explicit FIFO queue of launched kernels;
+ *   - stream binding ranks the AKB chains with qsort;
+ *   - delayed launching scans the other chains' AKB entries;
+ *   - batched / overlapped synchronisation follows PAPER.md:496-509 (§4.4.5);
+ *   - early chain exit follows PAPER.md:401 (§4.3);
+ *   - GPU dispatch sorts the waiting stream heads.
+ *
+ * Everything the paper leaves open is a DESIGN.md "Model M0" reading (R0-R23);
+ * comments name the rule.  All time is int64 nanoseconds, no floating point.
+ *
+ * Parity pins for every exported function: tests/test_oracle_*.py.
+ * Unpinned: the Table 2 C2/C7 rank tie (Q7) -- "parity unpinned".
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define ORC_INF INT64_MAX
+
+/* ------------------------------------------------------------------ */
+/* Input records (mirrors workloads/spec.py; oracle-private definition) */
+/* ------------------------------------------------------------------ */
+typedef struct {
+    /* workload */
+    uint32_t num_chains;
+    const int64_t *ch_period, *ch_deadline, *ch_offset;
+    const uint32_t *ch_ntasks, *ch_cpu_sigma, *ch_gpu_sigma;
+    const uint32_t *t_cpu_nom, *t_cpu_est, *t_nk;   /* all tasks, chain-major */
+    const uint32_t *k_nom, *k_est;                  /* all kernels, chain-major */
+    const uint16_t *k_util;
+    uint32_t num_prio;
+    int64_t launch_ns, launch_akb_ns, sync_lo_ns, sync_hi_ns, jitter_ns;
+    const int32_t *inst_q16;    /* 4096 z quantiles or NULL */
+    const uint32_t *kern_q16;   /* 4096 factor quantiles or NULL */
+    int64_t rt_bin_ns;
+    uint32_t rt_bins;
+    /* policy */
+    uint32_t kind, flags, sync_mode;
+    int64_t delta_eval_ns, lax_threshold_ns, sleep_ns;
+    uint32_t util_exempt_permille;
+    /* batch */
+    uint64_t seed, scenario_begin, scenario_count;
+    int64_t horizon_ns;
+    uint32_t fa_num, fa_den, fd_num, fd_den, ftight_permille, tight_explicit, tight_mask;
+} orc_input;
+
+enum { ORC_FIFO = 0, ORC_STATIC = 1, ORC_URGENGO = 2 };
+enum { ORC_BIND = 1, ORC_DELAY = 2, ORC_EARLY_EXIT = 4 };
+enum { ORC_ASYNC = 0, ORC_EACH = 1, ORC_BATCHED = 2, ORC_OVERLAP = 3 };
+enum { TAG_ARR = 1, TAG_TIGHT = 2, TAG_INST = 3, TAG_KERN = 4, TAG_SYNC = 5 };
+
+/* trace kinds */
+enum { TR_STEP = 1, TR_INST_START, TR_TASK_START, TR_EVAL, TR_DELAY, TR_BIND, TR_ENQUEUE,
+       TR_DISPATCH, TR_RETIRE, TR_SYNC_CALL, TR_SYNC_RET, TR_FREE_CLOSE, TR_INST_DONE,
+       TR_EARLY_EXIT };
+
+#define REC_WORDS 8
+#define AGG_COUNTERS 5
+#define RATIO_BINS 101
+
+/* ------------------------------------------------------------------ */
+/* Philox4x32-10 counter-based RNG (Salmon, Moraes, Dror, Shaw, SC'11). */
+/* Oracle-private copy; pinned by known-answer vectors in the tests.    */
+/* ------------------------------------------------------------------ */
+void orc_philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4])
+{
+    uint32_t c0 = ctr_in[0], c1 = ctr_in[1], c2 = ctr_in[2], c3 = ctr_in[3];
+    uint32_t k0 = key_in[0], k1 = key_in[1];
+    for (int r = 0; r < 10; ++r) {
+        uint64_t p0 = (uint64_t)0xD2511F53u * c0;
+        uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
+        uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+        uint32_t n0 = hi1 ^ c1 ^ k0, n1 = lo1, n2 = hi0 ^ c3 ^ k1, n3 = lo0;
+        c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+        k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* One 32-bit random word of scenario s (R3-R5):
+ * ctr = (s, tag<<24 | c<<16, i, k>>2), key = (seed_lo, seed_hi), word k&3. */
+static uint32_t orc_word(uint64_t seed, uint64_t s, uint32_t tag, uint32_t c, uint32_t i, uint32_t k)
+{
+    uint32_t ctr[4] = {(uint32_t)s, (tag << 24) | (c << 16), i, k >> 2};
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    uint32_t out[4];
+    orc_philox4x32_10(ctr, key, out);
+    return out[k & 3];
+}
+
+/* ------------------------------------------------------------------ */
+/* Urgency (Eq. 2), its order key and the "truly urgent" predicate      */
+/* ------------------------------------------------------------------ */
+
+/* Eq. 2 denominator, the laxity
+ *   L = t_arr + D - sum_{k=n}^{N-1} ~E^gpu_k - sum_{j=m}^{M-1} ~E^cpu_j - t,
+ * with n = I~gpu (the launch counter) and m = I~cpu
+ * (PAPER.md:335).  UL_C(t) = 1/L is never formed (R9). */
+int64_t orc_eq2_laxity(int64_t t_arr, int64_t D, const uint32_t *est_gpu, uint32_t N, uint32_t n,
+                       const uint32_t *est_cpu, uint32_t M, uint32_t m, int64_t t)
+{
+    int64_t rem_gpu = 0, rem_cpu = 0;
+    for (uint32_t k = n; k < N; ++k) rem_gpu += est_gpu[k];
+    for (uint32_t j = m; j < M; ++j) rem_cpu += est_cpu[j];
+    return t_arr + D - rem_gpu - rem_cpu - t;
+}
+
+/* An int64 whose order is the order of UL = 1/L (R9):
+ * L = 0 -> +max (saturation), L > 0 -> 2^62 - L, L < 0 -> -2^62 - L. */
+int64_t orc_urgency_key(int64_t L)
+{
+    if (L == 0) return INT64_MAX;
+    if (L > 0) return ((int64_t)1 << 62) - L;
+    return -((int64_t)1 << 62) - L;
+}
+
+/* UL >= TH_urgent  <=>  0 <= L <= L_th  (R10) */
+int orc_is_urgent(int64_t L, int64_t L_th) { return L >= 0 && L <= L_th; }
+
+/* ------------------------------------------------------------------ */
+/* Ranking and stream-level normalisation     */
+/* ------------------------------------------------------------------ */
+typedef struct { int64_t key; uint32_t chain; } orc_rank_item;
+
+static int orc_rank_cmp(const void *a, const void *b)
+{
+    const orc_rank_item *x = a, *y = b;
+    if (x->key != y->key) return x->key > y->key ? -1 : 1;   /* more urgent first */
+    return x->chain < y->chain ? -1 : (x->chain > y->chain);  /* ties: smaller chain id */
+}
+
+/* rank_out[i] = 1-based rank of item i when sorted by urgency key descending. */
+void orc_rank(const int64_t *keys, const uint32_t *chains, uint32_t n, uint32_t *rank_out)
+{
+    orc_rank_item *it = malloc(sizeof(orc_rank_item) * (n ? n : 1));
+    for (uint32_t i = 0; i < n; ++i) { it[i].key = keys[i]; it[i].chain = chains[i]; }
+    qsort(it, n, sizeof(orc_rank_item), orc_rank_cmp);
+    for (uint32_t i = 0; i < n; ++i)
+        for (uint32_t r = 0; r < n; ++r)
+            if (it[r].chain == chains[i] && it[r].key == keys[i]) { rank_out[i] = r + 1; break; }
+    free(it);
+}
+
+/* Rank r of n_r normalised onto stream levels 1..NUM_PRI-1 (PAPER.md:466,
+ * "normalize these rankings to the range (1, NUM_PRI-1)"); level 0 is reserved
+ * for truly urgent tasks.  Floor linear map, middle level for a single
+ * member (R15; SPEC.md:402-404 examples). */
+uint32_t orc_normalise_level(uint32_t r, uint32_t n_r, uint32_t num_prio)
+{
+    if (num_prio <= 2) return num_prio - 1;
+    if (n_r <= 1) return 1 + (num_prio - 2) / 2;
+    return 1 + (uint32_t)(((uint64_t)(r - 1) * (num_prio - 2)) / (n_r - 1));
+}
+
+/* Batch closing rule of batched launching: kernels join the
+ * batch while the running sum of their estimates stays below Delta_eval; the
+ * kernel whose estimate brings the sum to >= Delta_eval is the last member
+ * (R17 / Q9).  Returns 1 when the batch closes after this kernel. */
+int orc_batch_add(int64_t *acc, uint32_t est, int64_t delta_eval)
+{
+    *acc += est;
+    if (*acc >= delta_eval) { *acc = 0; return 1; }
+    return 0;
+}
+
+void orc_plan_batches(const uint32_t *est, uint32_t n, int64_t delta_eval, uint8_t *close_after)
+{
+    int64_t acc = 0;
+    for (uint32_t k = 0; k < n; ++k) close_after[k] = (uint8_t)orc_batch_add(&acc, est[k], delta_eval);
+}
+
+/* Eq. 3: mean over chains of M_miss/M_total; chains with
+ * M_total = 0 are left out (R22). */
+double orc_overall_miss_ratio(const uint64_t *miss, const uint64_t *total, uint32_t n)
+{
+    double s = 0.0;
+    uint32_t used = 0;
+    for (uint32_t i = 0; i < n; ++i)
+        if (total[i]) { s += (double)miss[i] / (double)total[i]; ++used; }
+    return used ? s / used : 0.0;
+}
+
+/* ------------------------------------------------------------------ */
+/* Simulation state                                                    */
+/* ------------------------------------------------------------------ */
+typedef struct {            /* one AKB entry */
+    uint32_t K;             /* kernel index within the chain instance */
+    uint32_t U;             /* profiled utilisation (per-mille) */
+    uint32_t S;             /* stream = priority level bound */
+    uint32_t C;             /* chain id */
+    int64_t T;              /* last evaluation time T_K */
+    int64_t L;              /* last-evaluated laxity (UL_C(T_K) = 1/L) */
+} orc_akb_entry;
+
+typedef struct { uint32_t K; int64_t t_enq; } orc_stream_entry;
+
+enum { PC_ARRIVE = 0, PC_CPU_DONE, PC_ATTEMPT, PC_ENQUEUE, PC_SYNC_WAIT, PC_SYNC_RET, PC_DONE };
+
+typedef struct {
+    /* static per scenario */
+    int64_t Pp, Dp;                 /* P', D' (R3) */
+    uint32_t static_level;
+    uint32_t N, M;                  /* kernels and tasks (= CPU segments) per instance */
+    uint32_t kbase, tbase;          /* offsets into the flattened kernel / task arrays */
+    /* CPU thread of the chain (R6) */
+    int pc;
+    int64_t cpu_next;
+    uint32_t inst;                  /* current (or next) instance index */
+    int64_t t_arr;
+    uint32_t Fg, Fc;                /* per-instance factors, Q16.16 */
+    uint32_t task;                  /* current task tau */
+    uint32_t launched;              /* I~gpu: kernels launched in this instance */
+    uint32_t cpu_idx;               /* I~cpu */
+    uint32_t done;                  /* kernels of this instance completed on the GPU */
+    uint32_t level;                 /* stream level of the current task */
+    int64_t acc;                    /* estimated time of the open batch */
+    uint32_t batch_start;           /* first kernel of the open batch */
+    uint32_t sync_target, sync_ord;
+    int64_t sync_cost;
+    /* AKB instance of the chain */
+    orc_akb_entry *akb;
+    uint32_t akb_n;
+    int64_t T_last, L_last;
+    /* stream */
+    orc_stream_entry *q;
+    uint32_t q_head, q_tail;        /* entries [q_head, q_tail) */
+    int head_running;
+    int64_t head_ready, head_end;
+    /* results */
+    uint32_t total, miss, early, unfin, launches, hash;
+    uint64_t sum_rt;
+} orc_lane;
+
+typedef struct {
+    const orc_input *in;
+    uint64_t s;
+    uint32_t C;
+    orc_lane *lane;
+    uint32_t gpu_used;              /* sum of running utilisations, <= 1000 */
+    int64_t H, H_stop;
+    int64_t *snap_L;                /* AKB read view at the start of Phase B */
+    uint32_t *snap_n;
+    int64_t *akb_L_view;            /* scratch */
+    int64_t *trace; int64_t trace_cap; int64_t trace_len;
+    int64_t *agg;
+    int64_t steps, launches;
+    /* calibration sampling */
+    int64_t cal_next, cal_end;
+    int64_t *cal_L; int64_t cal_n, cal_cap;
+} orc_sim;
+
+static void tr(orc_sim *S, int64_t t, int64_t kind, int64_t c, int64_t i, int64_t a, int64_t b)
+{
+    if (!S->trace || S->trace_len >= S->trace_cap) return;
+    int64_t *r = S->trace + 6 * S->trace_len++;
+    r[0] = t; r[1] = kind; r[2] = c; r[3] = i; r[4] = a; r[5] = b;
+}
+
+static uint32_t hash_fold(uint32_t h, uint32_t x) { return (h ^ x) * 16777619u; }
+
+/* ---- scenario randomness (R3-R5) ---- */
+static int64_t arrival(const orc_sim *S, uint32_t c, uint32_t i)
+{
+    const orc_input *in = S->in;
+    int64_t jit = 0;
+    if (in->jitter_ns > 0)
+        jit = (int64_t)(orc_word(in->seed, S->s, TAG_ARR, c, i, 0) % (uint64_t)(in->jitter_ns + 1));
+    return in->ch_offset[c] + (int64_t)i * S->lane[c].Pp + jit;
+}
+
+static uint32_t inst_factor(const orc_sim *S, uint32_t c, uint32_t i, uint32_t which, uint32_t sigma_ppm)
+{
+    const orc_input *in = S->in;
+    if (!in->inst_q16) return 65536u;
+    int64_t z = in->inst_q16[orc_word(in->seed, S->s, TAG_INST, c, i, which) >> 20];
+    int64_t F = 65536 + (z * (int64_t)sigma_ppm) / 1000000;   /* C division truncates toward 0 */
+    if (F < 6554) F = 6554;                                    /* factor floor 0.1 (R4) */
+    return (uint32_t)F;
+}
+
+static int64_t kernel_duration(const orc_sim *S, uint32_t c, uint32_t i, uint32_t k)
+{
+    const orc_input *in = S->in;
+    const orc_lane *L = &S->lane[c];
+    uint64_t G = 65536u;
+    if (in->kern_q16) G = in->kern_q16[orc_word(in->seed, S->s, TAG_KERN, c, i, k) >> 20];
+    uint64_t d = (((uint64_t)in->k_nom[L->kbase + k] * L->Fg) >> 16) * G >> 16;
+    if (d < 1) d = 1;
+    if (d > 0xFFFFFFFFull) d = 0xFFFFFFFFull;
+    return (int64_t)d;
+}
+
+static int64_t cpu_duration(const orc_sim *S, uint32_t c)
+{
+    const orc_lane *L = &S->lane[c];
+    return (int64_t)(((uint64_t)S->in->t_cpu_nom[L->tbase + L->task] * L->Fc) >> 16);
+}
+
+static int64_t sync_cost(const orc_sim *S, uint32_t c, uint32_t i, uint32_t ord)
+{
+    const orc_input *in = S->in;
+    if (in->sync_hi_ns <= in->sync_lo_ns) return in->sync_lo_ns;
+    uint64_t span = (uint64_t)(in->sync_hi_ns - in->sync_lo_ns + 1);
+    return in->sync_lo_ns + (int64_t)(orc_word(in->seed, S->s, TAG_SYNC, c, i, ord) % span);
+}
+
+/* ---- urgency evaluation trigger (R8): Eq. 2 + AKB refresh ---- */
+static int64_t evaluate(orc_sim *S, uint32_t c, int64_t t)
+{
+    orc_lane *L = &S->lane[c];
+    const orc_input *in = S->in;
+    int64_t lax = orc_eq2_laxity(L->t_arr, L->Dp, in->k_est + L->kbase, L->N, L->launched,
+                                 in->t_cpu_est + L->tbase, L->M, L->cpu_idx, t);
+    L->T_last = t; L->L_last = lax;
+    for (uint32_t e = 0; e < L->akb_n; ++e) { L->akb[e].T = t; L->akb[e].L = lax; }
+    tr(S, t, TR_EVAL, c, L->inst, lax, L->launched);
+    return lax;
+}
+
+static int urgengo(const orc_sim *S) { return S->in->kind == ORC_URGENGO; }
+static int flag(const orc_sim *S, uint32_t f) { return urgengo(S) && (S->in->flags & f); }
+
+/* Delayed launching (R14): delay kernel K iff its
+ * utilisation is not exempt, the launching chain itself is not truly urgent,
+ * and some other chain's active kernel has a truly urgent last evaluation. */
+static int should_delay(const orc_sim *S, uint32_t c, uint32_t util, int64_t own_L)
+{
+    const orc_input *in = S->in;
+    if (util < in->util_exempt_permille) return 0;
+    if (orc_is_urgent(own_L, in->lax_threshold_ns)) return 0;
+    for (uint32_t o = 0; o < S->C; ++o) {
+        if (o == c) continue;
+        for (uint32_t e = 0; e < S->snap_n[o]; ++e)   /* every active kernel of chain o */
+            if (orc_is_urgent(S->snap_L[o], in->lax_threshold_ns)) return 1;
+    }
+    return 0;
+}
+
+/* Task-level stream binding with reservation (R15). */
+static uint32_t bind_level(orc_sim *S, uint32_t c, int64_t own_L)
+{
+    const orc_input *in = S->in;
+    if (in->kind == ORC_FIFO) return in->num_prio - 1;
+    if (in->kind == ORC_STATIC) return S->lane[c].static_level;
+    if (!(in->flags & ORC_BIND)) return in->num_prio - 1;
+    if (orc_is_urgent(own_L, in->lax_threshold_ns)) return 0;
+    int64_t keys[64]; uint32_t chains[64], ranks[64], n = 0;
+    keys[n] = orc_urgency_key(own_L); chains[n] = c; ++n;
+    for (uint32_t o = 0; o < S->C; ++o)
+        if (o != c && S->snap_n[o] > 0) { keys[n] = orc_urgency_key(S->snap_L[o]); chains[n] = o; ++n; }
+    orc_rank(keys, chains, n, ranks);
+    return orc_normalise_level(ranks[0], n, in->num_prio);
+}
+
+static void record_outcome(orc_sim *S, uint32_t c, int64_t t, int early)
+{
+    orc_lane *L = &S->lane[c];
+    const orc_input *in = S->in;
+    if (early) {
+        L->early++; L->miss++;
+        L->hash = hash_fold(hash_fold(L->hash, 0xFFFFFFFFu), 0xFFFFFFFFu);
+        tr(S, t, TR_EARLY_EXIT, c, L->inst, 0, 0);
+        return;
+    }
+    int64_t rt = t - L->t_arr;                  /* response time (R18) */
+    int late = rt > L->Dp;
+    if (late) L->miss++;
+    L->sum_rt += (uint64_t)rt;
+    L->hash = hash_fold(hash_fold(L->hash, (uint32_t)rt), (uint32_t)((uint64_t)rt >> 32));
+    int64_t bin = rt / in->rt_bin_ns;
+    if (bin > (int64_t)in->rt_bins - 1) bin = in->rt_bins - 1;
+    S->agg[(int64_t)c * (AGG_COUNTERS + in->rt_bins + RATIO_BINS) + AGG_COUNTERS + bin] += 1;
+    tr(S, t, TR_INST_DONE, c, L->inst, rt, late);
+}
+
+/* Start of the instance L->inst at time t (frame arrival, or the end of the
+ * previous instance when the chain ran late -- DESIGN.md R6). */
+static void start_instance(orc_sim *S, uint32_t c, int64_t t)
+{
+    orc_lane *L = &S->lane[c];
+    L->total++;
+    L->Fg = inst_factor(S, c, L->inst, 0, S->in->ch_gpu_sigma[c]);
+    L->Fc = inst_factor(S, c, L->inst, 1, S->in->ch_cpu_sigma[c]);
+    L->task = 0; L->launched = 0; L->cpu_idx = 0; L->done = 0; L->sync_ord = 0;
+    L->q_head = L->q_tail = 0;
+    tr(S, t, TR_INST_START, c, L->inst, L->t_arr, 0);
+}
+
+/* the chain moves on to instance inst+1 at time t; returns 1 if it starts now */
+static int next_instance(orc_sim *S, uint32_t c, int64_t t)
+{
+    orc_lane *L = &S->lane[c];
+    L->inst++;
+    L->t_arr = arrival(S, c, L->inst);
+    if (L->t_arr >= S->H) { L->pc = PC_DONE; L->cpu_next = ORC_INF; return 0; }   /* not admitted (R7) */
+    if (L->t_arr > t) { L->pc = PC_ARRIVE; L->cpu_next = L->t_arr; return 0; }
+    L->pc = PC_ARRIVE; L->cpu_next = t;
+    return 1;
+}
+
+static void issue_sync(orc_sim *S, uint32_t c, int64_t t, uint32_t target)
+{
+    orc_lane *L = &S->lane[c];
+    L->sync_target = target;
+    L->sync_cost = sync_cost(S, c, L->inst, L->sync_ord++);
+    tr(S, t, TR_SYNC_CALL, c, L->inst, target, L->sync_cost);
+    if (L->done >= target) { L->pc = PC_SYNC_RET; L->cpu_next = t + L->sync_cost; }
+    else { L->pc = PC_SYNC_WAIT; L->cpu_next = ORC_INF; }
+}
+
+static uint32_t task_first_kernel(const orc_sim *S, uint32_t c)
+{
+    const orc_lane *L = &S->lane[c];
+    uint32_t k = 0;
+    for (uint32_t j = 0; j < L->task; ++j) k += S->in->t_nk[L->tbase + j];
+    return k;
+}
+
+/* One CPU step of chain c at time t (R21 Phase B): the thread runs
+ * its program until it must wait for time to pass or for the GPU. */
+static void lane_step(orc_sim *S, uint32_t c, int64_t t)
+{
+    orc_lane *L = &S->lane[c];
+    const orc_input *in = S->in;
+    for (;;) {
+        switch (L->pc) {
+        case PC_ARRIVE: {
+            start_instance(S, c, t);
+            goto task_start;
+        }
+        task_start: {
+            /* a new CPU segment starts: evaluate, early exit */
+            tr(S, t, TR_TASK_START, c, L->inst, L->task, 0);
+            if (urgengo(S)) {
+                int64_t lax = evaluate(S, c, t);
+                if (flag(S, ORC_EARLY_EXIT) && lax < 0) {
+                    L->akb_n = 0;                          /* purge the chain's AKB entries */
+                    record_outcome(S, c, t, 1);
+                    if (next_instance(S, c, t)) continue;
+                    return;
+                }
+            }
+            int64_t e = cpu_duration(S, c);
+            L->pc = PC_CPU_DONE; L->cpu_next = t + e;
+            if (e > 0) return;
+            continue;
+        }
+        case PC_CPU_DONE:
+        case PC_ATTEMPT: {
+            /* launch attempt for kernel n = L->launched */
+            uint32_t n = L->launched;
+            int64_t lax = 0;
+            if (urgengo(S)) lax = evaluate(S, c, t);
+            if (flag(S, ORC_DELAY) && should_delay(S, c, in->k_util[L->kbase + n], lax)) {
+                tr(S, t, TR_DELAY, c, L->inst, n, 0);
+                L->pc = PC_ATTEMPT; L->cpu_next = t + in->sleep_ns;
+                return;
+            }
+            if (n == task_first_kernel(S, c)) {          /* first kernel of the task: bind */
+                L->level = bind_level(S, c, lax);
+                tr(S, t, TR_BIND, c, L->inst, L->level, n);
+            }
+            int64_t busy = in->launch_ns + (urgengo(S) ? in->launch_akb_ns : 0);
+            L->pc = PC_ENQUEUE; L->cpu_next = t + busy;
+            if (busy > 0) return;
+            continue;
+        }
+        case PC_ENQUEUE: {
+            uint32_t n = L->launched;
+            uint32_t first = task_first_kernel(S, c);
+            uint32_t end = first + in->t_nk[L->tbase + L->task];
+            /* the kernel reaches its stream (R16) */
+            if (L->q_head == L->q_tail) { L->head_running = 0; L->head_ready = t; }
+            L->q[L->q_tail].K = n; L->q[L->q_tail].t_enq = t; L->q_tail++;
+            L->launched++; L->launches++; S->launches++;
+            if (urgengo(S)) {                            /* updateAKB: a new active kernel */
+                orc_akb_entry *a = &L->akb[L->akb_n++];
+                a->K = n; a->U = in->k_util[L->kbase + n]; a->S = L->level; a->C = c;
+                a->T = L->T_last; a->L = L->L_last;
+            }
+            tr(S, t, TR_ENQUEUE, c, L->inst, n, L->level);
+            int last = (L->launched == end);
+            if (last) L->cpu_idx++;
+            uint32_t est = in->k_est[L->kbase + n];
+            if (n == first) { L->acc = 0; L->batch_start = first; }
+            switch (in->sync_mode) {
+            case ORC_ASYNC:
+                if (last) { issue_sync(S, c, t, L->launched); return; }
+                break;
+            case ORC_EACH:
+                issue_sync(S, c, t, L->launched); return;
+            case ORC_BATCHED: {
+                int closes = orc_batch_add(&L->acc, est, in->delta_eval_ns);
+                if (closes || last) { L->acc = 0; issue_sync(S, c, t, L->launched); return; }
+                break;
+            }
+            case ORC_OVERLAP: {
+                int closes = orc_batch_add(&L->acc, est, in->delta_eval_ns);
+                if (last) { L->acc = 0; issue_sync(S, c, t, L->launched); return; }
+                if (closes) {
+                    uint32_t prev_batch_end = L->batch_start;   /* wait for the previous batch */
+                    L->batch_start = L->launched;
+                    if (prev_batch_end == first) {             /* the task's first close: no sync */
+                        tr(S, t, TR_FREE_CLOSE, c, L->inst, L->launched, 0);
+                        if (urgengo(S)) evaluate(S, c, t);
+                        break;
+                    }
+                    issue_sync(S, c, t, prev_batch_end);
+                    return;
+                }
+                break;
+            }
+            }
+            L->pc = PC_ATTEMPT;                          /* next kernel, same time */
+            continue;
+        }
+        case PC_SYNC_RET: {
+            /* the synchronisation returned: covered kernels leave the AKB */
+            uint32_t keep = 0;
+            for (uint32_t e = 0; e < L->akb_n; ++e)
+                if (L->akb[e].K >= L->sync_target) L->akb[keep++] = L->akb[e];
+            L->akb_n = keep;
+            tr(S, t, TR_SYNC_RET, c, L->inst, L->sync_target, 0);
+            if (urgengo(S)) evaluate(S, c, t);            /* periodic evaluation */
+            uint32_t end = task_first_kernel(S, c) + in->t_nk[L->tbase + L->task];
+            if (L->launched < end) { L->pc = PC_ATTEMPT; continue; }
+            L->task++;
+            if (L->task < L->M) goto task_start;
+            record_outcome(S, c, t, 0);                  /* instance complete (R18) */
+            if (next_instance(S, c, t)) continue;
+            return;
+        }
+        default:
+            return;
+        }
+    }
+}
+
+/* Phase C: GPU dispatch of waiting stream heads (R20). */
+typedef struct { uint32_t level; int64_t ready; uint32_t chain; } orc_cand;
+
+static int orc_cand_cmp(const void *a, const void *b)
+{
+    const orc_cand *x = a, *y = b;
+    if (x->level != y->level) return x->level < y->level ? -1 : 1;
+    if (x->ready != y->ready) return x->ready < y->ready ? -1 : 1;
+    return x->chain < y->chain ? -1 : (x->chain > y->chain);
+}
+
+static void dispatch(orc_sim *S, int64_t t)
+{
+    orc_cand cand[64];
+    uint32_t n = 0;
+    for (uint32_t c = 0; c < S->C; ++c) {
+        orc_lane *L = &S->lane[c];
+        if (L->q_head < L->q_tail && !L->head_running) {
+            cand[n].level = L->level; cand[n].ready = L->head_ready; cand[n].chain = c; ++n;
+        }
+    }
+    qsort(cand, n, sizeof(orc_cand), orc_cand_cmp);
+    for (uint32_t j = 0; j < n; ++j) {
+        orc_lane *L = &S->lane[cand[j].chain];
+        uint32_t K = L->q[L->q_head].K;
+        uint32_t u = S->in->k_util[L->kbase + K];
+        if (S->gpu_used + u > 1000) continue;            /* does not fit: skip (greedy) */
+        S->gpu_used += u;
+        L->head_running = 1;
+        L->head_end = t + kernel_duration(S, cand[j].chain, L->inst, K);
+        tr(S, t, TR_DISPATCH, cand[j].chain, L->inst, K, L->head_end);
+    }
+}
+
+/* Phase A: retire every kernel ending at t (R21). */
+static void retire(orc_sim *S, int64_t t)
+{
+    for (uint32_t c = 0; c < S->C; ++c) {
+        orc_lane *L = &S->lane[c];
+        if (!(L->q_head < L->q_tail && L->head_running && L->head_end == t)) continue;
+        uint32_t K = L->q[L->q_head].K;
+        S->gpu_used -= S->in->k_util[L->kbase + K];
+        L->q_head++; L->done++; L->head_running = 0;
+        if (L->q_head < L->q_tail) L->head_ready = t;    /* next kernel becomes head */
+        tr(S, t, TR_RETIRE, c, L->inst, K, 0);
+        if (L->pc == PC_SYNC_WAIT && L->done >= L->sync_target) {
+            L->pc = PC_SYNC_RET; L->cpu_next = t + L->sync_cost;
+        }
+    }
+}
+
+static void cal_sample(orc_sim *S)
+{
+    /* highest urgency among all active kernels of the AKB */
+    int have = 0; int64_t best = 0, bestL = 0;
+    for (uint32_t c = 0; c < S->C; ++c) {
+        orc_lane *L = &S->lane[c];
+        for (uint32_t e = 0; e < L->akb_n; ++e) {
+            int64_t k = orc_urgency_key(L->akb[e].L);
+            if (!have || k > best) { best = k; bestL = L->akb[e].L; have = 1; }
+        }
+    }
+    if (!have || bestL < 0) return;                      /* skip empty / negative (Q5) */
+    if (S->cal_n < S->cal_cap) S->cal_L[S->cal_n++] = bestL;
+}
+
+/* Simulate scenario s.  Returns 0 on success. */
+static int sim_scenario(const orc_input *in, uint64_t s, uint32_t *rec, int64_t *agg,
+                        int64_t *trace, int64_t trace_cap, int64_t *trace_len,
+                        int64_t *cal_L, int64_t cal_cap, int64_t *cal_n, int64_t cal_end)
+{
+    orc_sim S;
+    memset(&S, 0, sizeof S);
+    S.in = in; S.s = s; S.C = in->num_chains; S.agg = agg;
+    S.trace = trace; S.trace_cap = trace_cap; S.trace_len = trace_len ? *trace_len : 0;
+    S.cal_L = cal_L; S.cal_cap = cal_cap; S.cal_n = 0; S.cal_end = cal_end; S.cal_next = 0;
+    S.lane = calloc(S.C, sizeof(orc_lane));
+    S.snap_L = calloc(S.C, sizeof(int64_t));
+    S.snap_n = calloc(S.C, sizeof(uint32_t));
+    uint32_t kb = 0, tb = 0;
+    for (uint32_t c = 0; c < S.C; ++c) {
+        orc_lane *L = &S.lane[c];
+        L->tbase = tb; L->kbase = kb; L->M = in->ch_ntasks[c]; L->N = 0;
+        for (uint32_t j = 0; j < L->M; ++j) L->N += in->t_nk[tb + j];
+        tb += L->M; kb += L->N;
+        L->akb = calloc(L->N, sizeof(orc_akb_entry));
+        L->q = calloc(L->N, sizeof(orc_stream_entry));
+        L->hash = 2166136261u;
+    }
+    /* scenario factors (R3): P' = P / f_a, D' = D * f_d, tight set halved */
+    uint32_t tight = 0;
+    if (in->tight_explicit) tight = in->tight_mask;
+    else if (in->ftight_permille) {
+        uint32_t n_tight = (in->ftight_permille * S.C + 999) / 1000;
+        for (uint32_t c = 0; c < S.C; ++c) {
+            uint32_t wc = orc_word(in->seed, s, TAG_TIGHT, c, 0, 0), rank = 0;
+            for (uint32_t o = 0; o < S.C; ++o) {
+                uint32_t wo = orc_word(in->seed, s, TAG_TIGHT, o, 0, 0);
+                if (wo < wc || (wo == wc && o < c)) ++rank;
+            }
+            if (rank < n_tight) tight |= 1u << c;
+        }
+    }
+    int64_t maxD = 0;
+    for (uint32_t c = 0; c < S.C; ++c) {
+        orc_lane *L = &S.lane[c];
+        L->Pp = in->ch_period[c] * (int64_t)in->fa_den / (int64_t)in->fa_num;
+        L->Dp = in->ch_deadline[c] * (int64_t)in->fd_num / (int64_t)in->fd_den;
+        if (tight & (1u << c)) L->Dp /= 2;
+        if (L->Dp > maxD) maxD = L->Dp;
+    }
+    /* STATIC (PAAM-like) levels: rank by D' ascending, ties by chain id (R15) */
+    for (uint32_t c = 0; c < S.C; ++c) {
+        uint32_t r = 1;
+        for (uint32_t o = 0; o < S.C; ++o)
+            if (S.lane[o].Dp < S.lane[c].Dp || (S.lane[o].Dp == S.lane[c].Dp && o < c)) ++r;
+        S.lane[c].static_level = (S.C <= 1 || in->num_prio <= 1) ? 0
+            : (uint32_t)(((uint64_t)(r - 1) * (in->num_prio - 1)) / (S.C - 1));
+    }
+    S.H = in->horizon_ns;
+    S.H_stop = S.H + maxD;                               /* R7 */
+    for (uint32_t c = 0; c < S.C; ++c) {
+        orc_lane *L = &S.lane[c];
+        L->inst = 0;
+        L->t_arr = arrival(&S, c, 0);
+        if (L->t_arr < S.H) { L->pc = PC_ARRIVE; L->cpu_next = L->t_arr; }
+        else { L->pc = PC_DONE; L->cpu_next = ORC_INF; }
+    }
+    /* main loop (R21) */
+    for (;;) {
+        int64_t t = ORC_INF;
+        for (uint32_t c = 0; c < S.C; ++c) {
+            orc_lane *L = &S.lane[c];
+            if (L->cpu_next < t) t = L->cpu_next;
+            if (L->q_head < L->q_tail && L->head_running && L->head_end < t) t = L->head_end;
+        }
+        if (S.cal_L) {
+            while (S.cal_next < S.cal_end && S.cal_next < t) { cal_sample(&S); S.cal_next += 1000000; }
+        }
+        if (t > S.H_stop) break;
+        S.steps++;
+        tr(&S, t, TR_STEP, -1, -1, 0, 0);
+        retire(&S, t);                                                   /* Phase A */
+        for (uint32_t c = 0; c < S.C; ++c) { S.snap_L[c] = S.lane[c].L_last; S.snap_n[c] = S.lane[c].akb_n; }
+        for (uint32_t c = 0; c < S.C; ++c)                               /* Phase B */
+            if (S.lane[c].cpu_next == t) lane_step(&S, c, t);
+        dispatch(&S, t);                                                 /* Phase C */
+    }
+    /* end of horizon (R7): admitted, unfinished instances are misses */
+    const uint32_t stride = AGG_COUNTERS + in->rt_bins + RATIO_BINS;
+    for (uint32_t c = 0; c < S.C; ++c) {
+        orc_lane *L = &S.lane[c];
+        uint32_t first_unstarted = L->inst;
+        if (L->pc != PC_ARRIVE && L->pc != PC_DONE) { L->unfin++; first_unstarted = L->inst + 1; }
+        if (L->pc != PC_DONE)
+            for (uint32_t i = first_unstarted; arrival(&S, c, i) < S.H; ++i) { L->unfin++; L->total++; }
+        L->miss += L->unfin;
+        uint32_t *r = rec + (uint64_t)c * REC_WORDS;
+        r[0] = L->total; r[1] = L->miss; r[2] = L->early; r[3] = L->unfin;
+        r[4] = L->launches; r[5] = L->hash;
+        r[6] = (uint32_t)L->sum_rt; r[7] = (uint32_t)(L->sum_rt >> 32);
+        int64_t *a = agg + (int64_t)c * stride;
+        a[0] += L->total; a[1] += L->miss; a[2] += L->early; a[3] += L->unfin; a[4] += (int64_t)L->sum_rt;
+        if (L->total) a[AGG_COUNTERS + in->rt_bins + (uint64_t)100 * L->miss / L->total] += 1;
+        free(L->akb); free(L->q);
+    }
+    agg[(int64_t)S.C * stride + 0] += S.launches;
+    agg[(int64_t)S.C * stride + 1] += S.steps;
+    if (trace_len) *trace_len = S.trace_len;
+    if (cal_n) *cal_n = S.cal_n;
+    free(S.lane); free(S.snap_L); free(S.snap_n);
+    return 0;
+}
+
+/* Simulate scenarios [scenario_begin, scenario_begin + scenario_count).
+ * records: [count][C][8] u32; agg: int64 words (accumulated, caller zeroes);
+ * trace (optional): [cap][6] int64 (t, kind, chain, instance, a, b). */
+int orc_run(const orc_input *in, uint32_t *records, int64_t *agg,
+            int64_t *trace, int64_t trace_cap, int64_t *trace_len)
+{
+    if (!in || in->num_chains == 0 || in->num_chains > 32) return -1;
+    if (in->fa_num == 0 || in->fa_den == 0 || in->fd_den == 0 || in->rt_bins == 0 || in->rt_bin_ns <= 0) return -1;
+    for (uint32_t c = 0; c < in->num_chains; ++c)     /* arrivals strictly increasing: P' > J (R3) */
+        if (in->ch_period[c] * (int64_t)in->fa_den / (int64_t)in->fa_num <= in->jitter_ns) return -2;
+    if (trace_len) *trace_len = 0;
+    for (uint64_t j = 0; j < in->scenario_count; ++j) {
+        uint32_t *rec = records + j * (uint64_t)in->num_chains * REC_WORDS;
+        int rc = sim_scenario(in, in->scenario_begin + j, rec, agg, trace, trace_cap, trace_len, 0, 0, 0, 0);
+        if (rc) return rc;
+    }
+    return 0;
+}
+
+/* TH_urgent from recorded maximum urgencies: the
+ * nearest-rank pct-th percentile of UL = 1/L over the samples, returned as its
+ * laxity L_th (UL >= TH <=> 0 <= L <= L_th).  Samples with L < 0 are skipped
+ * (SPEC.md:328-330).  Sorts L[] in place by ascending urgency.  -1 if empty.
+ * DESIGN.md Q5 states the rank reading. */
+int64_t orc_nearest_rank_lth(int64_t *L, int64_t n, int64_t pct)
+{
+    int64_t m = 0;
+    for (int64_t i = 0; i < n; ++i) if (L[i] >= 0) L[m++] = L[i];
+    if (m == 0) return -1;
+    for (int64_t i = 1; i < m; ++i) {                 /* insertion sort by urgency key, plain */
+        int64_t ll = L[i], kk = orc_urgency_key(ll), j = i - 1;
+        while (j >= 0 && orc_urgency_key(L[j]) > kk) { L[j + 1] = L[j]; --j; }
+        L[j + 1] = ll;
+    }
+    /* rank floor(pct/100 * m) + 1 in ascending urgency: the smallest sample with
+     * more than pct % of the samples below it, so that UL >= TH holds for the top
+     * (100 - pct) % only (SPEC.md:328 example: {0.01 x95, 0.05 x5} -> 0.05). */
+    int64_t k = (pct * m) / 100 + 1;
+    if (k > m) k = m;
+    return L[k - 1];
+}
+
+/* TH_urgent calibration (Q5): run scenario
+ * scenario_begin with the threshold disabled (L_th = -1), record every 1 ms of
+ * the first min(H, window) the highest urgency among the AKB's active kernels,
+ * and return the laxity of the nearest-rank 95th percentile of those urgencies.
+ * *n_samples receives the number of samples; returns -1 if there were none. */
+int64_t orc_calibrate(const orc_input *in_, int64_t window_ns, int64_t *n_samples)
+{
+    orc_input in = *in_;
+    in.lax_threshold_ns = -1;
+    in.scenario_count = 1;
+    int64_t end = in.horizon_ns < window_ns ? in.horizon_ns : window_ns;
+    int64_t cap = end / 1000000 + 2;
+    int64_t *L = calloc(cap, sizeof(int64_t));
+    int64_t n = 0;
+    uint32_t *rec = calloc((size_t)in.num_chains * REC_WORDS, sizeof(uint32_t));
+    int64_t *agg = calloc((size_t)in.num_chains * (AGG_COUNTERS + in.rt_bins + RATIO_BINS) + 2, sizeof(int64_t));
+    sim_scenario(&in, in.scenario_begin, rec, agg, 0, 0, 0, L, cap, &n, end);
+    int64_t out = orc_nearest_rank_lth(L, n, 95);
+    if (n_samples) *n_samples = n;
+    free(L); free(rec); free(agg);
+    return out;
+}

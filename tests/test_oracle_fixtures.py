@@ -1,0 +1,152 @@
+"""The oracle against hand-worked timelines (tests/golden/w*.json) and single-chain
+closed forms.  The expected values were derived by hand from the paper's
+mechanisms (DESIGN.md Model M0), not by running any simulator."""
+import json
+import os
+import random
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from workloads import w1, w2, w3
+from workloads.spec import (FIFO, MS, REC_EARLY, REC_LAUNCH, REC_MISS, REC_SUMRT_HI, REC_SUMRT_LO,
+                            REC_TOTAL, SYNC_ASYNC, SYNC_BATCHED, SYNC_EACH, SYNC_OVERLAP, URGENGO,
+                            F_EARLY_EXIT, Batch, Chain, Kernel, Policy, Task, Workload)
+
+from .conftest import GOLDEN
+
+
+def _gold(name):
+    with open(os.path.join(GOLDEN, name)) as f:
+        return json.load(f)
+
+
+def _sum_rt(rec):
+    return int(rec[REC_SUMRT_LO]) | (int(rec[REC_SUMRT_HI]) << 32)
+
+
+@pytest.mark.parametrize("case", _gold("w1.json")["cases"], ids=lambda c: c["policy"])
+def test_w1_two_chain_timelines(case):
+    p = Policy(kind=case["kind"], flags=case["flags"], sync_mode=SYNC_ASYNC, lax_threshold_ns=5 * MS)
+    r = O.run(w1(), p, Batch(horizon_ns=1 * MS))
+    rec = r.records[0]
+    for c in range(2):
+        assert rec[c, REC_TOTAL] == 1
+        assert _sum_rt(rec[c]) == int(round(case["rt_ms"][c] * MS))
+        assert rec[c, REC_MISS] == case["miss"][c]
+    eq3 = O.overall_miss_ratio(rec[:, REC_MISS], rec[:, REC_TOTAL])
+    assert eq3 == case["eq3"]
+    assert r.launches == case["launches"]
+
+
+def test_w1_laxities_in_trace():
+    """The EVAL trace entries carry Eq. 2 laxities 2 ms / 4 ms (chain A at t = 1 ms) and 92 ms (B at 1.5 ms)."""
+    g = _gold("w1.json")["laxities_ms"]
+    p = Policy(kind=URGENGO, flags=3, sync_mode=SYNC_ASYNC, lax_threshold_ns=5 * MS)
+    r = O.run(w1(), p, Batch(horizon_ns=1 * MS), trace_cap=1000)
+    ev = [(int(t), int(c), int(a)) for t, k, c, i, a, b in r.trace if k == O.TRACE_CODES["EVAL"]]
+    assert (1 * MS, 0, int(g["A_attempt_k0_t1"] * MS)) in ev
+    assert (1 * MS, 0, int(g["A_attempt_k1_t1"] * MS)) in ev
+    assert (1_500_000, 1, int(g["B_attempt_k0_t1.5"] * MS)) in ev
+
+
+@pytest.mark.parametrize("mode", ["ASYNC", "OVERLAP", "BATCHED", "EACH"])
+def test_w2_sync_modes(mode):
+    g = _gold("w2.json")
+    p = Policy(kind=URGENGO, flags=0, sync_mode=g["sync_mode"][mode], lax_threshold_ns=-1)
+    r = O.run(w2(), p, Batch(horizon_ns=1 * MS))
+    assert _sum_rt(r.records[0, 0]) == int(round(g["rt_ms"][mode] * MS))
+    assert r.launches == 8
+
+
+def test_w3_early_exit():
+    g = _gold("w3.json")
+    r = O.run(w3(), Policy(kind=URGENGO, flags=F_EARLY_EXIT, sync_mode=SYNC_ASYNC), Batch(horizon_ns=1 * MS),
+              trace_cap=200)
+    e = g["urgengo_early_exit"]
+    rec = r.records[0, 0]
+    assert (rec[REC_TOTAL], rec[REC_MISS], rec[REC_EARLY], rec[REC_LAUNCH]) == (e["total"], e["miss"], e["early"],
+                                                                               e["launches"])
+    evals = [int(a) for t, k, c, i, a, b in r.trace if k == O.TRACE_CODES["TASK_START"] or k == O.TRACE_CODES["EVAL"]]
+    assert int(e["L_task0_ms"] * MS) in evals and int(e["L_task1_ms"] * MS) in evals
+    f = g["fifo"]
+    r = O.run(w3(), Policy(kind=FIFO, flags=0, sync_mode=SYNC_ASYNC), Batch(horizon_ns=1 * MS))
+    rec = r.records[0, 0]
+    assert (rec[REC_TOTAL], rec[REC_MISS], rec[REC_EARLY], rec[REC_LAUNCH]) == (f["total"], f["miss"], f["early"],
+                                                                               f["launches"])
+    assert _sum_rt(rec) == int(round(f["rt_ms"] * MS))
+
+
+# ---------------------------------------------------------------------------
+# Single-chain closed form (max-plus recurrence), independent of the event loop
+# ---------------------------------------------------------------------------
+
+def closed_form_rt(tasks, lam, sigma, mode, delta):
+    """Response time of one instance of one chain running alone (no contention).
+
+    Per task: CPU segment, then launches of lam each; kernel k becomes available at
+    e_k (end of its launch call); it starts at max(e_k, f_{k-1}) and ends f_k = start + d_k.
+    A synchronisation called at c waiting for kernels < j returns at max(c, f_{j-1}) + sigma.
+    (R16-R17.)"""
+    t = 0
+    f_prev = 0          # completion of the previous kernel on the stream
+    for cpu, kernels in tasks:
+        t += cpu
+        first_close = True
+        acc = 0
+        f = []          # completion times of this task's kernels
+        batch_start = 0
+        for k, (d, est) in enumerate(kernels):
+            t += lam                            # launch call
+            start = max(t, f_prev)
+            f_prev = start + d
+            f.append(f_prev)
+            last = k == len(kernels) - 1
+            if mode == SYNC_EACH or (mode == SYNC_ASYNC and last):
+                t = max(t, f[k]) + sigma
+                continue
+            if mode == SYNC_BATCHED:
+                acc += est
+                if acc >= delta or last:
+                    acc = 0
+                    t = max(t, f[k]) + sigma
+                continue
+            if mode == SYNC_OVERLAP:
+                acc += est
+                if last:
+                    t = max(t, f[k]) + sigma
+                elif acc >= delta:
+                    acc = 0
+                    if batch_start > 0:
+                        t = max(t, f[batch_start - 1]) + sigma
+                    batch_start = k + 1
+    return t
+
+
+@pytest.mark.parametrize("mode", [SYNC_ASYNC, SYNC_EACH, SYNC_BATCHED, SYNC_OVERLAP])
+def test_single_chain_closed_form(mode):
+    rng = random.Random(100 + mode)
+    for trial in range(60):
+        ntask = rng.randint(1, 3)
+        tasks, spec = [], []
+        for _ in range(ntask):
+            cpu = rng.choice([0, rng.randint(1, 3 * MS)])
+            ks = []
+            for _ in range(rng.randint(1, 12)):
+                d = rng.randint(1, 400_000)
+                est = rng.choice([d, rng.randint(1, 400_000)])
+                ks.append((d, est))
+            tasks.append((cpu, ks))
+            spec.append(Task(cpu, cpu, [Kernel(d, e, rng.choice([50, 400, 1000])) for d, e in ks]))
+        lam = rng.choice([0, 1000, 21_672, 200_000])
+        sigma = rng.choice([0, 10_000, 50_000])
+        delta = rng.choice([1, 300_000, 500_000, 10**9])
+        w = Workload(chains=[Chain(10_000 * MS, 5_000 * MS, 0, spec)], launch_ns=lam, launch_akb_ns=0,
+                     sync_lo_ns=sigma, sync_hi_ns=sigma, jitter_ns=0)
+        expect = closed_form_rt(tasks, lam, sigma, mode, delta)
+        # policy independence of a lone chain with lambda_akb = 0
+        for kind, flags in [(FIFO, 0), (1, 0), (URGENGO, 1), (URGENGO, 3)]:
+            p = Policy(kind=kind, flags=flags, sync_mode=mode, delta_eval_ns=delta, lax_threshold_ns=MS)
+            r = O.run(w, p, Batch(horizon_ns=1))
+            assert _sum_rt(r.records[0, 0]) == expect, (trial, kind, flags)

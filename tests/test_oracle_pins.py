@@ -1,0 +1,230 @@
+"""Pins of the oracle's pure functions against what the paper and mathematics fix.
+
+Each test names the passage it checks.  None of them re-types the oracle's
+formula: they compare with printed values, exact rational arithmetic, or
+brute force.
+"""
+import csv
+import os
+import random
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from workloads.spec import MS
+from workloads.templates import TABLE2, paper11
+
+from .conftest import GOLDEN
+
+
+def _table2():
+    rows = []
+    with open(os.path.join(GOLDEN, "table2.csv")) as f:
+        for r in csv.DictReader(l for l in f if not l.startswith("#")):
+            rows.append({k: float(v) for k, v in r.items()})
+    return rows
+
+
+def test_philox_known_answers():
+    """Philox4x32-10 KAT vectors (Random123, SC'11) -- the oracle's own RNG copy."""
+    n = 0
+    for line in open(os.path.join(GOLDEN, "philox_kat.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        v = [int(x, 16) for x in line.split()]
+        assert O.philox(v[:4], v[4:6]).tolist() == v[6:]
+        n += 1
+    assert n == 3
+
+
+@pytest.mark.parametrize("row", range(10))
+def test_table2_urgency_truncated(row):
+    """Eq. 2 at t = t_arr, I~gpu = I~cpu = 0 reproduces Table 2's
+    urgency column for C0-C9 when 1/L is truncated to 4 decimals."""
+    r = _table2()[row]
+    D = int(round(r["D_ms"] * MS))
+    egpu = int(round(r["Egpu_ms"] * MS))
+    ecpu = int(round(r["Ecpu_ms"] * MS))
+    L = O.eq2_laxity(0, D, [egpu], 0, [ecpu], 0, 0)
+    assert L == D - egpu - ecpu
+    ul_1e4 = (10_000 * 1_000_000) // L          # floor(1e4 * UL[1/ms]) with L in ns -- exact integers
+    assert ul_1e4 == int(round(r["UL_printed"] * 10_000))
+
+
+def test_table2_c10_is_not_eq2():
+    """C10's printed 0.0050 is 1/200, not Eq. 2 (Q18): documented mismatch."""
+    r = _table2()[10]
+    L = O.eq2_laxity(0, 200 * MS, [int(6.7 * MS)], 0, [int(17.8 * MS)], 0, 0)
+    assert (10_000 * 1_000_000) // L == 56 != int(round(r["UL_printed"] * 10_000))
+
+
+def test_table2_priority_ranks():
+    """Ranking C0-C10 by urgency gives Table 2's PRI column for
+    every chain but the exact C2/C7 tie (both L = 72.0 ms), which the paper orders
+    7-before-2 against the smaller-id tie-break of C3/C5 and C4/C6 (Q7:
+    parity unpinned for that pair)."""
+    rows = _table2()
+    keys, chains = [], []
+    for r in rows:
+        L = O.eq2_laxity(0, int(round(r["D_ms"] * MS)), [int(round(r["Egpu_ms"] * MS))], 0,
+                         [int(round(r["Ecpu_ms"] * MS))], 0, 0)
+        keys.append(O.urgency_key(L)); chains.append(int(r["chain"]))
+    ranks = O.rank(keys, chains)
+    printed = [int(r["PRI_printed"]) for r in rows]
+    for c in range(11):
+        if c in (2, 7):
+            continue
+        assert ranks[c] == printed[c], c
+    assert {int(ranks[2]), int(ranks[7])} == {printed[2], printed[7]} == {4, 5}
+
+
+def test_eq2_template_sums_match_table2():
+    """Eq. 2's literal sums over the paper11 template's kernels and CPU segments
+    equal Table 2's E^gpu_C and E^cpu_C (the template is built from them)."""
+    w = paper11()
+    for c, ch in enumerate(w.chains):
+        est = [k.estimate_ns for t in ch.tasks for k in t.kernels]
+        cpu = [t.cpu_estimate_ns for t in ch.tasks]
+        L = O.eq2_laxity(0, ch.deadline_ns, est, 0, cpu, 0, 0)
+        _, D, ecpu, _, egpu, _, _ = TABLE2[c]
+        assert L == D * MS - int(round(ecpu * MS)) - int(round(egpu * MS))
+
+
+def test_eq1_is_eq2_without_cpu_and_monotone():
+    """Eq. 1 is Eq. 2 with no CPU terms; L strictly decreases in t
+    and never decreases when I~gpu advances."""
+    rng = random.Random(1)
+    for _ in range(200):
+        n = rng.randint(1, 20)
+        est = [rng.randint(1, 10**6) for _ in range(n)]
+        D, ta = rng.randint(1, 10**9), rng.randint(0, 10**9)
+        t = ta + rng.randint(0, 10**9)
+        k = rng.randint(0, n)
+        eq1 = ta + D - sum(est[k:]) - t
+        assert O.eq2_laxity(ta, D, est, k, [], 0, t) == eq1
+        assert O.eq2_laxity(ta, D, est, k, [0, 0], 0, t) == eq1
+        assert O.eq2_laxity(ta, D, est, k, [], 0, t + 1) < O.eq2_laxity(ta, D, est, k, [], 0, t)
+        if k < n:
+            assert O.eq2_laxity(ta, D, est, k + 1, [], 0, t) >= O.eq2_laxity(ta, D, est, k, [], 0, t)
+
+
+def _ul(L):
+    return Fraction(10**30) if L == 0 else Fraction(1, L)   # L = 0 saturates to +inf
+
+
+def test_urgency_key_orders_like_reciprocal():
+    """key(L) orders exactly as UL = 1/L, with L = 0 as +infinity (R9; exact rationals)."""
+    rng = random.Random(7)
+    vals = [0, 1, -1, 2, -2, 10**12, -10**12, 5 * 10**17, -5 * 10**17]
+    vals += [rng.randint(-10**15, 10**15) for _ in range(300)]
+    for a in vals:
+        for b in vals[:60]:
+            ka, kb = O.urgency_key(a), O.urgency_key(b)
+            ua, ub = _ul(a), _ul(b)
+            assert (ka > kb) == (ua > ub) and (ka == kb) == (ua == ub), (a, b)
+
+
+def test_urgent_threshold_inclusive():
+    """UL >= TH_urgent (R10 / Q4) with TH = 1/L_th."""
+    lth = 5 * MS
+    for L in [-1, 0, 1, lth - 1, lth, lth + 1, 10**12]:
+        expect = L >= 0 and _ul(L) >= Fraction(1, lth)
+        assert O.is_urgent(L, lth) == expect, L
+
+
+def test_normalise_level_spec_examples():
+    """n_r = 4, NUM_PRI = 6: rank 1 -> level 1, rank 4 -> level 5;
+    empty AKB (n_r = 1) -> middle level ceil((NUM_PRI-1)/2) = 3."""
+    assert O.normalise_level(1, 4, 6) == 1
+    assert O.normalise_level(4, 4, 6) == 5
+    assert O.normalise_level(1, 1, 6) == 3
+    # NUM_PRI = 2: only the reserved level 0 and level 1 exist
+    assert O.normalise_level(1, 3, 2) == 1 and O.normalise_level(3, 3, 2) == 1
+
+
+def test_normalise_level_range_and_order():
+    """Every normalised level lies in 1..NUM_PRI-1 and is non-decreasing in rank, using
+    the top and bottom levels at the extremes ("normalize ... to (1, NUM_PRI-1)")."""
+    for P in range(3, 9):
+        for n in range(2, 33):
+            lv = [O.normalise_level(r, n, P) for r in range(1, n + 1)]
+            assert lv[0] == 1 and lv[-1] == P - 1
+            assert all(1 <= x <= P - 1 for x in lv) and lv == sorted(lv)
+
+
+def test_rank_brute_force():
+    """Rank = 1 + number of strictly more urgent members (ties: smaller chain id), on random multisets."""
+    rng = random.Random(3)
+    for _ in range(2000):
+        n = rng.randint(1, 12)
+        Ls = [rng.choice([0, rng.randint(-5, 5), rng.randint(-10**6, 10**6)]) for _ in range(n)]
+        chains = rng.sample(range(32), n)
+        r = O.rank([O.urgency_key(L) for L in Ls], chains)
+        for i in range(n):
+            better = sum(1 for j in range(n) if _ul(Ls[j]) > _ul(Ls[i]) or
+                         (_ul(Ls[j]) == _ul(Ls[i]) and chains[j] < chains[i]))
+            assert r[i] == 1 + better
+
+
+def test_plan_batches_spec_examples():
+    """[0.2,0.2,0.2,0.4] ms, Delta 0.5 -> [k0..k2],[k3];
+    one 10 ms kernel -> one batch; 100 x 0.01 ms -> batches of 50."""
+    d = 500_000
+    assert O.plan_batches([200_000, 200_000, 200_000, 400_000], d).tolist() == [0, 0, 1, 0]
+    assert O.plan_batches([10 * MS], d).tolist() == [1]
+    c = O.plan_batches([10_000] * 100, d)
+    assert np.flatnonzero(c).tolist() == [49, 99]
+
+
+def test_plan_batches_brute_force():
+    """Batch members are exactly the shortest prefixes whose estimated sum reaches Delta_eval."""
+    rng = random.Random(11)
+    for _ in range(3000):
+        n = rng.randint(1, 40)
+        est = [rng.randint(1, 300_000) for _ in range(n)]
+        delta = rng.randint(1, 1_000_000)
+        closes = O.plan_batches(est, delta)
+        start = 0
+        for k in range(n):
+            s = sum(est[start:k + 1])
+            assert bool(closes[k]) == (s >= delta)
+            if closes[k]:
+                start = k + 1
+
+
+def test_eq3_overall_miss_ratio():
+    """Eq. 3: unweighted mean of per-chain ratios; SPEC.md:566 example
+    1/10 and 3/10 -> 0.2; chains without instances are left out (R22)."""
+    assert O.overall_miss_ratio([1, 3], [10, 10]) == pytest.approx(0.2, abs=0)
+    assert O.overall_miss_ratio([1, 3, 0], [10, 10, 0]) == pytest.approx(0.2, abs=0)
+    assert O.overall_miss_ratio([0], [0]) == 0.0
+
+
+def test_nearest_rank_threshold_spec_example():
+    """samples {UL 0.01 x95, 0.05 x5} -> TH = 0.05 (rank
+    floor(0.95 n) + 1, Q5),
+    i.e. L_th = 20 ms; all equal -> that value; negative samples excluded."""
+    L = [100 * MS] * 95 + [20 * MS] * 5
+    random.Random(0).shuffle(L)
+    assert O.nearest_rank_lth(L) == 20 * MS
+    assert O.nearest_rank_lth([50 * MS] * 10) == 50 * MS
+    assert O.nearest_rank_lth([-5, -7] + [50 * MS] * 10) == 50 * MS
+    assert O.nearest_rank_lth([-1, -2]) == -1
+
+
+def test_nearest_rank_brute_force():
+    rng = random.Random(5)
+    for _ in range(500):
+        n = rng.randint(1, 60)
+        L = [rng.randint(-10, 10**8) for _ in range(n)]
+        pos = sorted([x for x in L if x >= 0], key=_ul)
+        got = O.nearest_rank_lth(L)
+        if not pos:
+            assert got == -1
+            continue
+        k = min(95 * len(pos) // 100 + 1, len(pos))
+        assert _ul(got) == _ul(pos[k - 1])
+        # at most 5 % of the samples are strictly more urgent than the threshold sample
+        assert sum(1 for x in pos if _ul(x) > _ul(got)) * 100 <= 5 * len(pos)
