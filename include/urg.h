@@ -1,0 +1,157 @@
+/*
+ * include/urg.h -- C ABI of the B200 batched UrgenGo launch-policy simulator.
+ *
+ * Implemented by liburg.so (paper_2509_12207_b200/csrc/, CUDA for sm_100a).
+ * All integers; times are int64 nanoseconds; utilisation is per-mille of the GPU.
+ * The rules being simulated are DESIGN.md "Model M0" (R0-R23), our reading of
+ * arXiv 2509.12207 (UrgenGo); every function below cites the passage that
+ * defines what it computes.
+ *
+ * Ownership: the caller owns every descriptor and output buffer.  The library
+ * allocates only inside urg_create_workload (a device copy of the template and
+ * two small device scratch words) and frees them in urg_destroy_workload.
+ * Errors: every call returns a urg_status; urg_last_error() gives a
+ * thread-local message naming the offending field, e.g.
+ * "chains[3].tasks[1].kernels[7].nominal_ns must be > 0".
+ */
+#ifndef URG_H
+#define URG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    URG_OK = 0,
+    URG_EINVAL = -1,     /* malformed descriptor or argument */
+    URG_ERANGE = -2,     /* valid but outside what the device path supports (C > 32, template > smem) */
+    URG_ENOMEM = -3,     /* device allocation failed */
+    URG_ECUDA = -4,      /* a CUDA runtime call failed */
+    URG_EINTERNAL = -5   /* the kernel tripped an internal invariant (see urg_check) */
+} urg_status;
+
+/* One GPU kernel of a task: its lookup-table record (Table 1).
+ * nominal_ns: execution time before per-scenario factors (> 0);
+ * estimate_ns: ~E^gpu_k used in Eq. 2; util_permille: U_k in [0, 1000]. */
+typedef struct {
+    uint32_t nominal_ns;
+    uint32_t estimate_ns;
+    uint16_t util_permille;
+    uint16_t flags;            /* reserved, must be 0 */
+} urg_kernel_desc;
+
+/* One task: a CPU segment, then num_kernels (>= 1) kernels launched in order on
+ * one stream, then a final stream synchronisation. */
+typedef struct {
+    uint32_t cpu_nominal_ns;   /* CPU segment time before the per-instance factor */
+    uint32_t cpu_estimate_ns;  /* ~E^cpu_j used in Eq. 2 */
+    uint32_t num_kernels;
+    const urg_kernel_desc *kernels;
+} urg_task_desc;
+
+/* A periodic task chain with an end-to-end deadline (Table 2). */
+typedef struct {
+    int64_t period_ns;         /* > 0 */
+    int64_t deadline_ns;       /* > 0 */
+    int64_t offset_ns;         /* >= 0, first arrival before jitter */
+    uint32_t num_tasks;        /* >= 1 */
+    const urg_task_desc *tasks;
+    uint32_t cpu_sigma_ppm;    /* per-instance CPU spread, ppm of the mean (Table 2 "+-") */
+    uint32_t gpu_sigma_ppm;    /* per-instance GPU spread */
+} urg_chain_desc;
+
+/* A workload template shared by every scenario of a batch. */
+typedef struct {
+    uint32_t num_chains;                  /* 1..32 (one warp lane per chain) */
+    const urg_chain_desc *chains;
+    uint32_t num_prio;                    /* NUM_PRI stream priorities, 1..8 (6) */
+    int64_t launch_ns;                    /* lambda, CPU cost of a launch */
+    int64_t launch_akb_ns;                /* extra UrgenGo cost per launch: AKB update */
+    int64_t sync_lo_ns, sync_hi_ns;       /* sigma range per sync call */
+    int64_t jitter_ns;                    /* arrival jitter J; must be < every P' */
+    const int32_t *inst_quantiles_q16;    /* host, 4096 truncated-normal z quantiles (Q16.16) or NULL */
+    const uint32_t *kern_quantiles_q16;   /* host, 4096 per-kernel factor quantiles (Q16.16) or NULL */
+    int64_t rt_bin_ns;                    /* response-time histogram bin width (> 0) */
+    uint32_t rt_bins;                     /* number of bins B (>= 1; last bin is open-ended) */
+} urg_workload_desc;
+
+typedef struct urg_workload urg_workload; /* opaque; immutable after create; owns its device copy */
+
+/* Validate d and build the device template (on the current CUDA device).
+ * All descriptor pointers are host pointers and are not retained. */
+urg_status urg_create_workload(const urg_workload_desc *d, urg_workload **out);
+void urg_destroy_workload(urg_workload *w);
+
+/* Policies (§4.4; baselines P:614-615). */
+enum { URG_FIFO = 0, URG_STATIC = 1, URG_URGENGO = 2 };
+/* UrgenGo mechanisms: stream binding, delayed launching, early exit. */
+enum { URG_F_BIND = 1, URG_F_DELAY = 2, URG_F_EARLY_EXIT = 4 };
+/* Launch synchronisation (Fig. fig:launch (a)-(d)). */
+enum { URG_SYNC_ASYNC = 0, URG_SYNC_EACH = 1, URG_SYNC_BATCHED = 2, URG_SYNC_OVERLAP = 3 };
+
+typedef struct {
+    uint32_t kind;                 /* URG_FIFO / URG_STATIC / URG_URGENGO */
+    uint32_t flags;                /* URG_F_* (UrgenGo only) */
+    uint32_t sync_mode;            /* URG_SYNC_* */
+    int64_t delta_eval_ns;         /* Delta_eval (0.5 ms), > 0 */
+    int64_t lax_threshold_ns;      /* L_th = 1/TH_urgent; < 0 disables urgency */
+    int64_t sleep_ns;              /* delay-loop sleep (1 ms), > 0 */
+    uint32_t util_exempt_permille; /* kernels below this are never delayed (100) */
+} urg_policy;
+
+typedef struct {
+    uint64_t seed;                 /* Philox key */
+    uint64_t scenario_begin;       /* global index of the first scenario (randomness is keyed by it) */
+    uint64_t scenario_count;       /* scenario_begin + scenario_count <= 2^32 */
+    int64_t horizon_ns;            /* H: instances arriving before H are admitted (R7) */
+    uint32_t fa_num, fa_den;       /* arrival-rate factor f_a = fa_num/fa_den */
+    uint32_t fd_num, fd_den;       /* deadline factor f_d */
+    uint32_t ftight_permille;      /* f_tight: fraction of chains with halved deadlines */
+    uint32_t tight_explicit;       /* 1: use tight_mask instead of the per-scenario draw */
+    uint32_t tight_mask;
+} urg_batch;
+
+/* Outputs (DEVICE pointers for urg_simulate_batch, HOST for urg_simulate_batch_host).
+ * records: [scenario_count][num_chains][8] uint32 per DESIGN.md R22 (total, miss, early,
+ *          unfinished, launches, rt_hash, sum_rt_lo, sum_rt_hi), or NULL;
+ * agg:     urg_agg_words(w) int64, R23 layout; the kernel ADDS into it (zero it first). */
+typedef struct {
+    uint32_t *records;
+    int64_t *agg;
+} urg_outputs;
+
+/* Number of int64 words of the aggregate buffer:
+ * num_chains * (5 + rt_bins + 101) + 2 (launch events, loop steps). */
+uint64_t urg_agg_words(const urg_workload *w);
+
+/* Simulate scenarios [scenario_begin, scenario_begin + scenario_count) of the
+ * workload under policy p (DESIGN.md Model M0) and add their results to o.
+ * Asynchronous: enqueued on cuda_stream (a cudaStream_t, NULL = legacy default);
+ * calls using the same workload must be ordered on one stream. */
+urg_status urg_simulate_batch(const urg_workload *w, const urg_policy *p, const urg_batch *b,
+                              const urg_outputs *o, void *cuda_stream);
+
+/* Same with HOST output buffers: allocates device outputs, simulates, copies
+ * records and agg back (agg is ADDED into the host buffer).  Synchronous. */
+urg_status urg_simulate_batch_host(const urg_workload *w, const urg_policy *p, const urg_batch *b,
+                                   const urg_outputs *host_o, void *cuda_stream);
+
+/* Synchronise cuda_stream and report a device-side invariant trip recorded by an
+ * earlier urg_simulate_batch (URG_EINTERNAL, *scenario_out = offending scenario). */
+urg_status urg_check(const urg_workload *w, void *cuda_stream, int64_t *scenario_out);
+
+/* Eq. 3 from a HOST aggregate buffer: per_chain_out[c] =
+ * M_miss/M_total (0 when M_total = 0); overall = mean over chains with M_total > 0. */
+urg_status urg_miss_ratios(const urg_workload *w, const int64_t *agg_host, double *per_chain_out,
+                           double *overall_out);
+
+/* Thread-local description of the last error (empty string if none). */
+const char *urg_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* URG_H */

@@ -261,7 +261,7 @@ typedef struct {
     int64_t *akb_L_view;            /* scratch */
     int64_t *trace; int64_t trace_cap; int64_t trace_len;
     int64_t *agg;
-    int64_t steps, launches;
+    int64_t steps, launches, t_prev;
     /* calibration sampling */
     int64_t cal_next, cal_end;
     int64_t *cal_L; int64_t cal_n, cal_cap;
@@ -501,33 +501,39 @@ static void lane_step(orc_sim *S, uint32_t c, int64_t t)
             if (last) L->cpu_idx++;                      /* PAPER.md:335 */
             uint32_t est = in->k_est[L->kbase + n];
             if (n == first) { L->acc = 0; L->batch_start = first; }
+            int sync = 0;
+            uint32_t target = 0;
             switch (in->sync_mode) {
             case ORC_ASYNC:                              /* PAPER.md:144, 491 */
-                if (last) { issue_sync(S, c, t, L->launched); return; }
+                if (last) { sync = 1; target = L->launched; }
                 break;
             case ORC_EACH:                               /* PAPER.md:493 */
-                issue_sync(S, c, t, L->launched); return;
+                sync = 1; target = L->launched;
+                break;
             case ORC_BATCHED: {                          /* PAPER.md:496-499 */
                 int closes = orc_batch_add(&L->acc, est, in->delta_eval_ns);
-                if (closes || last) { L->acc = 0; issue_sync(S, c, t, L->launched); return; }
+                if (closes || last) { L->acc = 0; sync = 1; target = L->launched; }
                 break;
             }
             case ORC_OVERLAP: {                          /* PAPER.md:504-509 */
                 int closes = orc_batch_add(&L->acc, est, in->delta_eval_ns);
-                if (last) { L->acc = 0; issue_sync(S, c, t, L->launched); return; }
-                if (closes) {
+                if (last) { L->acc = 0; sync = 1; target = L->launched; }
+                else if (closes) {
                     uint32_t prev_batch_end = L->batch_start;   /* wait for the previous batch */
                     L->batch_start = L->launched;
                     if (prev_batch_end == first) {             /* the task's first close: no sync */
                         tr(S, t, TR_FREE_CLOSE, c, L->inst, L->launched, 0);
                         if (urgengo(S)) evaluate(S, c, t);
-                        break;
-                    }
-                    issue_sync(S, c, t, prev_batch_end);
-                    return;
+                    } else { sync = 1; target = prev_batch_end; }
                 }
                 break;
             }
+            }
+            if (sync) {
+                issue_sync(S, c, t, target);
+                /* a wait already satisfied that costs 0 returns at this same t: the step goes on (R21) */
+                if (L->pc == PC_SYNC_RET && L->cpu_next == t) continue;
+                return;
             }
             L->pc = PC_ATTEMPT;                          /* next kernel, same time */
             continue;
@@ -630,6 +636,8 @@ static int sim_scenario(const orc_input *in, uint64_t s, uint32_t *rec, int64_t 
     S.in = in; S.s = s; S.C = in->num_chains; S.agg = agg;
     S.trace = trace; S.trace_cap = trace_cap; S.trace_len = trace_len ? *trace_len : 0;
     S.cal_L = cal_L; S.cal_cap = cal_cap; S.cal_n = 0; S.cal_end = cal_end; S.cal_next = 0;
+    S.t_prev = -1;
+    int rc = 0;
     S.lane = calloc(S.C, sizeof(orc_lane));
     S.snap_L = calloc(S.C, sizeof(int64_t));
     S.snap_n = calloc(S.C, sizeof(uint32_t));
@@ -694,6 +702,8 @@ static int sim_scenario(const orc_input *in, uint64_t s, uint32_t *rec, int64_t 
             while (S.cal_next < S.cal_end && S.cal_next < t) { cal_sample(&S); S.cal_next += 1000000; }
         }
         if (t > S.H_stop) break;
+        if (t <= S.t_prev) { rc = -3; break; }            /* every loop step advances time (R21) */
+        S.t_prev = t;
         S.steps++;
         tr(&S, t, TR_STEP, -1, -1, 0, 0);
         retire(&S, t);                                                   /* Phase A */
@@ -725,7 +735,7 @@ static int sim_scenario(const orc_input *in, uint64_t s, uint32_t *rec, int64_t 
     if (trace_len) *trace_len = S.trace_len;
     if (cal_n) *cal_n = S.cal_n;
     free(S.lane); free(S.snap_L); free(S.snap_n);
-    return 0;
+    return rc;
 }
 
 /* Simulate scenarios [scenario_begin, scenario_begin + scenario_count).

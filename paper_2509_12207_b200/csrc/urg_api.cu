@@ -1,0 +1,345 @@
+// urg_api.cu -- host side of liburg.so: the C ABI declared in include/urg.h.
+//
+// Validates descriptors (errors name the offending field), packs the workload
+// template into the device blob (urg_layout.h), owns its HBM copy, and launches
+// the simulation kernel (urg_sim.cu) on the caller's stream.  No simulation
+// arithmetic happens here: every step of the path runs in the kernel.
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/urg.h"
+#include "urg_layout.h"
+
+extern "C" __global__ void urg_sim_kernel(const uint8_t *blob, const UrgSimParams P, uint32_t *records,
+                                          unsigned long long *agg, unsigned long long *work, long long *err);
+extern "C" __global__ void urg_philox_kat_kernel(const uint4 *ctr, const uint2 *key, uint4 *out, int n);
+
+struct urg_workload {
+    uint32_t num_chains, num_prio, rt_bins;
+    int64_t launch_ns, launch_akb_ns, sync_lo_ns, sync_hi_ns, jitter_ns, rt_bin_ns;
+    std::vector<int64_t> period, deadline;
+    std::vector<uint8_t> blob;        // host copy of the packed template
+    uint8_t *d_blob = nullptr;        // HBM copy
+    unsigned long long *d_work = nullptr;   // per-launch scenario counter
+    long long *d_err = nullptr;       // [code, scenario]
+    int device = 0;
+    int num_sms = 148;
+};
+
+static thread_local std::string g_err;
+
+static urg_status fail(urg_status st, const char *fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+
+static urg_status cuda_fail(cudaError_t e, const char *what)
+{
+    return fail(URG_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define CUDA_TRY(x, what)                                  \
+    do {                                                   \
+        cudaError_t e_ = (x);                              \
+        if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+    } while (0)
+
+extern "C" const char *urg_last_error(void) { return g_err.c_str(); }
+
+static uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
+
+extern "C" urg_status urg_create_workload(const urg_workload_desc *d, urg_workload **out)
+{
+    g_err.clear();
+    if (!out) return fail(URG_EINVAL, "out must not be NULL");
+    *out = nullptr;
+    if (!d) return fail(URG_EINVAL, "desc must not be NULL");
+    if (d->num_chains == 0) return fail(URG_EINVAL, "num_chains must be >= 1");
+    if (d->num_chains > 32) return fail(URG_ERANGE, "num_chains = %u exceeds 32 (one warp lane per chain)", d->num_chains);
+    if (!d->chains) return fail(URG_EINVAL, "chains must not be NULL");
+    if (d->num_prio < 1 || d->num_prio > 8) return fail(URG_EINVAL, "num_prio must be in 1..8");
+    if (d->launch_ns < 0) return fail(URG_EINVAL, "launch_ns must be >= 0");
+    if (d->launch_akb_ns < 0) return fail(URG_EINVAL, "launch_akb_ns must be >= 0");
+    if (d->sync_lo_ns < 0 || d->sync_hi_ns < d->sync_lo_ns)
+        return fail(URG_EINVAL, "sync range must satisfy 0 <= sync_lo_ns <= sync_hi_ns");
+    if (d->sync_hi_ns - d->sync_lo_ns >= 0xFFFFFFFFLL) return fail(URG_ERANGE, "sync_hi_ns - sync_lo_ns must be < 2^32 - 1");
+    if (d->jitter_ns < 0 || d->jitter_ns >= 0xFFFFFFFFLL) return fail(URG_EINVAL, "jitter_ns must be in [0, 2^32 - 1)");
+    if (d->rt_bin_ns <= 0) return fail(URG_EINVAL, "rt_bin_ns must be > 0");
+    if (d->rt_bins < 1 || d->rt_bins > (1u << 20)) return fail(URG_EINVAL, "rt_bins must be in 1..2^20");
+
+    uint32_t n_tasks = 0, n_kern = 0;
+    for (uint32_t c = 0; c < d->num_chains; ++c) {
+        const urg_chain_desc &ch = d->chains[c];
+        if (ch.period_ns <= 0) return fail(URG_EINVAL, "chains[%u].period_ns must be > 0", c);
+        if (ch.deadline_ns <= 0) return fail(URG_EINVAL, "chains[%u].deadline_ns must be > 0", c);
+        if (ch.offset_ns < 0) return fail(URG_EINVAL, "chains[%u].offset_ns must be >= 0", c);
+        if (ch.period_ns >= (1LL << 40) || ch.deadline_ns >= (1LL << 40) || ch.offset_ns >= (1LL << 40))
+            return fail(URG_ERANGE, "chains[%u]: period/deadline/offset must be < 2^40 ns", c);
+        if (ch.num_tasks < 1) return fail(URG_EINVAL, "chains[%u].num_tasks must be >= 1", c);
+        if (!ch.tasks) return fail(URG_EINVAL, "chains[%u].tasks must not be NULL", c);
+        for (uint32_t j = 0; j < ch.num_tasks; ++j) {
+            const urg_task_desc &t = ch.tasks[j];
+            if (t.num_kernels < 1) return fail(URG_EINVAL, "chains[%u].tasks[%u].num_kernels must be >= 1", c, j);
+            if (!t.kernels) return fail(URG_EINVAL, "chains[%u].tasks[%u].kernels must not be NULL", c, j);
+            for (uint32_t k = 0; k < t.num_kernels; ++k) {
+                const urg_kernel_desc &kd = t.kernels[k];
+                if (kd.nominal_ns == 0)
+                    return fail(URG_EINVAL, "chains[%u].tasks[%u].kernels[%u].nominal_ns must be > 0", c, j, k);
+                if (kd.util_permille > 1000)
+                    return fail(URG_EINVAL, "chains[%u].tasks[%u].kernels[%u].util_permille must be <= 1000", c, j, k);
+                if (kd.flags != 0)
+                    return fail(URG_EINVAL, "chains[%u].tasks[%u].kernels[%u].flags must be 0", c, j, k);
+            }
+            n_kern += t.num_kernels;
+        }
+        n_tasks += ch.num_tasks;
+    }
+
+    // ---- pack the blob ----
+    UrgBlobHeader h = {};
+    h.magic = URG_BLOB_MAGIC;
+    h.num_chains = d->num_chains;
+    h.num_tasks = n_tasks;
+    h.num_kernels = n_kern;
+    uint32_t off = align16(sizeof(UrgBlobHeader));
+    h.off_chains = off; off = align16(off + d->num_chains * (uint32_t)sizeof(UrgChainRec));
+    h.off_tasks = off;  off = align16(off + n_tasks * (uint32_t)sizeof(UrgTaskRec));
+    h.off_kerns = off;  off = align16(off + n_kern * (uint32_t)sizeof(UrgKernRec));
+    if (d->inst_quantiles_q16) { h.off_inst_q = off; off = align16(off + URG_QTABLE * 4); }
+    if (d->kern_quantiles_q16) { h.off_kern_q = off; off = align16(off + URG_QTABLE * 4); }
+    h.total_bytes = off;
+    if (off > URG_MAX_BLOB_BYTES)
+        return fail(URG_ERANGE, "template needs %u bytes of shared memory, more than the %u-byte budget", off,
+                    URG_MAX_BLOB_BYTES);
+
+    urg_workload *w = new urg_workload();
+    w->num_chains = d->num_chains; w->num_prio = d->num_prio; w->rt_bins = d->rt_bins;
+    w->launch_ns = d->launch_ns; w->launch_akb_ns = d->launch_akb_ns;
+    w->sync_lo_ns = d->sync_lo_ns; w->sync_hi_ns = d->sync_hi_ns;
+    w->jitter_ns = d->jitter_ns; w->rt_bin_ns = d->rt_bin_ns;
+    w->blob.assign(off, 0);
+    memcpy(w->blob.data(), &h, sizeof h);
+    UrgChainRec *chs = (UrgChainRec *)(w->blob.data() + h.off_chains);
+    UrgTaskRec *tks = (UrgTaskRec *)(w->blob.data() + h.off_tasks);
+    UrgKernRec *krs = (UrgKernRec *)(w->blob.data() + h.off_kerns);
+    uint32_t tb = 0, kb = 0;
+    for (uint32_t c = 0; c < d->num_chains; ++c) {
+        const urg_chain_desc &ch = d->chains[c];
+        UrgChainRec &r = chs[c];
+        r.period_ns = ch.period_ns; r.deadline_ns = ch.deadline_ns; r.offset_ns = ch.offset_ns;
+        r.num_tasks = ch.num_tasks; r.task_base = tb;
+        r.kern_base = kb; r.cpu_sigma_ppm = ch.cpu_sigma_ppm; r.gpu_sigma_ppm = ch.gpu_sigma_ppm;
+        uint32_t local = 0;
+        for (uint32_t j = 0; j < ch.num_tasks; ++j) {
+            const urg_task_desc &t = ch.tasks[j];
+            tks[tb + j] = UrgTaskRec{t.cpu_nominal_ns, t.cpu_estimate_ns, t.num_kernels, local};
+            for (uint32_t k = 0; k < t.num_kernels; ++k)
+                krs[kb + local + k] = UrgKernRec{t.kernels[k].nominal_ns, t.kernels[k].estimate_ns,
+                                                 t.kernels[k].util_permille, 0};
+            local += t.num_kernels;
+        }
+        r.num_kernels = local;
+        tb += ch.num_tasks; kb += local;
+        w->period.push_back(ch.period_ns);
+        w->deadline.push_back(ch.deadline_ns);
+    }
+    if (d->inst_quantiles_q16) memcpy(w->blob.data() + h.off_inst_q, d->inst_quantiles_q16, URG_QTABLE * 4);
+    if (d->kern_quantiles_q16) memcpy(w->blob.data() + h.off_kern_q, d->kern_quantiles_q16, URG_QTABLE * 4);
+
+    cudaError_t e;
+    if ((e = cudaGetDevice(&w->device)) != cudaSuccess) { delete w; return cuda_fail(e, "cudaGetDevice"); }
+    cudaDeviceGetAttribute(&w->num_sms, cudaDevAttrMultiProcessorCount, w->device);
+    if ((e = cudaMalloc(&w->d_blob, off)) != cudaSuccess) { delete w; return fail(URG_ENOMEM, "cudaMalloc(blob)"); }
+    if ((e = cudaMalloc(&w->d_work, 64)) != cudaSuccess) { cudaFree(w->d_blob); delete w; return fail(URG_ENOMEM, "cudaMalloc(work)"); }
+    w->d_err = (long long *)(w->d_work + 2);
+    if ((e = cudaMemcpy(w->d_blob, w->blob.data(), off, cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaMemset(w->d_work, 0, 64)) != cudaSuccess) {
+        cudaFree(w->d_blob); cudaFree(w->d_work); delete w;
+        return cuda_fail(e, "copying the template to the device");
+    }
+    *out = w;
+    return URG_OK;
+}
+
+extern "C" void urg_destroy_workload(urg_workload *w)
+{
+    if (!w) return;
+    cudaFree(w->d_blob);
+    cudaFree(w->d_work);
+    delete w;
+}
+
+extern "C" uint64_t urg_agg_words(const urg_workload *w)
+{
+    return w ? (uint64_t)w->num_chains * (5 + w->rt_bins + 101) + 2 : 0;
+}
+
+static urg_status validate_call(const urg_workload *w, const urg_policy *p, const urg_batch *b)
+{
+    if (!w || !p || !b) return fail(URG_EINVAL, "workload, policy and batch must not be NULL");
+    if (p->kind > URG_URGENGO) return fail(URG_EINVAL, "policy.kind must be 0..2");
+    if (p->flags > 7) return fail(URG_EINVAL, "policy.flags has unknown bits");
+    if (p->sync_mode > URG_SYNC_OVERLAP) return fail(URG_EINVAL, "policy.sync_mode must be 0..3");
+    if (p->delta_eval_ns <= 0) return fail(URG_EINVAL, "policy.delta_eval_ns must be > 0");
+    if (p->sleep_ns <= 0) return fail(URG_EINVAL, "policy.sleep_ns must be > 0");
+    if (b->fa_num == 0 || b->fa_den == 0) return fail(URG_EINVAL, "batch.fa_num and batch.fa_den must be > 0");
+    if (b->fd_num == 0 || b->fd_den == 0) return fail(URG_EINVAL, "batch.fd_num and batch.fd_den must be > 0");
+    if (b->ftight_permille > 1000) return fail(URG_EINVAL, "batch.ftight_permille must be <= 1000");
+    if (b->horizon_ns < 0 || b->horizon_ns >= (1LL << 44)) return fail(URG_ERANGE, "batch.horizon_ns must be in [0, 2^44)");
+    if (b->scenario_begin + b->scenario_count > (1ULL << 32) || b->scenario_begin >= (1ULL << 32))
+        return fail(URG_ERANGE, "batch: scenario indices must stay below 2^32");
+    for (uint32_t c = 0; c < w->num_chains; ++c) {
+        const int64_t Pp = w->period[c] * (int64_t)b->fa_den / (int64_t)b->fa_num;   // < 2^72? guarded below
+        if ((double)w->period[c] * b->fa_den > 4.0e18 || (double)w->deadline[c] * b->fd_num > 4.0e18)
+            return fail(URG_ERANGE, "chains[%u]: period*fa_den or deadline*fd_num overflows int64", c);
+        if (Pp <= w->jitter_ns) return fail(URG_EINVAL, "chains[%u]: scaled period P' = %lld must exceed jitter_ns", c, (long long)Pp);
+        if (w->deadline[c] * (int64_t)b->fd_num / (int64_t)b->fd_den >= (1LL << 44))
+            return fail(URG_ERANGE, "chains[%u]: scaled deadline must be < 2^44 ns", c);
+    }
+    return URG_OK;
+}
+
+static void fill_params(const urg_workload *w, const urg_policy *p, const urg_batch *b, UrgSimParams &P)
+{
+    memset(&P, 0, sizeof P);
+    P.num_chains = w->num_chains; P.num_prio = w->num_prio; P.rt_bins = w->rt_bins;
+    P.agg_stride = 5 + w->rt_bins + 101;
+    P.launch_ns = w->launch_ns; P.launch_akb_ns = w->launch_akb_ns;
+    P.sync_lo_ns = w->sync_lo_ns; P.sync_hi_ns = w->sync_hi_ns;
+    P.jitter_ns = w->jitter_ns; P.rt_bin_ns = w->rt_bin_ns;
+    P.kind = p->kind; P.flags = p->flags; P.sync_mode = p->sync_mode; P.util_exempt = p->util_exempt_permille;
+    P.delta_eval_ns = p->delta_eval_ns; P.lax_threshold_ns = p->lax_threshold_ns; P.sleep_ns = p->sleep_ns;
+    P.seed = b->seed; P.scenario_begin = b->scenario_begin; P.scenario_count = b->scenario_count;
+    P.horizon_ns = b->horizon_ns;
+    P.fa_num = b->fa_num; P.fa_den = b->fa_den; P.fd_num = b->fd_num; P.fd_den = b->fd_den;
+    P.ftight_permille = b->ftight_permille; P.tight_explicit = b->tight_explicit; P.tight_mask = b->tight_mask;
+}
+
+// launch geometry: one warp per scenario in flight, persistent CTAs over the SMs
+static void geometry(const urg_workload *w, uint64_t count, int &warps, int &ctas)
+{
+    const char *ew = getenv("URG_WARPS_PER_CTA");
+    int per_sm_target = 16;                                 // warps resident per SM when work is plentiful
+    if (const char *es = getenv("URG_WARPS_PER_SM")) per_sm_target = atoi(es);
+    uint64_t need = (count + (uint64_t)w->num_sms - 1) / (uint64_t)w->num_sms;   // warps per SM to hold all
+    warps = (int)(need < (uint64_t)per_sm_target ? need : (uint64_t)per_sm_target);
+    if (ew) warps = atoi(ew);
+    if (warps < 1) warps = 1;
+    if (warps > 16) warps = 16;
+    const uint64_t blocks_needed = (count + warps - 1) / warps;
+    ctas = (int)(blocks_needed < (uint64_t)w->num_sms ? blocks_needed : (uint64_t)w->num_sms);
+    if (ctas < 1) ctas = 1;
+}
+
+extern "C" urg_status urg_simulate_batch(const urg_workload *w, const urg_policy *p, const urg_batch *b,
+                                         const urg_outputs *o, void *cuda_stream)
+{
+    g_err.clear();
+    urg_status st = validate_call(w, p, b);
+    if (st != URG_OK) return st;
+    if (!o || !o->agg) return fail(URG_EINVAL, "outputs.agg must not be NULL");
+    if (b->scenario_count == 0) return URG_OK;
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    UrgSimParams P;
+    fill_params(w, p, b, P);
+    int warps, ctas;
+    geometry(w, b->scenario_count, warps, ctas);
+    P.blob_bytes = (uint32_t)w->blob.size();
+    P.mbar_offset = align16(P.blob_bytes);
+    P.snap_offset = align16(P.mbar_offset + 16);
+    P.smem_bytes = P.snap_offset + warps * 32 * 8;
+    CUDA_TRY(cudaFuncSetAttribute(urg_sim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem_bytes),
+             "cudaFuncSetAttribute(smem)");
+    CUDA_TRY(cudaMemsetAsync(w->d_work, 0, 8, s), "cudaMemsetAsync(work counter)");
+    urg_sim_kernel<<<ctas, warps * 32, P.smem_bytes, s>>>(w->d_blob, P, o->records, (unsigned long long *)o->agg,
+                                                           w->d_work, w->d_err);
+    CUDA_TRY(cudaGetLastError(), "launching urg_sim_kernel");
+    return URG_OK;
+}
+
+extern "C" urg_status urg_simulate_batch_host(const urg_workload *w, const urg_policy *p, const urg_batch *b,
+                                              const urg_outputs *host_o, void *cuda_stream)
+{
+    g_err.clear();
+    urg_status st = validate_call(w, p, b);
+    if (st != URG_OK) return st;
+    if (!host_o || !host_o->agg) return fail(URG_EINVAL, "outputs.agg must not be NULL");
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    const uint64_t nagg = urg_agg_words(w);
+    const uint64_t nrec = host_o->records ? b->scenario_count * w->num_chains * 8 : 0;
+    urg_outputs d = {nullptr, nullptr};
+    std::vector<int64_t> tmp(nagg);
+    CUDA_TRY(cudaMallocAsync((void **)&d.agg, nagg * 8, s), "cudaMallocAsync(agg)");
+    if (nrec) CUDA_TRY(cudaMallocAsync((void **)&d.records, nrec * 4, s), "cudaMallocAsync(records)");
+    CUDA_TRY(cudaMemsetAsync(d.agg, 0, nagg * 8, s), "cudaMemsetAsync(agg)");
+    st = urg_simulate_batch(w, p, b, &d, cuda_stream);
+    if (st == URG_OK) {
+        cudaError_t e = cudaMemcpyAsync(tmp.data(), d.agg, nagg * 8, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess && nrec)
+            e = cudaMemcpyAsync(host_o->records, d.records, nrec * 4, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) st = cuda_fail(e, "copying results to the host");
+    }
+    cudaFreeAsync(d.agg, s);
+    if (d.records) cudaFreeAsync(d.records, s);
+    if (st != URG_OK) return st;
+    for (uint64_t i = 0; i < nagg; ++i) host_o->agg[i] += tmp[i];
+    return URG_OK;
+}
+
+extern "C" urg_status urg_check(const urg_workload *w, void *cuda_stream, int64_t *scenario_out)
+{
+    g_err.clear();
+    if (!w) return fail(URG_EINVAL, "workload must not be NULL");
+    long long e2[2] = {0, 0};
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    CUDA_TRY(cudaMemcpyAsync(e2, w->d_err, sizeof e2, cudaMemcpyDeviceToHost, s), "reading the error word");
+    CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    if (scenario_out) *scenario_out = e2[1];
+    if (e2[0] != 0)
+        return fail(URG_EINTERNAL, "device invariant %lld tripped in scenario %lld (%s)", e2[0], e2[1],
+                    e2[0] == 1 ? "time did not advance" : "step iteration guard");
+    return URG_OK;
+}
+
+extern "C" urg_status urg_miss_ratios(const urg_workload *w, const int64_t *agg_host, double *per_chain_out,
+                                      double *overall_out)
+{
+    g_err.clear();
+    if (!w || !agg_host) return fail(URG_EINVAL, "workload and agg_host must not be NULL");
+    const uint64_t stride = 5 + w->rt_bins + 101;
+    double sum = 0.0;
+    uint32_t used = 0;
+    for (uint32_t c = 0; c < w->num_chains; ++c) {
+        const int64_t total = agg_host[c * stride + 0], miss = agg_host[c * stride + 1];
+        const double r = total ? (double)miss / (double)total : 0.0;
+        if (per_chain_out) per_chain_out[c] = r;
+        if (total) { sum += r; ++used; }
+    }
+    if (overall_out) *overall_out = used ? sum / used : 0.0;
+    return URG_OK;
+}
+
+// test hook: device Philox on n (ctr, key) pairs in device memory (Philox KAT / oracle cross-check)
+extern "C" urg_status urg_debug_philox(const void *d_ctr, const void *d_key, void *d_out, int n, void *cuda_stream)
+{
+    if (n <= 0) return URG_OK;
+    urg_philox_kat_kernel<<<(n + 255) / 256, 256, 0, (cudaStream_t)cuda_stream>>>((const uint4 *)d_ctr,
+                                                                                   (const uint2 *)d_key,
+                                                                                   (uint4 *)d_out, n);
+    CUDA_TRY(cudaGetLastError(), "launching urg_philox_kat_kernel");
+    return URG_OK;
+}

@@ -1,0 +1,52 @@
+// Device template ("blob") layout and kernel parameters -- internal to liburg.so.
+//
+// The workload template is packed once on the host (urg_api.cu) into one
+// 16-byte-aligned blob, copied to HBM at urg_create_workload, and staged whole
+// into each CTA's shared memory by the simulation kernel (row A0).
+#pragma once
+#include <stdint.h>
+
+#define URG_BLOB_MAGIC 0x55524731u   // "URG1"
+#define URG_QTABLE 4096              // quantile-table entries (12-bit index)
+#define URG_MAX_BLOB_BYTES (160u * 1024u)
+
+enum { URG_TAG_ARR = 1, URG_TAG_TIGHT = 2, URG_TAG_INST = 3, URG_TAG_KERN = 4, URG_TAG_SYNC = 5 };
+
+struct __align__(16) UrgChainRec {     // 64 B
+    int64_t period_ns, deadline_ns, offset_ns;
+    uint32_t num_tasks, task_base;     // tasks [task_base, task_base + num_tasks)
+    uint32_t num_kernels, kern_base;   // kernels [kern_base, kern_base + num_kernels)
+    uint32_t cpu_sigma_ppm, gpu_sigma_ppm;
+    int64_t gpu_est_total;             // filled in-kernel at staging (sum of estimates)
+    int64_t cpu_est_total;             // filled in-kernel at staging
+};
+
+struct __align__(16) UrgTaskRec {      // 16 B
+    uint32_t cpu_nominal_ns, cpu_estimate_ns, num_kernels, first_kernel;   // first_kernel: chain-local
+};
+
+struct __align__(16) UrgKernRec {      // 16 B: one LDS.128 per access
+    uint32_t nominal_ns, estimate_ns, util_permille, reserved;
+};
+
+struct __align__(16) UrgBlobHeader {   // 64 B
+    uint32_t magic, num_chains, num_tasks, num_kernels;
+    uint32_t off_chains, off_tasks, off_kerns, off_inst_q;   // byte offsets; 0 = absent table
+    uint32_t off_kern_q, total_bytes, reserved0, reserved1;
+    uint32_t reserved[4];
+};
+
+struct UrgSimParams {
+    // workload scalars
+    uint32_t num_chains, num_prio, rt_bins, agg_stride;
+    int64_t launch_ns, launch_akb_ns, sync_lo_ns, sync_hi_ns, jitter_ns, rt_bin_ns;
+    // policy
+    uint32_t kind, flags, sync_mode, util_exempt;
+    int64_t delta_eval_ns, lax_threshold_ns, sleep_ns;
+    // batch
+    uint64_t seed, scenario_begin, scenario_count;
+    int64_t horizon_ns;
+    uint32_t fa_num, fa_den, fd_num, fd_den, ftight_permille, tight_explicit, tight_mask;
+    // staging
+    uint32_t blob_bytes, snap_offset, mbar_offset, smem_bytes;
+};

@@ -1,0 +1,207 @@
+"""Thin ctypes binding of liburg.so (include/urg.h).  Argument marshalling only:
+every step of the simulation runs in the CUDA kernel.  There is no CPU fallback:
+if the library is missing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as ct
+import os
+from typing import Optional
+
+import numpy as np
+
+from workloads.spec import Batch, Policy, Workload
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liburg.so")
+
+URG_OK, URG_EINVAL, URG_ERANGE, URG_ENOMEM, URG_ECUDA, URG_EINTERNAL = 0, -1, -2, -3, -4, -5
+
+
+class UrgError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"urg status {status}: {msg}")
+        self.status = status
+
+
+class KernelDesc(ct.Structure):
+    _fields_ = [("nominal_ns", ct.c_uint32), ("estimate_ns", ct.c_uint32),
+                ("util_permille", ct.c_uint16), ("flags", ct.c_uint16)]
+
+
+class TaskDesc(ct.Structure):
+    _fields_ = [("cpu_nominal_ns", ct.c_uint32), ("cpu_estimate_ns", ct.c_uint32),
+                ("num_kernels", ct.c_uint32), ("kernels", ct.POINTER(KernelDesc))]
+
+
+class ChainDesc(ct.Structure):
+    _fields_ = [("period_ns", ct.c_int64), ("deadline_ns", ct.c_int64), ("offset_ns", ct.c_int64),
+                ("num_tasks", ct.c_uint32), ("tasks", ct.POINTER(TaskDesc)),
+                ("cpu_sigma_ppm", ct.c_uint32), ("gpu_sigma_ppm", ct.c_uint32)]
+
+
+class WorkloadDesc(ct.Structure):
+    _fields_ = [("num_chains", ct.c_uint32), ("chains", ct.POINTER(ChainDesc)), ("num_prio", ct.c_uint32),
+                ("launch_ns", ct.c_int64), ("launch_akb_ns", ct.c_int64),
+                ("sync_lo_ns", ct.c_int64), ("sync_hi_ns", ct.c_int64), ("jitter_ns", ct.c_int64),
+                ("inst_quantiles_q16", ct.c_void_p), ("kern_quantiles_q16", ct.c_void_p),
+                ("rt_bin_ns", ct.c_int64), ("rt_bins", ct.c_uint32)]
+
+
+class PolicyS(ct.Structure):
+    _fields_ = [("kind", ct.c_uint32), ("flags", ct.c_uint32), ("sync_mode", ct.c_uint32),
+                ("delta_eval_ns", ct.c_int64), ("lax_threshold_ns", ct.c_int64), ("sleep_ns", ct.c_int64),
+                ("util_exempt_permille", ct.c_uint32)]
+
+
+class BatchS(ct.Structure):
+    _fields_ = [("seed", ct.c_uint64), ("scenario_begin", ct.c_uint64), ("scenario_count", ct.c_uint64),
+                ("horizon_ns", ct.c_int64), ("fa_num", ct.c_uint32), ("fa_den", ct.c_uint32),
+                ("fd_num", ct.c_uint32), ("fd_den", ct.c_uint32), ("ftight_permille", ct.c_uint32),
+                ("tight_explicit", ct.c_uint32), ("tight_mask", ct.c_uint32)]
+
+
+class OutputsS(ct.Structure):
+    _fields_ = [("records", ct.c_void_p), ("agg", ct.c_void_p)]
+
+
+SYMBOLS = ["urg_create_workload", "urg_destroy_workload", "urg_agg_words", "urg_simulate_batch",
+           "urg_simulate_batch_host", "urg_check", "urg_miss_ratios", "urg_last_error"]
+
+_lib = None
+
+
+def lib():
+    """Load liburg.so (built by paper_2509_12207_b200.build / __graft_entry__.build)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                               "(the CUDA path has no CPU fallback)")
+        L = ct.CDLL(LIB_PATH)
+        L.urg_create_workload.restype = ct.c_int
+        L.urg_create_workload.argtypes = [ct.POINTER(WorkloadDesc), ct.POINTER(ct.c_void_p)]
+        L.urg_destroy_workload.restype = None
+        L.urg_destroy_workload.argtypes = [ct.c_void_p]
+        L.urg_agg_words.restype = ct.c_uint64
+        L.urg_agg_words.argtypes = [ct.c_void_p]
+        for f in (L.urg_simulate_batch, L.urg_simulate_batch_host):
+            f.restype = ct.c_int
+            f.argtypes = [ct.c_void_p, ct.POINTER(PolicyS), ct.POINTER(BatchS), ct.POINTER(OutputsS), ct.c_void_p]
+        L.urg_check.restype = ct.c_int
+        L.urg_check.argtypes = [ct.c_void_p, ct.c_void_p, ct.POINTER(ct.c_int64)]
+        L.urg_miss_ratios.restype = ct.c_int
+        L.urg_miss_ratios.argtypes = [ct.c_void_p, ct.c_void_p, ct.c_void_p, ct.POINTER(ct.c_double)]
+        L.urg_last_error.restype = ct.c_char_p
+        L.urg_last_error.argtypes = []
+        L.urg_debug_philox.restype = ct.c_int
+        L.urg_debug_philox.argtypes = [ct.c_void_p, ct.c_void_p, ct.c_void_p, ct.c_int, ct.c_void_p]
+        _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status != URG_OK:
+        raise UrgError(status, lib().urg_last_error().decode())
+
+
+def policy_struct(p: Policy) -> PolicyS:
+    return PolicyS(p.kind, p.flags, p.sync_mode, p.delta_eval_ns, p.lax_threshold_ns, p.sleep_ns,
+                   p.util_exempt_permille)
+
+
+def batch_struct(b: Batch) -> BatchS:
+    return BatchS(b.seed, b.scenario_begin, b.scenario_count, b.horizon_ns, b.fa_num, b.fa_den, b.fd_num,
+                  b.fd_den, b.ftight_permille, b.tight_explicit, b.tight_mask)
+
+
+def _stream_handle(stream) -> Optional[int]:
+    if stream is None:
+        return None
+    return int(getattr(stream, "cuda_stream", stream))
+
+
+class DeviceWorkload:
+    """urg_workload handle: the template resident in HBM (urg_create_workload)."""
+
+    def __init__(self, w: Workload):
+        self.spec = w
+        keep = []
+        chains = (ChainDesc * w.num_chains)()
+        for ci, ch in enumerate(w.chains):
+            tasks = (TaskDesc * len(ch.tasks))()
+            for ti, t in enumerate(ch.tasks):
+                ks = (KernelDesc * len(t.kernels))(*[KernelDesc(k.nominal_ns, k.estimate_ns, k.util_permille, k.flags)
+                                                     for k in t.kernels])
+                keep.append(ks)
+                tasks[ti] = TaskDesc(t.cpu_nominal_ns, t.cpu_estimate_ns, len(t.kernels), ks)
+            keep.append(tasks)
+            chains[ci] = ChainDesc(ch.period_ns, ch.deadline_ns, ch.offset_ns, len(ch.tasks), tasks,
+                                   ch.cpu_sigma_ppm, ch.gpu_sigma_ppm)
+        inst = None if w.inst_quantiles_q16 is None else np.ascontiguousarray(w.inst_quantiles_q16, np.int32)
+        kern = None if w.kern_quantiles_q16 is None else np.ascontiguousarray(w.kern_quantiles_q16, np.uint32)
+        self.desc = WorkloadDesc(w.num_chains, chains, w.num_prio, w.launch_ns, w.launch_akb_ns, w.sync_lo_ns,
+                                 w.sync_hi_ns, w.jitter_ns, None if inst is None else inst.ctypes.data,
+                                 None if kern is None else kern.ctypes.data, w.rt_bin_ns, w.rt_bins)
+        self._keep = (keep, chains, inst, kern)
+        h = ct.c_void_p()
+        _check(lib().urg_create_workload(ct.byref(self.desc), ct.byref(h)))
+        self.handle = h
+        self.num_chains = w.num_chains
+        self.agg_words = int(lib().urg_agg_words(h))
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().urg_destroy_workload(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- device buffers (torch tensors on the current CUDA device) --
+    def simulate(self, p: Policy, b: Batch, agg, records=None, stream=None):
+        """urg_simulate_batch: asynchronous on `stream`; adds into `agg` (int64 device tensor)."""
+        o = OutputsS(None if records is None else records.data_ptr(), agg.data_ptr())
+        _check(lib().urg_simulate_batch(self.handle, ct.byref(policy_struct(p)), ct.byref(batch_struct(b)),
+                                        ct.byref(o), _stream_handle(stream)))
+
+    # -- host buffers (numpy) --
+    def simulate_host(self, p: Policy, b: Batch, agg: np.ndarray, records: Optional[np.ndarray] = None,
+                      stream=None):
+        """urg_simulate_batch_host: synchronous; agg (int64[agg_words]) is added into."""
+        assert agg.dtype == np.int64 and agg.flags.c_contiguous
+        o = OutputsS(None if records is None else records.ctypes.data, agg.ctypes.data)
+        _check(lib().urg_simulate_batch_host(self.handle, ct.byref(policy_struct(p)), ct.byref(batch_struct(b)),
+                                             ct.byref(o), _stream_handle(stream)))
+
+    def check(self, stream=None) -> None:
+        s = ct.c_int64(0)
+        _check(lib().urg_check(self.handle, _stream_handle(stream), ct.byref(s)))
+
+    def miss_ratios(self, agg_host: np.ndarray):
+        per = np.zeros(self.num_chains, np.float64)
+        ov = ct.c_double(0.0)
+        a = np.ascontiguousarray(agg_host, np.int64)
+        _check(lib().urg_miss_ratios(self.handle, a.ctypes.data, per.ctypes.data, ct.byref(ov)))
+        return per, ov.value
+
+
+def philox_device(ctr, key, stream=None):
+    """Device Philox4x32-10 of n (ctr, key) pairs (test hook for the known-answer vectors)."""
+    import torch
+    c = torch.as_tensor(np.ascontiguousarray(ctr, np.uint32).view(np.int32)).cuda()
+    k = torch.as_tensor(np.ascontiguousarray(key, np.uint32).view(np.int32)).cuda()
+    out = torch.zeros_like(c)
+    n = c.shape[0]
+    _check(lib().urg_debug_philox(c.data_ptr(), k.data_ptr(), out.data_ptr(), n, _stream_handle(stream)))
+    torch.cuda.synchronize()
+    return out.cpu().numpy().view(np.uint32)

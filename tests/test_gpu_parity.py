@@ -1,0 +1,200 @@
+"""CUDA path vs the CPU oracle, element by element, through the C ABI (-m gpu).
+
+Integer results must match bit-exactly (DESIGN.md §2 R22-R23): per-scenario
+records (including rt_hash, which pins every individual response time), the
+aggregate counters, both histograms, and the launch / loop-step counters.
+"""
+import random
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from workloads import get_config, paper11, toy2, w1, w2, w3
+from workloads.configs import _paper11_heavy
+from workloads.spec import (F_ALL, FIFO, MS, STATIC, SYNC_ASYNC, SYNC_BATCHED, SYNC_EACH, SYNC_OVERLAP, URGENGO,
+                            US, Batch, Chain, Kernel, Policy, Task, Workload)
+
+from .gpu_helpers import agg_from_records, assert_same, gpu_run
+from .test_oracle_properties import random_policy, random_workload
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2509_12207_b200.urg import lib
+    lib()   # loud failure if liburg.so is missing
+
+
+def both(w, p, b, ctx=""):
+    o = O.run(w, p, b)
+    r, a = gpu_run(w, p, b)
+    assert_same(o, r, a, ctx)
+    return o, r, a
+
+
+def test_philox_known_answers_device():
+    from paper_2509_12207_b200.urg import philox_device
+    kat = [([0, 0, 0, 0], [0, 0], [0x6627e8d5, 0xe169c58d, 0xbc57ac4c, 0x9b00dbd8]),
+           ([0xffffffff] * 4, [0xffffffff] * 2, [0x408f276d, 0x41c83b0e, 0xa20bc7c6, 0x6d5451fd]),
+           ([0x243f6a88, 0x85a308d3, 0x13198a2e, 0x03707344], [0xa4093822, 0x299f31d0],
+            [0xd16cfe09, 0x94fdcceb, 0x5001e420, 0x24126ea1])]
+    out = philox_device(np.array([k[0] for k in kat]), np.array([k[1] for k in kat]))
+    assert out.tolist() == [k[2] for k in kat]
+    rng = np.random.default_rng(0)
+    ctr = rng.integers(0, 2**32, size=(20000, 4), dtype=np.uint64).astype(np.uint32)
+    key = rng.integers(0, 2**32, size=(20000, 2), dtype=np.uint64).astype(np.uint32)
+    dev = philox_device(ctr, key)
+    for i in range(0, 20000, 997):
+        assert dev[i].tolist() == O.philox(ctr[i], key[i]).tolist()
+
+
+@pytest.mark.parametrize("kind,flags", [(FIFO, 0), (STATIC, 0), (URGENGO, 1), (URGENGO, 2), (URGENGO, 3), (URGENGO, 0)])
+def test_w1(kind, flags):
+    both(w1(), Policy(kind=kind, flags=flags, sync_mode=SYNC_ASYNC, lax_threshold_ns=5 * MS), Batch(horizon_ns=1 * MS))
+
+
+@pytest.mark.parametrize("mode", [SYNC_ASYNC, SYNC_EACH, SYNC_BATCHED, SYNC_OVERLAP])
+def test_w2(mode):
+    both(w2(), Policy(kind=URGENGO, flags=0, sync_mode=mode, lax_threshold_ns=-1), Batch(horizon_ns=1 * MS))
+
+
+def test_w3():
+    both(w3(), Policy(kind=URGENGO, flags=4, sync_mode=SYNC_ASYNC), Batch(horizon_ns=1 * MS))
+    both(w3(), Policy(kind=FIFO, flags=0, sync_mode=SYNC_ASYNC), Batch(horizon_ns=1 * MS))
+
+
+@pytest.mark.parametrize("mode", [SYNC_ASYNC, SYNC_EACH, SYNC_BATCHED, SYNC_OVERLAP])
+def test_toy2_all_policies(mode):
+    """BASELINE.json configs[0]: every policy and UrgenGo flag combination, bit-exact."""
+    cfg = get_config("toy2")
+    w = toy2()
+    pols = [Policy(kind=FIFO, flags=0, sync_mode=mode), Policy(kind=STATIC, flags=0, sync_mode=mode)]
+    pols += [Policy(kind=URGENGO, flags=f, sync_mode=mode, lax_threshold_ns=10 * MS) for f in range(8)]
+    for p in pols:
+        both(w, p, cfg.batch, f"toy2 kind={p.kind} flags={p.flags} mode={mode}")
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_small_workloads(seed):
+    rng = random.Random(seed)
+    w = random_workload(rng, C=rng.choice([1, 2, 3, 5, 8, 13, 32]), jitter=rng.choice([0, 3 * MS]))
+    w.sync_lo_ns = rng.choice([0, 10 * US])
+    w.sync_hi_ns = w.sync_lo_ns + rng.choice([0, 150 * US])
+    if rng.random() < 0.5:
+        from workloads.quantiles import inst_z_table, pareto_table
+        w.inst_quantiles_q16 = inst_z_table()
+        for ch in w.chains:
+            ch.cpu_sigma_ppm, ch.gpu_sigma_ppm = rng.randint(0, 500_000), rng.randint(0, 500_000)
+        if rng.random() < 0.5:
+            w.kern_quantiles_q16 = pareto_table()
+    p = random_policy(rng)
+    b = Batch(seed=seed * 7 + 1, scenario_begin=rng.randint(0, 1000), scenario_count=rng.randint(1, 40),
+              horizon_ns=rng.choice([100, 300]) * MS, ftight_permille=rng.choice([0, 400, 1000]),
+              fa_num=rng.choice([1, 5]), fa_den=rng.choice([1, 4]), fd_num=rng.choice([1, 3]), fd_den=rng.choice([1, 2]))
+    both(w, p, b, f"seed {seed}")
+
+
+@pytest.mark.parametrize("name", ["urgengo", "fifo", "static"])
+def test_paper11_small(name):
+    """configs[1] workload at a size the oracle finishes in seconds: 48 scenarios x 2 s, spanning many CTAs."""
+    cfg = get_config("paper11")
+    b = Batch(seed=cfg.batch.seed, scenario_count=48, horizon_ns=2_000 * MS, ftight_permille=400)
+    o, r, a = both(cfg.workload(), cfg.policies[name], b, name)
+    assert o.launches > 0
+
+
+def test_paper11_full_size_sampled():
+    """configs[1] at full size in bench.py's launch configuration (1000 scenarios x 10 s, UrgenGo):
+    sampled scenarios vs the oracle one by one, and the aggregate vs the GPU's own records."""
+    cfg = get_config("paper11")
+    w, p, b = cfg.workload(), cfg.policies["urgengo"], cfg.batch
+    r, a = gpu_run(w, p, b)
+    assert r.shape == (1000, 11, 8)
+    recon = agg_from_records(r, w.num_chains, w.rt_bins)
+    stride = 5 + w.rt_bins + 101
+    for c in range(w.num_chains):
+        assert np.array_equal(a[c * stride: c * stride + 5], recon[c * stride: c * stride + 5])
+        assert np.array_equal(a[c * stride + 5 + w.rt_bins:(c + 1) * stride],
+                              recon[c * stride + 5 + w.rt_bins:(c + 1) * stride])
+        # completed instances = rt histogram mass
+        comp = int(r[:, c, 0].astype(np.int64).sum() - r[:, c, 2].astype(np.int64).sum() - r[:, c, 3].astype(np.int64).sum())
+        assert a[c * stride + 5: c * stride + 5 + w.rt_bins].sum() == comp
+    assert a[-2] == recon[-2]
+    for s in [0, 1, 2, 333, 500, 998, 999]:
+        bs = Batch(seed=b.seed, scenario_begin=s, scenario_count=1, horizon_ns=b.horizon_ns,
+                   ftight_permille=b.ftight_permille)
+        o = O.run(w, p, bs)
+        assert np.array_equal(o.records[0], r[s]), f"scenario {s}"
+
+
+def test_heavy_tail_and_sweep_points():
+    """configs[3] (Pareto kernel factors) and two configs[2] sweep points, exact."""
+    lth = get_config("paper11").policies["urgengo"].lax_threshold_ns
+    wj = _paper11_heavy()
+    for p in [Policy(kind=URGENGO, flags=F_ALL, sync_mode=SYNC_OVERLAP, lax_threshold_ns=lth),
+              Policy(kind=FIFO, flags=0, sync_mode=SYNC_ASYNC)]:
+        both(wj, p, Batch(seed=0x5EED0004, scenario_count=16, horizon_ns=3_000 * MS, ftight_permille=400), "jitter")
+    cfg3 = get_config("usweep")
+    for bb in (cfg3.sweep[0], cfg3.sweep[-1]):
+        b = Batch(seed=bb.seed, scenario_begin=12345, scenario_count=16, horizon_ns=2_000 * MS,
+                  ftight_permille=400, fa_num=bb.fa_num, fa_den=bb.fa_den)
+        for name in ("urgengo", "static"):
+            both(cfg3.workload(), cfg3.policies[name], b, f"usweep {bb.fa_num}/{bb.fa_den} {name}")
+
+
+def test_edge_cases():
+    cfg = get_config("paper11")
+    w, p = cfg.workload(), cfg.policies["urgengo"]
+    # empty batch: no-op
+    r, a = gpu_run(w, p, Batch(scenario_count=0, horizon_ns=MS))
+    assert not a.any()
+    # horizon 0: nothing admitted
+    both(w, p, Batch(seed=3, scenario_count=4, horizon_ns=0), "H=0")
+    # one bin, explicit tight set, single chain
+    w1c = toy2()
+    w1c.rt_bins = 1
+    both(w1c, p, Batch(seed=5, scenario_count=3, horizon_ns=700 * MS, tight_explicit=1, tight_mask=0b10), "rt_bins=1")
+    solo = Workload(chains=[paper11().chains[10]], jitter_ns=0, inst_quantiles_q16=None)
+    both(solo, p, Batch(seed=9, scenario_count=2, horizon_ns=20_000 * MS), "C=1 llama")
+
+
+def test_sharding_invariance_single_gpu():
+    """Sub-range calls add up to the full-range call (SURVEY.md §4 fake-shard test)."""
+    import torch
+
+    from paper_2509_12207_b200.dist import shard_batch
+    from paper_2509_12207_b200.urg import DeviceWorkload
+    cfg = get_config("paper11")
+    w, p = cfg.workload(), cfg.policies["urgengo"]
+    b = Batch(seed=cfg.batch.seed, scenario_count=300, horizon_ns=1_000 * MS, ftight_permille=400)
+    with DeviceWorkload(w) as dw:
+        full = torch.zeros(dw.agg_words, dtype=torch.int64, device="cuda")
+        dw.simulate(p, b, full)
+        parts = torch.zeros_like(full)
+        for g in range(3):
+            dw.simulate(p, shard_batch(b, g, 3), parts)
+        torch.cuda.synchronize()
+        assert torch.equal(full, parts)
+
+
+def test_host_variant_matches_device():
+    from paper_2509_12207_b200.urg import DeviceWorkload
+    cfg = get_config("paper11")
+    w, p = cfg.workload(), cfg.policies["urgengo"]
+    b = Batch(seed=cfg.batch.seed, scenario_count=64, horizon_ns=1_000 * MS, ftight_permille=400)
+    r, a = gpu_run(w, p, b)
+    agg = np.zeros_like(a)
+    rec = np.zeros_like(r)
+    with DeviceWorkload(w) as dw:
+        dw.simulate_host(p, b, agg, rec)
+        per, overall = dw.miss_ratios(agg)
+    assert np.array_equal(agg, a) and np.array_equal(rec, r)
+    tot = rec[:, :, 0].astype(np.int64).sum(0)
+    miss = rec[:, :, 1].astype(np.int64).sum(0)
+    assert overall == O.overall_miss_ratio(miss, tot)

@@ -1,0 +1,73 @@
+"""CPU-side checks of the C-ABI library: it builds for sm_100a, loads, exports every
+symbol include/urg.h declares, and rejects malformed descriptors with a field
+locus before touching the GPU.  No compute calls (no GPU here)."""
+import ctypes as ct
+import os
+import re
+
+import pytest
+
+from workloads import paper11, toy2
+from workloads.spec import Chain, Kernel, Task, Workload
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2509_12207_b200 import build as B
+    B.build()
+    from paper_2509_12207_b200.urg import lib
+    return lib()
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "urg.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(urg_[a-z_]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol(L):
+    syms = declared_symbols()
+    assert {"urg_create_workload", "urg_simulate_batch", "urg_miss_ratios"} <= set(syms)
+    for s in syms:
+        assert hasattr(L, s), s
+
+
+def test_sass_is_sm100a():
+    import subprocess
+    from paper_2509_12207_b200 import build as B
+    B.build()
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", B.OUT], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def _create(w):
+    from paper_2509_12207_b200.urg import DeviceWorkload, UrgError
+    with pytest.raises(UrgError) as e:
+        DeviceWorkload(w)
+    return e.value
+
+
+def test_validation_loci(L):
+    w = toy2()
+    w.chains[1].tasks[2].kernels[3].nominal_ns = 0
+    e = _create(w)
+    assert e.status == -1 and "chains[1].tasks[2].kernels[3].nominal_ns" in str(e)
+    w = toy2()
+    w.chains[0].tasks[1].kernels[0].util_permille = 1001
+    assert "chains[0].tasks[1].kernels[0].util_permille" in str(_create(w))
+    w = toy2()
+    w.chains[0].period_ns = 0
+    assert "chains[0].period_ns" in str(_create(w))
+    w = toy2()
+    w.chains[1].tasks = []
+    assert "chains[1].num_tasks" in str(_create(w))
+    w = toy2()
+    w.num_prio = 9
+    assert "num_prio" in str(_create(w))
+    w = Workload(chains=[paper11().chains[0]] * 33)
+    e = _create(w)
+    assert e.status == -2 and "exceeds 32" in str(e)
+    w = Workload(chains=[])
+    assert "num_chains" in str(_create(w))
