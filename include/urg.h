@@ -126,6 +126,10 @@ typedef struct {
  * num_chains * (5 + rt_bins + 101) + 2 (launch events, loop steps). */
 uint64_t urg_agg_words(const urg_workload *w);
 
+/* Bytes of the packed template urg_create_workload copied host -> device
+ * (chains, tasks, kernel records, quantile tables; urg_layout.h). */
+uint64_t urg_template_bytes(const urg_workload *w);
+
 /* Simulate scenarios [scenario_begin, scenario_begin + scenario_count) of the
  * workload under policy p (DESIGN.md Model M0) and add their results to o.
  * Asynchronous: enqueued on cuda_stream (a cudaStream_t, NULL = legacy default);

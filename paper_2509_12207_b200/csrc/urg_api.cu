@@ -187,6 +187,11 @@ extern "C" uint64_t urg_agg_words(const urg_workload *w)
     return w ? (uint64_t)w->num_chains * (5 + w->rt_bins + 101) + 2 : 0;
 }
 
+extern "C" uint64_t urg_template_bytes(const urg_workload *w)
+{
+    return w ? (uint64_t)w->blob.size() : 0;
+}
+
 static urg_status validate_call(const urg_workload *w, const urg_policy *p, const urg_batch *b)
 {
     if (!w || !p || !b) return fail(URG_EINVAL, "workload, policy and batch must not be NULL");

@@ -65,7 +65,7 @@ class OutputsS(ct.Structure):
     _fields_ = [("records", ct.c_void_p), ("agg", ct.c_void_p)]
 
 
-SYMBOLS = ["urg_create_workload", "urg_destroy_workload", "urg_agg_words", "urg_simulate_batch",
+SYMBOLS = ["urg_create_workload", "urg_destroy_workload", "urg_agg_words", "urg_template_bytes", "urg_simulate_batch",
            "urg_simulate_batch_host", "urg_check", "urg_miss_ratios", "urg_last_error"]
 
 _lib = None
@@ -85,6 +85,8 @@ def lib():
         L.urg_destroy_workload.argtypes = [ct.c_void_p]
         L.urg_agg_words.restype = ct.c_uint64
         L.urg_agg_words.argtypes = [ct.c_void_p]
+        L.urg_template_bytes.restype = ct.c_uint64
+        L.urg_template_bytes.argtypes = [ct.c_void_p]
         for f in (L.urg_simulate_batch, L.urg_simulate_batch_host):
             f.restype = ct.c_int
             f.argtypes = [ct.c_void_p, ct.POINTER(PolicyS), ct.POINTER(BatchS), ct.POINTER(OutputsS), ct.c_void_p]
@@ -149,6 +151,7 @@ class DeviceWorkload:
         self.handle = h
         self.num_chains = w.num_chains
         self.agg_words = int(lib().urg_agg_words(h))
+        self.template_bytes = int(lib().urg_template_bytes(h))
 
     def close(self):
         if getattr(self, "handle", None):
