@@ -14,23 +14,28 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
          "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
 
 
-def needs_build() -> bool:
-    if not os.path.exists(OUT):
+def needs_build(out: str = OUT) -> bool:
+    if not os.path.exists(out):
         return True
-    t = os.path.getmtime(OUT)
+    t = os.path.getmtime(out)
     return any(os.path.getmtime(f) > t for f in SOURCES + HEADERS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if force or needs_build():
-        tmp = OUT + f".{os.getpid()}.tmp"
-        r = subprocess.run([NVCC, *FLAGS, *SOURCES, "-o", tmp], capture_output=True, text=True)
+STATS_OUT = os.path.join(HERE, "liburg_stats.so")   # profiling variant (-DURG_STATS event-loop counters)
+
+
+def build(force: bool = False, verbose: bool = False, stats: bool = False) -> str:
+    out = STATS_OUT if stats else OUT
+    if force or needs_build(out):
+        tmp = out + f".{os.getpid()}.tmp"
+        extra = ["-DURG_STATS"] if stats else []
+        r = subprocess.run([NVCC, *FLAGS, *extra, *SOURCES, "-o", tmp], capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed:\n{r.stdout}\n{r.stderr}")
         if verbose:
             print(r.stderr)
-        os.replace(tmp, OUT)
-    return OUT
+        os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":

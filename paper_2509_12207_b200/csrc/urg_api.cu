@@ -17,8 +17,9 @@
 #include "../../include/urg.h"
 #include "urg_layout.h"
 
-extern "C" __global__ void urg_sim_kernel(const uint8_t *blob, const UrgSimParams P, uint32_t *records,
-                                          unsigned long long *agg, unsigned long long *work, long long *err);
+typedef void (*urg_sim_fn)(const uint8_t *blob, const UrgSimParams P, uint32_t *records, unsigned long long *agg,
+                           unsigned long long *work, long long *err);
+const void *urg_sim_kernel_for(uint32_t kind, uint32_t flags, bool kern_q);   // urg_sim.cu
 extern "C" __global__ void urg_philox_kat_kernel(const uint4 *ctr, const uint2 *key, uint4 *out, int n);
 
 struct urg_workload {
@@ -31,6 +32,7 @@ struct urg_workload {
     long long *d_err = nullptr;       // [code, scenario]
     int device = 0;
     int num_sms = 148;
+    bool has_kern_q = false;          // per-kernel factor table present (selects the kernel instantiation)
 };
 
 static thread_local std::string g_err;
@@ -130,6 +132,7 @@ extern "C" urg_status urg_create_workload(const urg_workload_desc *d, urg_worklo
     w->launch_ns = d->launch_ns; w->launch_akb_ns = d->launch_akb_ns;
     w->sync_lo_ns = d->sync_lo_ns; w->sync_hi_ns = d->sync_hi_ns;
     w->jitter_ns = d->jitter_ns; w->rt_bin_ns = d->rt_bin_ns;
+    w->has_kern_q = d->kern_quantiles_q16 != nullptr;
     w->blob.assign(off, 0);
     memcpy(w->blob.data(), &h, sizeof h);
     UrgChainRec *chs = (UrgChainRec *)(w->blob.data() + h.off_chains);
@@ -266,11 +269,13 @@ extern "C" urg_status urg_simulate_batch(const urg_workload *w, const urg_policy
     P.mbar_offset = align16(P.blob_bytes);
     P.snap_offset = align16(P.mbar_offset + 16);
     P.smem_bytes = P.snap_offset + warps * 32 * 8;
-    CUDA_TRY(cudaFuncSetAttribute(urg_sim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem_bytes),
+    const urg_sim_fn fn = (urg_sim_fn)urg_sim_kernel_for(p->kind, p->kind == URG_URGENGO ? p->flags : 0,
+                                                         w->has_kern_q);
+    CUDA_TRY(cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem_bytes),
              "cudaFuncSetAttribute(smem)");
     CUDA_TRY(cudaMemsetAsync(w->d_work, 0, 8, s), "cudaMemsetAsync(work counter)");
-    urg_sim_kernel<<<ctas, warps * 32, P.smem_bytes, s>>>(w->d_blob, P, o->records, (unsigned long long *)o->agg,
-                                                           w->d_work, w->d_err);
+    fn<<<ctas, warps * 32, P.smem_bytes, s>>>(w->d_blob, P, o->records, (unsigned long long *)o->agg, w->d_work,
+                                              w->d_err);
     CUDA_TRY(cudaGetLastError(), "launching urg_sim_kernel");
     return URG_OK;
 }
@@ -335,6 +340,17 @@ extern "C" urg_status urg_miss_ratios(const urg_workload *w, const int64_t *agg_
         if (total) { sum += r; ++used; }
     }
     if (overall_out) *overall_out = used ? sum / used : 0.0;
+    return URG_OK;
+}
+
+// profiling hook (liburg_stats.so, -DURG_STATS): event-loop counters of the launches since the
+// last call -- [single-chain steps, multi-chain steps, Phase C dispatches, 64-bit rebases]
+extern "C" urg_status urg_debug_stats(const urg_workload *w, uint64_t *out4)
+{
+    if (!w || !out4) return fail(URG_EINVAL, "workload and out must not be NULL");
+    CUDA_TRY(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+    CUDA_TRY(cudaMemcpy(out4, w->d_work + 4, 32, cudaMemcpyDeviceToHost), "reading stats");
+    CUDA_TRY(cudaMemset(w->d_work + 4, 0, 32), "clearing stats");
     return URG_OK;
 }
 

@@ -36,8 +36,10 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k)
     return c;
 }
 
-// word(tag, c, i, k) of scenario s (R3-R5)
-__device__ __forceinline__ uint32_t rng_word(uint64_t seed, uint32_t s, uint32_t tag, uint32_t c, uint32_t i,
+// word(tag, c, i, k) of scenario s (R3-R5).  Not inlined: the draws are
+// rare (per arrival, instance, sync call), and an inlined copy lets the compiler
+// hoist ~80 speculative instructions into the per-step path.
+__device__ __noinline__ uint32_t rng_word(uint64_t seed, uint32_t s, uint32_t tag, uint32_t c, uint32_t i,
                                              uint32_t k)
 {
     const uint4 o = philox4x32_10(make_uint4(s, (tag << 24) | (c << 16), i, k >> 2),
@@ -116,7 +118,11 @@ struct Tmpl {   // shared-memory views of the staged template
     const uint32_t *kern_q;
 };
 
-extern "C" __global__ void __launch_bounds__(512, 1)
+// One instantiation per (policy kind, UrgenGo flags, per-kernel factor table present):
+// the policy is uniform over a launch, so its branches are resolved at compile time
+// and code a policy never runs (e.g. the per-kernel Philox draw) is not in its loop.
+template <int KIND, int FLAGS, bool KQ>
+__global__ void __launch_bounds__(512, 1)
 urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t *__restrict__ records,
                unsigned long long *__restrict__ agg, unsigned long long *__restrict__ work,
                long long *__restrict__ err)
@@ -149,15 +155,18 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
     }
     __syncthreads();
 
-    int64_t *snapkey = (int64_t *)(sm + P.snap_offset) + warp * 32;
-    const bool urg = P.kind == K_URGENGO;
-    const bool f_bind = urg && (P.flags & F_BIND), f_delay = urg && (P.flags & F_DELAY),
-               f_early = urg && (P.flags & F_EARLY);
+    int64_t *snapL = (int64_t *)(sm + P.snap_offset) + warp * 32;   // per-warp Phase B laxity snapshot
+    constexpr bool urg = KIND == K_URGENGO;
+    constexpr bool f_bind = urg && (FLAGS & F_BIND), f_delay = urg && (FLAGS & F_DELAY),
+                   f_early = urg && (FLAGS & F_EARLY);
     const int64_t busy_launch = P.launch_ns + (urg ? P.launch_akb_ns : 0);
     const uint32_t stride = P.agg_stride;
     const bool valid = (uint32_t)lane < C;
     const uint32_t c = lane;
     unsigned long long my_launches = 0, my_steps = 0;
+#ifdef URG_STATS
+    unsigned long long st_single = 0, st_multi = 0, st_dispatch = 0, st_rebase = 0;   // profiling build only
+#endif
 
     // static per-chain template data
     UrgChainRec cr = {};
@@ -220,9 +229,10 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         int64_t sync_cost = 0;
         uint32_t akb = 0;
         int64_t L_last = 0;
-        bool head_running = false;
-        int64_t head_ready = 0, head_end = 0;
-        uint32_t head_util = 0;
+        int64_t head_end = INF64;              // end of the running kernel, INF64 when the stream runs nothing
+        int64_t head_ready = 0;                // time the waiting head became head (R20 key)
+        uint32_t head_util = 0;                // util of the running kernel
+        uint32_t head_u = 0xFFFFu;             // util of the waiting head (valid while one waits)
         uint32_t n_total = 0, n_miss = 0, n_early = 0, n_unfin = 0, n_launch = 0, hash = 2166136261u;
         uint64_t sum_rt = 0;
 
@@ -244,234 +254,273 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             if (t_arr < H) { pc = PC_ARRIVE; cpu_next = t_arr; }
         }
 
+        // ---- lane-local pieces of a loop step (R21); used by the warp-wide
+        //      step and by the single-lane ("solo") steps below ----
+        // Phase A for a lane whose running kernel ends at t (R19)
+        auto retire = [&](int64_t t) {
+            ++done;
+            head_end = INF64;
+            if (launched > done) { head_ready = t; head_u = T.kern[cr.kern_base + done].util_permille; }
+            if (pc == PC_SYNC_WAIT && done >= sync_target) { pc = PC_SYNC_RET; cpu_next = t + sync_cost; }
+        };
+        // Phase C start of this lane's waiting head: non-preemptive, exact duration (R4, R19, R20)
+        auto start_head = [&](int64_t t) {
+            uint64_t G = 65536u;
+            if (KQ) G = T.kern_q[rng_word(P.seed, s, URG_TAG_KERN, c, inst, done) >> 20];
+            uint64_t d = ((((uint64_t)T.kern[cr.kern_base + done].nominal_ns * Fg) >> 16) * G) >> 16;
+            d = d < 1 ? 1 : (d > 0xFFFFFFFFull ? 0xFFFFFFFFull : d);
+            head_util = head_u;
+            head_end = t + (int64_t)d;
+        };
+        // Phase B: this lane's CPU program at t, until it has to wait for time to pass.
+        // urgent_m / active_m / snapL are the round snapshot of the other chains (R14, R15).
+        // Returns true if the lane's stream got a new head (Phase C must run).
+        auto phase_b = [&](int64_t t, uint32_t urgent_m, uint32_t active_m) -> bool {
+            bool newhead = false;
+            for (uint32_t guard = 0;; ++guard) {
+                if (guard > (1u << 24)) {
+                    if (atomicCAS((unsigned long long *)err, 0ull, (unsigned long long)ERR_GUARD) == 0ull) err[1] = s;
+                    cpu_next = INF64;
+                    break;
+                }
+                bool next_inst = false;
+                if (pc == PC_SYNC_RET) {   // sync returned: covered kernels leave the AKB
+                    if (urg) akb = launched - sync_target;
+                    if (launched < task_end) pc = PC_ATTEMPT;
+                    else if (++task < cr.num_tasks) {
+                        task_first = task_end;
+                        task_end += T.task[cr.task_base + task].num_kernels;
+                        pc = PC_TASK_START;
+                    } else {   // instance complete (R18, R22)
+                        const int64_t rt = t - t_arr;
+                        if (rt > Dp) ++n_miss;
+                        sum_rt += (uint64_t)rt;
+                        hash = (hash ^ (uint32_t)rt) * 16777619u;
+                        hash = (hash ^ (uint32_t)((uint64_t)rt >> 32)) * 16777619u;
+                        int64_t bin = rt / P.rt_bin_ns;
+                        if (bin > (int64_t)P.rt_bins - 1) bin = P.rt_bins - 1;
+                        atomicAdd(&agg[(uint64_t)c * stride + 5 + bin], 1ull);
+                        next_inst = true;
+                    }
+                }
+                if (pc == PC_ARRIVE) {   // frame arrival / instance start (R6)
+                    ++n_total;
+                    Fg = inst_factor(rng_word(P.seed, s, URG_TAG_INST, c, inst, 0), cr.gpu_sigma_ppm);
+                    Fc = inst_factor(rng_word(P.seed, s, URG_TAG_INST, c, inst, 1), cr.cpu_sigma_ppm);
+                    task = 0; launched = 0; done = 0; sync_ord = 0;
+                    rem_g = cr.gpu_est_total; rem_c = cr.cpu_est_total;
+                    task_first = 0; task_end = T.task[cr.task_base].num_kernels;
+                    pc = PC_TASK_START;
+                }
+                if (pc == PC_TASK_START) {   // new CPU segment: evaluate, early exit
+                    bool exited = false;
+                    if (urg) {
+                        const int64_t lax = t_arr + Dp - rem_g - rem_c - t;   // Eq. 2 (R9)
+                        L_last = lax;
+                        if (f_early && lax < 0) {
+                            akb = 0;
+                            ++n_early; ++n_miss;
+                            hash = (hash ^ 0xFFFFFFFFu) * 16777619u;
+                            hash = (hash ^ 0xFFFFFFFFu) * 16777619u;
+                            pc = PC_DONE;
+                            next_inst = exited = true;
+                        }
+                    }
+                    if (!exited) {
+                        const int64_t e = (int64_t)(((uint64_t)T.task[cr.task_base + task].cpu_nominal_ns * Fc) >> 16);
+                        pc = PC_CPU_DONE;
+                        cpu_next = t + e;
+                        if (e > 0) break;
+                    }
+                }
+                if (next_inst) {   // advance to the next instance of this chain (R6, R7)
+                    ++inst;
+                    t_arr = arrival(inst);
+                    if (t_arr >= H) { pc = PC_DONE; cpu_next = INF64; break; }   // not admitted
+                    pc = PC_ARRIVE;
+                    cpu_next = t_arr;
+                    if (t_arr > t) break;
+                    continue;
+                }
+                if (pc == PC_ENQUEUE) {   // the kernel reaches its stream (R16) + sync decision (R17)
+                    const uint32_t n = launched;
+                    const UrgKernRec kr = T.kern[cr.kern_base + n];
+                    const int64_t est = kr.estimate_ns;
+                    if (launched == done) { head_ready = t; head_u = kr.util_permille; newhead = true; }   // stream was empty
+                    ++launched; ++n_launch;
+                    rem_g -= est;
+                    if (urg) ++akb;
+                    const bool last = launched == task_end;
+                    if (last) rem_c -= T.task[cr.task_base + task].cpu_estimate_ns;
+                    if (n == task_first) { acc = 0; batch_start = task_first; }
+                    int32_t target = -1;
+                    if (P.sync_mode == S_ASYNC) {
+                        if (last) target = (int32_t)launched;
+                    } else if (P.sync_mode == S_EACH) {
+                        target = (int32_t)launched;
+                    } else {
+                        acc += est;
+                        const bool closes = acc >= P.delta_eval_ns;
+                        if (closes) acc = 0;
+                        if (last) { acc = 0; target = (int32_t)launched; }
+                        else if (closes) {
+                            if (P.sync_mode == S_BATCHED) target = (int32_t)launched;
+                            else {   // OVERLAP: wait for the previous batch
+                                const uint32_t prev = batch_start;
+                                batch_start = launched;
+                                if (prev != task_first) target = (int32_t)prev;   // first close: not issued
+                            }
+                        }
+                    }
+                    if (target >= 0) {
+                        sync_target = (uint32_t)target;
+                        sync_cost = P.sync_lo_ns;
+                        if (P.sync_hi_ns > P.sync_lo_ns)
+                            sync_cost += (int64_t)(rng_word(P.seed, s, URG_TAG_SYNC, c, inst, sync_ord) %
+                                                   (uint32_t)(P.sync_hi_ns - P.sync_lo_ns + 1));
+                        ++sync_ord;
+                        if (done >= sync_target) {
+                            pc = PC_SYNC_RET;
+                            cpu_next = t + sync_cost;
+                            if (sync_cost > 0) break;
+                            continue;
+                        }
+                        pc = PC_SYNC_WAIT;
+                        cpu_next = INF64;
+                        break;
+                    }
+                    pc = PC_ATTEMPT;
+                }
+                if (pc == PC_CPU_DONE || pc == PC_ATTEMPT) {   // launch attempt for kernel n = launched (R14-R16)
+                    int64_t lax = 0;
+                    if (urg) { lax = t_arr + Dp - rem_g - rem_c - t; L_last = lax; }
+                    const bool own_urgent = lax >= 0 && lax <= P.lax_threshold_ns;
+                    if (f_delay && !own_urgent && (urgent_m & ~(1u << lane)) &&
+                        T.kern[cr.kern_base + launched].util_permille >= P.util_exempt) {
+                        pc = PC_ATTEMPT;
+                        cpu_next = t + P.sleep_ns;
+                        break;
+                    }
+                    if (launched == task_first) {   // task-level stream binding
+                        if (KIND == K_STATIC) level = static_level;
+                        else if (!f_bind) level = P.num_prio - 1;
+                        else if (own_urgent) level = 0;
+                        else {
+                            const int64_t own = urgency_key(lax);
+                            uint32_t mm = active_m & ~(1u << lane);
+                            const uint32_t n_r = 1 + __popc(mm);
+                            uint32_t r = 1;
+                            while (mm) {
+                                const int o = __ffs(mm) - 1;
+                                mm &= mm - 1;
+                                const int64_t k = urgency_key(snapL[o]);
+                                r += (k > own || (k == own && o < lane)) ? 1u : 0u;
+                            }
+                            level = P.num_prio <= 2 ? P.num_prio - 1
+                                    : n_r <= 1      ? 1 + (P.num_prio - 2) / 2
+                                                    : 1 + (uint32_t)(((uint64_t)(r - 1) * (P.num_prio - 2)) / (n_r - 1));
+                        }
+                    }
+                    pc = PC_ENQUEUE;
+                    cpu_next = t + busy_launch;
+                    if (busy_launch > 0) break;
+                    continue;
+                }
+                break;   // PC_SYNC_WAIT / PC_DONE: nothing to do at t
+            }
+            return newhead;
+        };
+        // Round snapshot of the chains' (AKB non-empty, last laxity) for Phase B (R14, R15, R21).
+        // `may_bind`: this lane can reach a task's first launch in this phase (else the
+        // binding snapshot is not needed).
+        auto snapshot = [&](bool may_bind, uint32_t &urgent_m, uint32_t &active_m) {
+            urgent_m = 0; active_m = 0;
+            if (f_delay) urgent_m = __ballot_sync(FULL, akb > 0 && L_last >= 0 && L_last <= P.lax_threshold_ns);
+            if (f_bind && __any_sync(FULL, may_bind)) {
+                active_m = __ballot_sync(FULL, akb > 0);
+                snapL[lane] = L_last;
+                __syncwarp();
+            }
+        };
+        // a due lane can bind in this phase unless it is mid-task and the launch cost
+        // makes it yield before reaching the next task's first kernel
+        auto can_bind = [&]() -> bool {
+            return !(busy_launch > 0 && ((pc == PC_ENQUEUE && launched + 1 < task_end) ||
+                                         (pc == PC_ATTEMPT && launched != task_first)));
+        };
+
         // ---- A2-A10: the event loop (R21) ----
+        // Warp-uniform: t_prev (time of the previous loop step) and `used`, the util
+        // per-mille of the running kernels (kept incrementally).
         int64_t t_prev = -1;
+        uint32_t used = 0;
         for (;;) {
-            const int64_t mine = head_running && head_end < cpu_next ? head_end : cpu_next;
-            const int64_t t = warp_min_nonneg(mine);
+            // A2: next event time.  Every lane's next event is strictly after t_prev, so
+            // the warp minimum is taken on the 32-bit distance (one REDUX); distances that
+            // do not fit 32 bits saturate and fall back to the exact 64-bit minimum.
+            const int64_t mine = head_end < cpu_next ? head_end : cpu_next;
+            const uint64_t dl = (uint64_t)mine - (uint64_t)t_prev;   // exact when mine > t_prev
+            const uint32_t d32 = mine <= t_prev ? 0u : (dl >= 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)dl);
+            const uint32_t m = __reduce_min_sync(FULL, d32);
+            int64_t t;
+            if (m == 0xFFFFFFFFu) t = warp_min_nonneg(mine);
+            else t = t_prev + m;
             if (t > H_stop) break;
-            if (t <= t_prev) {   // time must advance (invariant); report and stop this scenario
+            if (m == 0u) {   // time must advance (invariant); report and stop this scenario
                 if (lane == 0 && atomicCAS((unsigned long long *)err, 0ull, (unsigned long long)ERR_TIME) == 0ull)
                     err[1] = s;
                 break;
             }
             t_prev = t;
             ++my_steps;
+            bool dirty = false;                 // GPU state changed: Phase C must run
 
             // Phase A: retire (R21, R19)
-            const bool ret = head_running && head_end == t;
-            if (__any_sync(FULL, ret) && ret) {
-                ++done;
-                head_running = false;
-                if (launched > done) head_ready = t;            // next kernel becomes head
-                if (pc == PC_SYNC_WAIT && done >= sync_target) { pc = PC_SYNC_RET; cpu_next = t + sync_cost; }
+            const bool ret = head_end == t;
+            if (__any_sync(FULL, ret)) {
+                dirty = true;
+                used -= __reduce_add_sync(FULL, ret ? head_util : 0u);
+                if (ret) retire(t);
             }
 
             // Phase B: CPU steps of every chain due at t, against the round snapshot
             const bool due = cpu_next == t;
             if (__any_sync(FULL, due)) {
-                uint32_t active_m = 0, urgent_m = 0;
-                if (urg) {
-                    active_m = __ballot_sync(FULL, akb > 0);
-                    urgent_m = __ballot_sync(FULL, akb > 0 && L_last >= 0 && L_last <= P.lax_threshold_ns);
-                    if (f_bind) { snapkey[lane] = urgency_key(L_last); __syncwarp(); }
-                }
-                if (due) {
-                    for (uint32_t guard = 0;; ++guard) {
-                        if (guard > (1u << 24)) {
-                            if (atomicCAS((unsigned long long *)err, 0ull, (unsigned long long)ERR_GUARD) == 0ull)
-                                err[1] = s;
-                            cpu_next = INF64;
-                            break;
-                        }
-                        bool yield = false;
-                        switch (pc) {
-                        case PC_ARRIVE: {   // frame arrival / instance start (R6)
-                            ++n_total;
-                            const uint4 w = philox4x32_10(make_uint4(s, (URG_TAG_INST << 24) | (c << 16), inst, 0),
-                                                          make_uint2((uint32_t)P.seed, (uint32_t)(P.seed >> 32)));
-                            Fg = inst_factor(w.x, cr.gpu_sigma_ppm);
-                            Fc = inst_factor(w.y, cr.cpu_sigma_ppm);
-                            task = 0; launched = 0; done = 0; sync_ord = 0;
-                            rem_g = cr.gpu_est_total; rem_c = cr.cpu_est_total;
-                            task_first = 0; task_end = T.task[cr.task_base].num_kernels;
-                            pc = PC_TASK_START;
-                            break;
-                        }
-                        case PC_TASK_START: {   // new CPU segment: evaluate, early exit
-                            if (urg) {
-                                const int64_t lax = t_arr + Dp - rem_g - rem_c - t;   // Eq. 2 (R9)
-                                L_last = lax;
-                                if (f_early && lax < 0) {
-                                    akb = 0;
-                                    ++n_early; ++n_miss;
-                                    hash = (hash ^ 0xFFFFFFFFu) * 16777619u;
-                                    hash = (hash ^ 0xFFFFFFFFu) * 16777619u;
-                                    pc = PC_DONE;   // -> next instance below
-                                    goto next_instance;
-                                }
-                            }
-                            {
-                                const int64_t e =
-                                    (int64_t)(((uint64_t)T.task[cr.task_base + task].cpu_nominal_ns * Fc) >> 16);
-                                pc = PC_CPU_DONE;
-                                cpu_next = t + e;
-                                yield = e > 0;
-                            }
-                            break;
-                        }
-                        case PC_CPU_DONE:
-                        case PC_ATTEMPT: {   // launch attempt for kernel n = launched (R14, R15, R16)
-                            int64_t lax = 0;
-                            if (urg) { lax = t_arr + Dp - rem_g - rem_c - t; L_last = lax; }
-                            const bool own_urgent = lax >= 0 && lax <= P.lax_threshold_ns;
-                            if (f_delay && !own_urgent && (urgent_m & ~(1u << lane)) &&
-                                T.kern[cr.kern_base + launched].util_permille >= P.util_exempt) {
-                                pc = PC_ATTEMPT;
-                                cpu_next = t + P.sleep_ns;
-                                yield = true;
-                                break;
-                            }
-                            if (launched == task_first) {   // task-level stream binding
-                                if (P.kind == K_STATIC) level = static_level;
-                                else if (!f_bind) level = P.num_prio - 1;
-                                else if (own_urgent) level = 0;
-                                else {
-                                    const int64_t own = urgency_key(lax);
-                                    uint32_t m = active_m & ~(1u << lane);
-                                    const uint32_t n_r = 1 + __popc(m);
-                                    uint32_t r = 1;
-                                    while (m) {
-                                        const int o = __ffs(m) - 1;
-                                        m &= m - 1;
-                                        const int64_t k = snapkey[o];
-                                        r += (k > own || (k == own && o < lane)) ? 1u : 0u;
-                                    }
-                                    level = P.num_prio <= 2 ? P.num_prio - 1
-                                            : n_r <= 1      ? 1 + (P.num_prio - 2) / 2
-                                                            : 1 + (uint32_t)(((uint64_t)(r - 1) * (P.num_prio - 2)) / (n_r - 1));
-                                }
-                            }
-                            pc = PC_ENQUEUE;
-                            cpu_next = t + busy_launch;
-                            yield = busy_launch > 0;
-                            break;
-                        }
-                        case PC_ENQUEUE: {   // the kernel reaches its stream (R16) + sync decision (R17)
-                            const uint32_t n = launched;
-                            const int64_t est = T.kern[cr.kern_base + n].estimate_ns;
-                            if (launched == done) head_ready = t;   // stream was empty: head now
-                            ++launched; ++n_launch;
-                            rem_g -= est;
-                            if (urg) ++akb;
-                            const bool last = launched == task_end;
-                            if (last) rem_c -= T.task[cr.task_base + task].cpu_estimate_ns;
-                            if (n == task_first) { acc = 0; batch_start = task_first; }
-                            int32_t target = -1;
-                            if (P.sync_mode == S_ASYNC) {
-                                if (last) target = (int32_t)launched;
-                            } else if (P.sync_mode == S_EACH) {
-                                target = (int32_t)launched;
-                            } else {
-                                acc += est;
-                                const bool closes = acc >= P.delta_eval_ns;
-                                if (closes) acc = 0;
-                                if (last) { acc = 0; target = (int32_t)launched; }
-                                else if (closes) {
-                                    if (P.sync_mode == S_BATCHED) target = (int32_t)launched;
-                                    else {   // OVERLAP: wait for the previous batch
-                                        const uint32_t prev = batch_start;
-                                        batch_start = launched;
-                                        if (prev != task_first) target = (int32_t)prev;   // first close: not issued
-                                    }
-                                }
-                            }
-                            if (target >= 0) {
-                                sync_target = (uint32_t)target;
-                                sync_cost = P.sync_lo_ns;
-                                if (P.sync_hi_ns > P.sync_lo_ns)
-                                    sync_cost += (int64_t)(rng_word(P.seed, s, URG_TAG_SYNC, c, inst, sync_ord) %
-                                                           (uint32_t)(P.sync_hi_ns - P.sync_lo_ns + 1));
-                                ++sync_ord;
-                                if (done >= sync_target) { pc = PC_SYNC_RET; cpu_next = t + sync_cost; yield = sync_cost > 0; }
-                                else { pc = PC_SYNC_WAIT; cpu_next = INF64; yield = true; }
-                            } else {
-                                pc = PC_ATTEMPT;
-                            }
-                            break;
-                        }
-                        case PC_SYNC_RET: {   // sync returned: covered kernels leave the AKB
-                            if (urg) akb = launched - sync_target;
-                            if (launched < task_end) { pc = PC_ATTEMPT; break; }
-                            ++task;
-                            if (task < cr.num_tasks) {
-                                task_first = task_end;
-                                task_end += T.task[cr.task_base + task].num_kernels;
-                                pc = PC_TASK_START;
-                                break;
-                            }
-                            {   // instance complete (R18, R22)
-                                const int64_t rt = t - t_arr;
-                                if (rt > Dp) ++n_miss;
-                                sum_rt += (uint64_t)rt;
-                                hash = (hash ^ (uint32_t)rt) * 16777619u;
-                                hash = (hash ^ (uint32_t)((uint64_t)rt >> 32)) * 16777619u;
-                                int64_t bin = rt / P.rt_bin_ns;
-                                if (bin > (int64_t)P.rt_bins - 1) bin = P.rt_bins - 1;
-                                atomicAdd(&agg[(uint64_t)c * stride + 5 + bin], 1ull);
-                            }
-                            goto next_instance;
-                        }
-                        default:
-                            yield = true;
-                            break;
-                        }
-                        if (yield) break;
-                        continue;
-                    next_instance:
-                        ++inst;
-                        t_arr = arrival(inst);
-                        if (t_arr >= H) { pc = PC_DONE; cpu_next = INF64; break; }   // not admitted (R7)
-                        pc = PC_ARRIVE;
-                        cpu_next = t_arr;
-                        if (t_arr > t) break;
-                    }
-                }
-                __syncwarp();
+#ifdef URG_STATS
+                ++st_multi;
+#endif
+                uint32_t urgent_m = 0, active_m = 0;
+                if (urg) snapshot(due && can_bind(), urgent_m, active_m);
+                bool nh = false;
+                if (due) nh = phase_b(t, urgent_m, active_m);
+                if (__any_sync(FULL, nh)) dirty = true;
             }
 
-            // Phase C: dispatch waiting stream heads by (level, ready, chain) under capacity (R20)
-            const bool waiting = launched > done && !head_running;
-            uint32_t cand = __ballot_sync(FULL, waiting);
-            if (cand) {
-                uint32_t used = __reduce_add_sync(FULL, head_running ? head_util : 0u);
-                UrgKernRec hk;
-                uint32_t u = 0xFFFFu;
-                if (waiting) { hk = T.kern[cr.kern_base + done]; u = hk.util_permille; }
-                const uint32_t minu = __reduce_min_sync(FULL, u);
-                if (used + minu <= 1000u) {
-                    const uint64_t key = ((uint64_t)level << 56) | ((uint64_t)head_ready << 5) | (uint64_t)lane;
-                    while (cand) {
-                        const bool in = (cand >> lane) & 1u;
+            // Phase C: dispatch waiting stream heads by (level, ready, chain) under capacity (R20).
+            // Runs only when a kernel retired or a stream got a new head: otherwise every
+            // waiting head was already found not to fit and `used` has not decreased.
+            // The greedy scan in key order starts, each time, the smallest-key head that
+            // fits the capacity left (heads that do not fit stay unfit as `used` grows).
+            if (dirty) {
+#ifdef URG_STATS
+                ++st_dispatch;
+#endif
+                bool waiting = launched > done && head_end == INF64;
+                for (;;) {
+                    const uint32_t fit = __ballot_sync(FULL, waiting && used + head_u <= 1000u);
+                    if (!fit) break;
+                    int wl;
+                    if ((fit & (fit - 1)) == 0) wl = __ffs(fit) - 1;
+                    else {
+                        const bool in = (fit >> lane) & 1u;
+                        const uint64_t key = ((uint64_t)level << 56) | ((uint64_t)head_ready << 5) | (uint64_t)lane;
                         const uint32_t hi = in ? (uint32_t)(key >> 32) : 0xFFFFFFFFu;
                         const uint32_t mh = __reduce_min_sync(FULL, hi);
                         const uint32_t ml = __reduce_min_sync(FULL, (in && hi == mh) ? (uint32_t)key : 0xFFFFFFFFu);
-                        const int wl = (int)(ml & 31u);
-                        const uint32_t uw = __shfl_sync(FULL, u, wl);
-                        if (used + uw <= 1000u) {
-                            used += uw;
-                            if (lane == wl) {   // start: non-preemptive, exact duration (R4, R19)
-                                uint64_t G = 65536u;
-                                if (T.kern_q) G = T.kern_q[rng_word(P.seed, s, URG_TAG_KERN, c, inst, done) >> 20];
-                                uint64_t d = ((((uint64_t)hk.nominal_ns * Fg) >> 16) * G) >> 16;
-                                d = d < 1 ? 1 : (d > 0xFFFFFFFFull ? 0xFFFFFFFFull : d);
-                                head_running = true;
-                                head_util = uw;
-                                head_end = t + (int64_t)d;
-                            }
-                        }
-                        cand &= ~(1u << wl);
+                        wl = (int)(ml & 31u);
                     }
+                    used += __shfl_sync(FULL, head_u, wl);
+                    if (lane == wl) { start_head(t); waiting = false; }
                 }
             }
         }
@@ -502,5 +551,26 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
     if (lane == 0) {
         atomicAdd(&agg[(uint64_t)C * stride + 0], my_launches);
         atomicAdd(&agg[(uint64_t)C * stride + 1], my_steps);
+#ifdef URG_STATS
+        atomicAdd(&work[4], st_single); atomicAdd(&work[5], st_multi);
+        atomicAdd(&work[6], st_dispatch); atomicAdd(&work[7], st_rebase);
+#endif
     }
+}
+
+// ---------------------------------------------------------------------------
+// instantiation table (host side picks one per launch; see urg_api.cu)
+// ---------------------------------------------------------------------------
+#define URG_I(K, F)                                                                                  \
+    (const void *)urg_sim_kernel<K, F, false>, (const void *)urg_sim_kernel<K, F, true>
+static const void *const g_sim_kernels[10][2] = {
+    {URG_I(K_FIFO, 0)},    {URG_I(K_STATIC, 0)},  {URG_I(K_URGENGO, 0)}, {URG_I(K_URGENGO, 1)},
+    {URG_I(K_URGENGO, 2)}, {URG_I(K_URGENGO, 3)}, {URG_I(K_URGENGO, 4)}, {URG_I(K_URGENGO, 5)},
+    {URG_I(K_URGENGO, 6)}, {URG_I(K_URGENGO, 7)}};
+#undef URG_I
+
+const void *urg_sim_kernel_for(uint32_t kind, uint32_t flags, bool kern_q)
+{
+    const uint32_t row = kind == K_FIFO ? 0 : kind == K_STATIC ? 1 : 2 + (flags & 7u);
+    return g_sim_kernels[row][kern_q ? 1 : 0];
 }

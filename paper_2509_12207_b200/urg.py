@@ -75,10 +75,12 @@ def lib():
     """Load liburg.so (built by paper_2509_12207_b200.build / __graft_entry__.build)."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
-            raise RuntimeError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+        # URG_LIB selects another build of the same library (liburg_stats.so, the profiling variant)
+        path = os.environ.get("URG_LIB") or LIB_PATH
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
                                "(the CUDA path has no CPU fallback)")
-        L = ct.CDLL(LIB_PATH)
+        L = ct.CDLL(path)
         L.urg_create_workload.restype = ct.c_int
         L.urg_create_workload.argtypes = [ct.POINTER(WorkloadDesc), ct.POINTER(ct.c_void_p)]
         L.urg_destroy_workload.restype = None
@@ -96,6 +98,9 @@ def lib():
         L.urg_miss_ratios.argtypes = [ct.c_void_p, ct.c_void_p, ct.c_void_p, ct.POINTER(ct.c_double)]
         L.urg_last_error.restype = ct.c_char_p
         L.urg_last_error.argtypes = []
+        if hasattr(L, "urg_debug_stats"):
+            L.urg_debug_stats.restype = ct.c_int
+            L.urg_debug_stats.argtypes = [ct.c_void_p, ct.c_void_p]
         L.urg_debug_philox.restype = ct.c_int
         L.urg_debug_philox.argtypes = [ct.c_void_p, ct.c_void_p, ct.c_void_p, ct.c_int, ct.c_void_p]
         _lib = L
