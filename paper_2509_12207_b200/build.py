@@ -38,6 +38,17 @@ def build(force: bool = False, verbose: bool = False, stats: bool = False) -> st
     return out
 
 
+def build_variant(name: str, defines) -> str:
+    """An experiment build liburg_<name>.so with extra -D flags (A/B timing via URG_LIB)."""
+    out = os.path.join(HERE, f"liburg_{name}.so")
+    tmp = out + f".{os.getpid()}.tmp"
+    r = subprocess.run([NVCC, *FLAGS, *[f"-D{d}" for d in defines], *SOURCES, "-o", tmp], capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc failed:\n{r.stdout}\n{r.stderr}")
+    os.replace(tmp, out)
+    return out
+
+
 if __name__ == "__main__":
     build(force=True, verbose=True)
     print(OUT)

@@ -19,7 +19,7 @@
 
 typedef void (*urg_sim_fn)(const uint8_t *blob, const UrgSimParams P, uint32_t *records, unsigned long long *agg,
                            unsigned long long *work, long long *err);
-const void *urg_sim_kernel_for(uint32_t kind, uint32_t flags, bool kern_q);   // urg_sim.cu
+const void *urg_sim_kernel_for(uint32_t kind, uint32_t flags, bool kern_q, bool wide);   // urg_sim.cu
 extern "C" __global__ void urg_philox_kat_kernel(const uint4 *ctr, const uint2 *key, uint4 *out, int n);
 
 struct urg_workload {
@@ -236,20 +236,34 @@ static void fill_params(const urg_workload *w, const urg_policy *p, const urg_ba
     P.ftight_permille = b->ftight_permille; P.tight_explicit = b->tight_explicit; P.tight_mask = b->tight_mask;
 }
 
-// launch geometry: one warp per scenario in flight, persistent CTAs over the SMs
-static void geometry(const urg_workload *w, uint64_t count, int &warps, int &ctas)
+// Launch geometry: one warp per scenario in flight, persistent CTAs pulling scenarios
+// from an atomic counter.  Few scenarios: spread them one warp each over all SMs
+// (the batch is latency-bound: fewer warps per scheduler, same per-scenario time).
+// Many scenarios: the largest CTA the kernel allows, as many CTAs per SM as
+// registers and shared memory (the staged template is per CTA) let reside.
+static urg_status geometry(const urg_workload *w, const void *fn, uint64_t count, uint32_t smem_fixed, int &warps,
+                           int &ctas, uint32_t &smem)
 {
-    const char *ew = getenv("URG_WARPS_PER_CTA");
-    int per_sm_target = 16;                                 // warps resident per SM when work is plentiful
-    if (const char *es = getenv("URG_WARPS_PER_SM")) per_sm_target = atoi(es);
-    uint64_t need = (count + (uint64_t)w->num_sms - 1) / (uint64_t)w->num_sms;   // warps per SM to hold all
-    warps = (int)(need < (uint64_t)per_sm_target ? need : (uint64_t)per_sm_target);
-    if (ew) warps = atoi(ew);
+    cudaFuncAttributes fa;
+    CUDA_TRY(cudaFuncGetAttributes(&fa, fn), "cudaFuncGetAttributes");
+    int max_w = fa.maxThreadsPerBlock / 32;
+    if (max_w > 32) max_w = 32;
+    const uint64_t need = (count + (uint64_t)w->num_sms - 1) / (uint64_t)w->num_sms;   // warps per SM to hold all
+    warps = (int)(need < (uint64_t)max_w ? need : (uint64_t)max_w);
+    if (const char *ew = getenv("URG_WARPS_PER_CTA")) warps = atoi(ew);
     if (warps < 1) warps = 1;
-    if (warps > 16) warps = 16;
+    if (warps > max_w) warps = max_w;
+    smem = smem_fixed + (uint32_t)warps * 32u * 8u;
+    CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+             "cudaFuncSetAttribute(smem)");
+    int per_sm = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, warps * 32, smem), "cudaOccupancy");
+    if (per_sm < 1) return fail(URG_ERANGE, "urg_sim_kernel cannot reside on an SM with %u B of shared memory", smem);
     const uint64_t blocks_needed = (count + warps - 1) / warps;
-    ctas = (int)(blocks_needed < (uint64_t)w->num_sms ? blocks_needed : (uint64_t)w->num_sms);
+    const uint64_t resident = (uint64_t)w->num_sms * (uint64_t)per_sm;
+    ctas = (int)(blocks_needed < resident ? blocks_needed : resident);
     if (ctas < 1) ctas = 1;
+    return URG_OK;
 }
 
 extern "C" urg_status urg_simulate_batch(const urg_workload *w, const urg_policy *p, const urg_batch *b,
@@ -263,16 +277,18 @@ extern "C" urg_status urg_simulate_batch(const urg_workload *w, const urg_policy
     cudaStream_t s = (cudaStream_t)cuda_stream;
     UrgSimParams P;
     fill_params(w, p, b, P);
-    int warps, ctas;
-    geometry(w, b->scenario_count, warps, ctas);
+    // throughput build once the batch needs more than 16 warps per SM (bench: paper11's 1000
+    // scenarios use the latency build, configs[2]-[4]'s 1e5-1e8 the throughput build)
+    bool wide = b->scenario_count > (uint64_t)w->num_sms * 16u;
+    if (const char *ev = getenv("URG_WIDE")) wide = atoi(ev) != 0;
+    const urg_sim_fn fn = (urg_sim_fn)urg_sim_kernel_for(p->kind, p->kind == URG_URGENGO ? p->flags : 0,
+                                                         w->has_kern_q, wide);
     P.blob_bytes = (uint32_t)w->blob.size();
     P.mbar_offset = align16(P.blob_bytes);
     P.snap_offset = align16(P.mbar_offset + 16);
-    P.smem_bytes = P.snap_offset + warps * 32 * 8;
-    const urg_sim_fn fn = (urg_sim_fn)urg_sim_kernel_for(p->kind, p->kind == URG_URGENGO ? p->flags : 0,
-                                                         w->has_kern_q);
-    CUDA_TRY(cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem_bytes),
-             "cudaFuncSetAttribute(smem)");
+    int warps, ctas;
+    st = geometry(w, (const void *)fn, b->scenario_count, P.snap_offset, warps, ctas, P.smem_bytes);
+    if (st != URG_OK) return st;
     CUDA_TRY(cudaMemsetAsync(w->d_work, 0, 8, s), "cudaMemsetAsync(work counter)");
     fn<<<ctas, warps * 32, P.smem_bytes, s>>>(w->d_blob, P, o->records, (unsigned long long *)o->agg, w->d_work,
                                               w->d_err);

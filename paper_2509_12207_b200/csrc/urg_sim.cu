@@ -17,7 +17,9 @@
 enum { K_FIFO = 0, K_STATIC = 1, K_URGENGO = 2 };
 enum { F_BIND = 1, F_DELAY = 2, F_EARLY = 4 };
 enum { S_ASYNC = 0, S_EACH = 1, S_BATCHED = 2, S_OVERLAP = 3 };
-enum { PC_ARRIVE = 0, PC_TASK_START, PC_CPU_DONE, PC_ATTEMPT, PC_ENQUEUE, PC_SYNC_WAIT, PC_SYNC_RET, PC_DONE };
+// lane program counter; the per-launch states come first so one range test skips the
+// per-task / per-instance states on the common path
+enum { PC_ENQUEUE = 0, PC_ATTEMPT, PC_CPU_DONE, PC_SYNC_RET, PC_ARRIVE, PC_TASK_START, PC_SYNC_WAIT, PC_DONE };
 enum { ERR_TIME = 1, ERR_GUARD = 2 };
 
 // ---------------------------------------------------------------------------
@@ -121,8 +123,12 @@ struct Tmpl {   // shared-memory views of the staged template
 // One instantiation per (policy kind, UrgenGo flags, per-kernel factor table present):
 // the policy is uniform over a launch, so its branches are resolved at compile time
 // and code a policy never runs (e.g. the per-kernel Philox draw) is not in its loop.
-template <int KIND, int FLAGS, bool KQ>
-__global__ void __launch_bounds__(512, 1)
+//
+// WIDE: the throughput build (1024 threads per CTA, so <= 64 registers and 32 warps per
+// SM) for batches that fill the GPU; otherwise the latency build (512 threads, ~100
+// registers), faster per scenario when there are fewer scenarios than warp slots.
+template <int KIND, int FLAGS, bool KQ, bool WIDE>
+__global__ void __launch_bounds__(WIDE ? 1024 : 512, 1)
 urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t *__restrict__ records,
                unsigned long long *__restrict__ agg, unsigned long long *__restrict__ work,
                long long *__restrict__ err)
@@ -283,6 +289,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     cpu_next = INF64;
                     break;
                 }
+                if ((uint32_t)(pc - PC_SYNC_RET) <= (uint32_t)(PC_TASK_START - PC_SYNC_RET)) {
                 bool next_inst = false;
                 if (pc == PC_SYNC_RET) {   // sync returned: covered kernels leave the AKB
                     if (urg) akb = launched - sync_target;
@@ -341,6 +348,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     cpu_next = t_arr;
                     if (t_arr > t) break;
                     continue;
+                }
                 }
                 if (pc == PC_ENQUEUE) {   // the kernel reaches its stream (R16) + sync decision (R17)
                     const uint32_t n = launched;
@@ -473,17 +481,16 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             }
             t_prev = t;
             ++my_steps;
-            bool dirty = false;                 // GPU state changed: Phase C must run
 
             // Phase A: retire (R21, R19)
             const bool ret = head_end == t;
-            if (__any_sync(FULL, ret)) {
-                dirty = true;
+            bool dirty = __any_sync(FULL, ret);   // GPU state changed: Phase C must run
+            if (dirty) {
                 used -= __reduce_add_sync(FULL, ret ? head_util : 0u);
                 if (ret) retire(t);
             }
 
-            // Phase B: CPU steps of every chain due at t, against the round snapshot
+            // Phase B: CPU steps of every chain due at t, against the round snapshot (R21)
             const bool due = cpu_next == t;
             if (__any_sync(FULL, due)) {
 #ifdef URG_STATS
@@ -493,8 +500,9 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                 if (urg) snapshot(due && can_bind(), urgent_m, active_m);
                 bool nh = false;
                 if (due) nh = phase_b(t, urgent_m, active_m);
-                if (__any_sync(FULL, nh)) dirty = true;
+                dirty |= __any_sync(FULL, nh);
             }
+
 
             // Phase C: dispatch waiting stream heads by (level, ready, chain) under capacity (R20).
             // Runs only when a kernel retired or a stream got a new head: otherwise every
@@ -521,6 +529,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     }
                     used += __shfl_sync(FULL, head_u, wl);
                     if (lane == wl) { start_head(t); waiting = false; }
+                    if ((fit & (fit - 1)) == 0) break;   // the others did not fit before; `used` only grew
                 }
             }
         }
@@ -562,15 +571,16 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
 // instantiation table (host side picks one per launch; see urg_api.cu)
 // ---------------------------------------------------------------------------
 #define URG_I(K, F)                                                                                  \
-    (const void *)urg_sim_kernel<K, F, false>, (const void *)urg_sim_kernel<K, F, true>
-static const void *const g_sim_kernels[10][2] = {
+    (const void *)urg_sim_kernel<K, F, false, false>, (const void *)urg_sim_kernel<K, F, true, false>,     \
+        (const void *)urg_sim_kernel<K, F, false, true>, (const void *)urg_sim_kernel<K, F, true, true>
+static const void *const g_sim_kernels[10][4] = {
     {URG_I(K_FIFO, 0)},    {URG_I(K_STATIC, 0)},  {URG_I(K_URGENGO, 0)}, {URG_I(K_URGENGO, 1)},
     {URG_I(K_URGENGO, 2)}, {URG_I(K_URGENGO, 3)}, {URG_I(K_URGENGO, 4)}, {URG_I(K_URGENGO, 5)},
     {URG_I(K_URGENGO, 6)}, {URG_I(K_URGENGO, 7)}};
 #undef URG_I
 
-const void *urg_sim_kernel_for(uint32_t kind, uint32_t flags, bool kern_q)
+const void *urg_sim_kernel_for(uint32_t kind, uint32_t flags, bool kern_q, bool wide)
 {
     const uint32_t row = kind == K_FIFO ? 0 : kind == K_STATIC ? 1 : 2 + (flags & 7u);
-    return g_sim_kernels[row][kern_q ? 1 : 0];
+    return g_sim_kernels[row][(kern_q ? 1 : 0) + (wide ? 2 : 0)];
 }

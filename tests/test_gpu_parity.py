@@ -198,3 +198,43 @@ def test_host_variant_matches_device():
     tot = rec[:, :, 0].astype(np.int64).sum(0)
     miss = rec[:, :, 1].astype(np.int64).sum(0)
     assert overall == O.overall_miss_ratio(miss, tot)
+
+
+@pytest.fixture
+def wide_build(monkeypatch):
+    """Force the throughput instantiations (1024-thread CTAs, <= 64 registers) that
+    urg_simulate_batch picks for batches larger than 16 warps per SM."""
+    monkeypatch.setenv("URG_WIDE", "1")
+    yield
+
+
+@pytest.mark.parametrize("name", ["urgengo", "fifo", "static"])
+def test_wide_build_paper11(wide_build, name):
+    cfg = get_config("paper11")
+    b = Batch(seed=cfg.batch.seed, scenario_begin=777, scenario_count=40, horizon_ns=2_000 * MS, ftight_permille=400)
+    both(cfg.workload(), cfg.policies[name], b, f"wide {name}")
+
+
+def test_wide_build_heavy_tail_and_toy(wide_build):
+    lth = get_config("paper11").policies["urgengo"].lax_threshold_ns
+    both(_paper11_heavy(), Policy(kind=URGENGO, flags=F_ALL, sync_mode=SYNC_OVERLAP, lax_threshold_ns=lth),
+         Batch(seed=0x5EED0004, scenario_count=16, horizon_ns=3_000 * MS, ftight_permille=400), "wide jitter")
+    for mode in (SYNC_ASYNC, SYNC_EACH, SYNC_BATCHED, SYNC_OVERLAP):
+        for f in (0, 3, 7):
+            both(toy2(), Policy(kind=URGENGO, flags=f, sync_mode=mode, lax_threshold_ns=10 * MS),
+                 get_config("toy2").batch, f"wide toy2 {f} {mode}")
+
+
+def test_throughput_batch_sampled():
+    """A batch large enough to select the throughput build by itself (> 16 warps per SM):
+    configs[4]'s workload, 4000 scenarios x 200 ms, sampled scenarios vs the oracle."""
+    cfg = get_config("scaleout")
+    w, p = cfg.workload(), cfg.policies["urgengo"]
+    b = Batch(seed=cfg.batch.seed, scenario_count=4000, horizon_ns=200 * MS, ftight_permille=400)
+    r, a = gpu_run(w, p, b)
+    recon = agg_from_records(r, w.num_chains, w.rt_bins)
+    assert a[-2] == recon[-2]
+    for s in [0, 1, 2047, 3998, 3999]:
+        o = O.run(w, p, Batch(seed=b.seed, scenario_begin=s, scenario_count=1, horizon_ns=b.horizon_ns,
+                              ftight_permille=400))
+        assert np.array_equal(o.records[0], r[s]), f"scenario {s}"
