@@ -248,9 +248,16 @@ def main():
     pool = oracle_pool(a.config, a.policy, _cores()) if want_cpu else None   # fork before CUDA init
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device (the product path has no CPU fallback)")
-    torch.cuda.set_device(local)
+    # one process per GPU; URG_BENCH_BACKEND=gloo (test only) lets several ranks share one
+    # device so the N > 1 path can be exercised on a single-GPU box
+    backend = os.environ.get("URG_BENCH_BACKEND", "nccl")
+    dev = local % torch.cuda.device_count() if backend != "nccl" else local
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     n = world
 
     cfg, w, p, b0 = workload_batch(a)
@@ -285,7 +292,7 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    with Clocks(local) as clk:
+    with Clocks(dev) as clk:
         for i in range(a.steps):
             flush.fill_(i & 0xFF)            # L2 flush outside the timed events
             step(evs[i])
@@ -345,7 +352,7 @@ def main():
     assert np.array_equal(host_rec, rec.cpu().numpy().view(np.uint32)), "host-buffer path differs from device path"
 
     # ---- roofline: issue-bound event loop ----
-    props = torch.cuda.get_device_properties(local)
+    props = torch.cuda.get_device_properties(dev)
     sms = props.multi_processor_count
     peak_mhz = clocks["sm_max_mhz"] or 1965.0
     # per-rank algorithmic instruction count of one launch of urg_sim_kernel
