@@ -23,7 +23,7 @@ _LIB = os.path.join(_HERE, "liburg_oracle.so")
 
 TRACE_KINDS = {1: "STEP", 2: "INST_START", 3: "TASK_START", 4: "EVAL", 5: "DELAY", 6: "BIND", 7: "ENQUEUE",
                8: "DISPATCH", 9: "RETIRE", 10: "SYNC_CALL", 11: "SYNC_RET", 12: "FREE_CLOSE",
-               13: "INST_DONE", 14: "EARLY_EXIT"}
+               13: "INST_DONE", 14: "EARLY_EXIT", 15: "COLLISION"}
 TRACE_CODES = {v: k for k, v in TRACE_KINDS.items()}
 
 

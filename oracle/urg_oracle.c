@@ -62,18 +62,19 @@ typedef struct {
 } orc_input;
 
 enum { ORC_FIFO = 0, ORC_STATIC = 1, ORC_URGENGO = 2 };
-enum { ORC_BIND = 1, ORC_DELAY = 2, ORC_EARLY_EXIT = 4 };
+enum { ORC_BIND = 1, ORC_DELAY = 2, ORC_EARLY_EXIT = 4, ORC_COLLISIONS = 8 };
 enum { ORC_ASYNC = 0, ORC_EACH = 1, ORC_BATCHED = 2, ORC_OVERLAP = 3 };
 enum { TAG_ARR = 1, TAG_TIGHT = 2, TAG_INST = 3, TAG_KERN = 4, TAG_SYNC = 5 };
 
 /* trace kinds */
 enum { TR_STEP = 1, TR_INST_START, TR_TASK_START, TR_EVAL, TR_DELAY, TR_BIND, TR_ENQUEUE,
        TR_DISPATCH, TR_RETIRE, TR_SYNC_CALL, TR_SYNC_RET, TR_FREE_CLOSE, TR_INST_DONE,
-       TR_EARLY_EXIT };
+       TR_EARLY_EXIT, TR_COLLISION };
 
 #define REC_WORDS 8
 #define AGG_COUNTERS 5
 #define RATIO_BINS 101
+#define COLL_BINS 33      /* kernel-collision histogram by number of colliding tasks (R24) */
 
 /* ------------------------------------------------------------------ */
 /* Philox4x32-10 counter-based RNG (Salmon, Moraes, Dror, Shaw, SC'11). */
@@ -258,6 +259,8 @@ typedef struct {
     int64_t H, H_stop;
     int64_t *snap_L;                /* AKB read view at the start of Phase B */
     uint32_t *snap_n;
+    uint32_t *snap_level;           /* stream level of each chain's current task, same snapshot */
+    uint8_t *snap_busy;             /* the chain's stream holds a kernel (waiting or running) */
     int64_t *akb_L_view;            /* scratch */
     int64_t *trace; int64_t trace_cap; int64_t trace_len;
     int64_t *agg;
@@ -434,6 +437,31 @@ static uint32_t task_first_kernel(const orc_sim *S, uint32_t c)
     return k;
 }
 
+/* Kernel collisions of an urgent kernel ("priority collision" /
+ * "inverted binding", "kernel collisions for urgent kernels";
+ * DESIGN.md R24): when chain c enqueues a kernel while its last evaluation is
+ * truly urgent, every other chain whose stream holds a kernel and whose task is
+ * bound to the same or a higher priority (level <= c's) while being less urgent
+ * collides with it.  One event per such enqueue, counted in the histogram bin
+ * of the number of colliding tasks (c and its colliders). */
+static void count_collision(orc_sim *S, uint32_t c, int64_t t)
+{
+    orc_lane *L = &S->lane[c];
+    const orc_input *in = S->in;
+    if (!orc_is_urgent(L->L_last, in->lax_threshold_ns)) return;
+    int64_t own = orc_urgency_key(L->L_last);
+    uint32_t k = 0;
+    for (uint32_t o = 0; o < S->C; ++o) {
+        if (o == c || !S->snap_busy[o]) continue;
+        if (S->snap_level[o] <= L->level && orc_urgency_key(S->snap_L[o]) < own) ++k;
+    }
+    if (k == 0) return;
+    uint32_t card = k + 1;
+    if (card > COLL_BINS - 1) card = COLL_BINS - 1;
+    S->agg[(int64_t)S->C * (AGG_COUNTERS + in->rt_bins + RATIO_BINS) + card] += 1;
+    tr(S, t, TR_COLLISION, c, L->inst, card, L->level);
+}
+
 /* One CPU step of chain c at time t (R21 Phase B): the thread runs
  * its program until it must wait for time to pass or for the GPU. */
 static void lane_step(orc_sim *S, uint32_t c, int64_t t)
@@ -497,6 +525,7 @@ static void lane_step(orc_sim *S, uint32_t c, int64_t t)
                 a->T = L->T_last; a->L = L->L_last;
             }
             tr(S, t, TR_ENQUEUE, c, L->inst, n, L->level);
+            if (flag(S, ORC_COLLISIONS)) count_collision(S, c, t);
             int last = (L->launched == end);
             if (last) L->cpu_idx++;                      /* PAPER.md:335 */
             uint32_t est = in->k_est[L->kbase + n];
@@ -641,6 +670,8 @@ static int sim_scenario(const orc_input *in, uint64_t s, uint32_t *rec, int64_t 
     S.lane = calloc(S.C, sizeof(orc_lane));
     S.snap_L = calloc(S.C, sizeof(int64_t));
     S.snap_n = calloc(S.C, sizeof(uint32_t));
+    S.snap_level = calloc(S.C, sizeof(uint32_t));
+    S.snap_busy = calloc(S.C, sizeof(uint8_t));
     uint32_t kb = 0, tb = 0;
     for (uint32_t c = 0; c < S.C; ++c) {
         orc_lane *L = &S.lane[c];
@@ -707,7 +738,10 @@ static int sim_scenario(const orc_input *in, uint64_t s, uint32_t *rec, int64_t 
         S.steps++;
         tr(&S, t, TR_STEP, -1, -1, 0, 0);
         retire(&S, t);                                                   /* Phase A */
-        for (uint32_t c = 0; c < S.C; ++c) { S.snap_L[c] = S.lane[c].L_last; S.snap_n[c] = S.lane[c].akb_n; }
+        for (uint32_t c = 0; c < S.C; ++c) {
+            S.snap_L[c] = S.lane[c].L_last; S.snap_n[c] = S.lane[c].akb_n;
+            S.snap_level[c] = S.lane[c].level; S.snap_busy[c] = S.lane[c].q_head < S.lane[c].q_tail;
+        }
         for (uint32_t c = 0; c < S.C; ++c)                               /* Phase B */
             if (S.lane[c].cpu_next == t) lane_step(&S, c, t);
         dispatch(&S, t);                                                 /* Phase C */
@@ -730,11 +764,11 @@ static int sim_scenario(const orc_input *in, uint64_t s, uint32_t *rec, int64_t 
         if (L->total) a[AGG_COUNTERS + in->rt_bins + (uint64_t)100 * L->miss / L->total] += 1;
         free(L->akb); free(L->q);
     }
-    agg[(int64_t)S.C * stride + 0] += S.launches;
-    agg[(int64_t)S.C * stride + 1] += S.steps;
+    agg[(int64_t)S.C * stride + COLL_BINS + 0] += S.launches;
+    agg[(int64_t)S.C * stride + COLL_BINS + 1] += S.steps;
     if (trace_len) *trace_len = S.trace_len;
     if (cal_n) *cal_n = S.cal_n;
-    free(S.lane); free(S.snap_L); free(S.snap_n);
+    free(S.lane); free(S.snap_L); free(S.snap_n); free(S.snap_level); free(S.snap_busy);
     return rc;
 }
 
@@ -795,7 +829,8 @@ int64_t orc_calibrate(const orc_input *in_, int64_t window_ns, int64_t *n_sample
     int64_t *L = calloc(cap, sizeof(int64_t));
     int64_t n = 0;
     uint32_t *rec = calloc((size_t)in.num_chains * REC_WORDS, sizeof(uint32_t));
-    int64_t *agg = calloc((size_t)in.num_chains * (AGG_COUNTERS + in.rt_bins + RATIO_BINS) + 2, sizeof(int64_t));
+    int64_t *agg = calloc((size_t)in.num_chains * (AGG_COUNTERS + in.rt_bins + RATIO_BINS) + COLL_BINS + 2,
+                          sizeof(int64_t));
     sim_scenario(&in, in.scenario_begin, rec, agg, 0, 0, 0, L, cap, &n, end);
     int64_t out = orc_nearest_rank_lth(L, n, 95);
     if (n_samples) *n_samples = n;

@@ -150,3 +150,35 @@ def test_single_chain_closed_form(mode):
             p = Policy(kind=kind, flags=flags, sync_mode=mode, delta_eval_ns=delta, lax_threshold_ns=MS)
             r = O.run(w, p, Batch(horizon_ns=1))
             assert _sum_rt(r.records[0, 0]) == expect, (trial, kind, flags)
+
+
+@pytest.mark.parametrize("case", _gold("w4.json")["cases"], ids=lambda c: c["policy"])
+def test_w4_kernel_collisions(case):
+    """Collision histogram and response times of the hand-worked W4 (R24)."""
+    from workloads import w4
+    from workloads.spec import collision_hist
+    w = w4()
+    p = Policy(kind=case["kind"], flags=case["flags"], sync_mode=SYNC_ASYNC, lax_threshold_ns=5 * MS)
+    r = O.run(w, p, Batch(horizon_ns=1 * MS))
+    h = collision_hist(r.agg, w.num_chains, w.rt_bins)
+    want = np.zeros_like(h)
+    for k, v in case["hist"].items():
+        want[int(k)] = v
+    assert h.tolist() == want.tolist()
+    for c in range(3):
+        assert _sum_rt(r.records[0][c]) == int(round(case["rt_ms"][c] * MS))
+        assert r.records[0][c, REC_MISS] == case["miss"][c]
+
+
+def test_collisions_need_concurrency():
+    """A single chain never collides (SPEC.md:580 'no concurrent execution -> all-zero histogram'),
+    and the metric does not change the schedule (records identical with and without it)."""
+    from workloads import w3
+    from workloads.spec import F_COLLISIONS, collision_hist
+    w = w3()
+    for lth in (-1, 10 * MS):
+        a = O.run(w, Policy(kind=URGENGO, flags=7 | F_COLLISIONS, sync_mode=SYNC_ASYNC, lax_threshold_ns=lth),
+                  Batch(horizon_ns=1 * MS))
+        b = O.run(w, Policy(kind=URGENGO, flags=7, sync_mode=SYNC_ASYNC, lax_threshold_ns=lth), Batch(horizon_ns=1 * MS))
+        assert not collision_hist(a.agg, 1, w.rt_bins).any()
+        assert np.array_equal(a.records, b.records)

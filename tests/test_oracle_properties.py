@@ -325,3 +325,59 @@ def test_bruteforce_tiny(seed):
         assert min(all_miss) <= misses <= max(all_miss)                # (4)
         if p.kind == FIFO:
             assert all(v == w.num_prio - 1 for v in levels.values())
+
+
+def _replay_collisions(w, lth, trace):
+    """Independent recount of DESIGN.md R24 from the event trace: snapshot of (stream busy,
+    level, last laxity) at the start of each Phase B, checked at every enqueue of an urgent
+    chain.  Returns the histogram by number of colliding tasks."""
+    C = w.num_chains
+    busy, level, lax = [0] * C, [0] * C, [0] * C
+    snap = None
+    hist = np.zeros(33, np.int64)
+
+    def key(L):
+        return (1 << 63) if L == 0 else ((1 << 62) - L if L > 0 else -(1 << 62) - L)
+
+    for t, kind, c, i, a, bb in trace:
+        kind, c, a, bb = int(kind), int(c), int(a), int(bb)
+        if kind == K["STEP"]:
+            snap = None
+            continue
+        if kind == K["RETIRE"]:
+            busy[c] -= 1
+            continue
+        if snap is None:
+            snap = (list(busy), list(level), list(lax))
+        if kind == K["EVAL"]:
+            lax[c] = a
+        elif kind == K["BIND"]:
+            level[c] = a
+        elif kind == K["ENQUEUE"]:
+            busy[c] += 1
+            if 0 <= lax[c] <= lth:
+                sb, sl, sL = snap
+                k = sum(1 for o in range(C) if o != c and sb[o] > 0 and sl[o] <= level[c] and key(sL[o]) < key(lax[c]))
+                if k:
+                    hist[min(k + 1, 32)] += 1
+    return hist
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_collision_histogram_replayed_from_trace(seed):
+    from workloads.spec import F_COLLISIONS, collision_hist
+    rng = random.Random(1000 + seed)
+    w = random_workload(rng, C=rng.randint(2, 6))
+    p = random_policy(rng)
+    p.kind = URGENGO
+    p.lax_threshold_ns = rng.choice([2 * MS, 8 * MS, 30 * MS])
+    p.flags = rng.randint(0, 7) | F_COLLISIONS
+    b = Batch(seed=seed, scenario_count=1, horizon_ns=400 * MS)
+    r = O.run(w, p, b, trace_cap=400_000)
+    assert len(r.trace) < 400_000
+    got = collision_hist(r.agg, w.num_chains, w.rt_bins)
+    want = _replay_collisions(w, p.lax_threshold_ns, r.trace)
+    assert got.tolist() == want.tolist()
+    plain = O.run(w, Policy(kind=p.kind, flags=p.flags & 7, sync_mode=p.sync_mode, delta_eval_ns=p.delta_eval_ns,
+                            lax_threshold_ns=p.lax_threshold_ns, sleep_ns=p.sleep_ns), b)
+    assert np.array_equal(plain.records, r.records)   # a metric: the schedule is unchanged

@@ -25,6 +25,7 @@ import numpy as np
 # ---- policy / mode identifiers (values of the C-ABI enums in include/urg.h) ----
 FIFO, STATIC, URGENGO = 0, 1, 2
 F_BIND, F_DELAY, F_EARLY_EXIT = 1, 2, 4
+F_COLLISIONS = 8           # count kernel collisions of urgent kernels (metric only; R24)
 F_ALL = F_BIND | F_DELAY | F_EARLY_EXIT
 SYNC_ASYNC, SYNC_EACH, SYNC_BATCHED, SYNC_OVERLAP = 0, 1, 2, 3
 
@@ -132,8 +133,16 @@ RECORD_WORDS = 8   # per scenario, per chain: total, miss, early, unfinished, la
 REC_TOTAL, REC_MISS, REC_EARLY, REC_UNFIN, REC_LAUNCH, REC_HASH, REC_SUMRT_LO, REC_SUMRT_HI = range(8)
 AGG_COUNTERS = 5   # per chain: total, miss, early, unfinished, sum_rt
 RATIO_BINS = 101
+COLL_BINS = 33     # kernel-collision histogram, bin = number of colliding tasks (2..32)
 
 
 def agg_words(num_chains: int, rt_bins: int) -> int:
-    """int64 words of the aggregate buffer: per chain [5 counters | rt_bins | 101 ratio bins], then 2 event counters."""
-    return num_chains * (AGG_COUNTERS + rt_bins + RATIO_BINS) + 2
+    """int64 words of the aggregate buffer: per chain [5 counters | rt_bins | 101 ratio bins], then the
+    33-bin kernel-collision histogram, then 2 event counters (launch events, loop steps)."""
+    return num_chains * (AGG_COUNTERS + rt_bins + RATIO_BINS) + COLL_BINS + 2
+
+
+def collision_hist(agg, num_chains: int, rt_bins: int):
+    """View of the collision histogram inside an aggregate buffer (index = number of colliding tasks)."""
+    o = num_chains * (AGG_COUNTERS + rt_bins + RATIO_BINS)
+    return agg[o: o + COLL_BINS]

@@ -143,3 +143,12 @@ def w3() -> Workload:
     t1 = Task(1 * MS, 1 * MS, [Kernel(1 * MS, 1 * MS, 1000)])
     return Workload(chains=[Chain(1000 * MS, 4_500_000, 0, [t0, t1])], num_prio=6,
                     launch_ns=0, launch_akb_ns=0, sync_lo_ns=0, sync_hi_ns=0, jitter_ns=0)
+
+
+def w4() -> Workload:
+    """Fixture W4 (tests/golden/w4.json): three chains for the kernel-collision metric (R24)."""
+    a = Chain(1000 * MS, 6 * MS, 0, [Task(1 * MS, 1 * MS, [Kernel(1 * MS, 1 * MS, 1000), Kernel(1 * MS, 1 * MS, 1000)])])
+    b = Chain(1000 * MS, 100 * MS, 0, [Task(500 * US, 500 * US, [Kernel(4 * MS, 4 * MS, 1000)])])
+    b2 = Chain(1000 * MS, 100 * MS, 0, [Task(600 * US, 600 * US, [Kernel(4 * MS, 4 * MS, 1000)])])
+    return Workload(chains=[a, b, b2], num_prio=2, launch_ns=0, launch_akb_ns=0, sync_lo_ns=0, sync_hi_ns=0,
+                    jitter_ns=0)
