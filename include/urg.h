@@ -86,8 +86,10 @@ void urg_destroy_workload(urg_workload *w);
 
 /* Policies (§4.4; baselines P:614-615). */
 enum { URG_FIFO = 0, URG_STATIC = 1, URG_URGENGO = 2 };
-/* UrgenGo mechanisms: stream binding, delayed launching, early exit. */
-enum { URG_F_BIND = 1, URG_F_DELAY = 2, URG_F_EARLY_EXIT = 4 };
+/* UrgenGo mechanisms: stream binding, delayed launching, early exit;
+ * URG_F_COLLISIONS counts kernel collisions of urgent kernels (R24) into the
+ * aggregate's collision histogram -- a metric only, the schedule is unchanged. */
+enum { URG_F_BIND = 1, URG_F_DELAY = 2, URG_F_EARLY_EXIT = 4, URG_F_COLLISIONS = 8 };
 /* Launch synchronisation (Fig. fig:launch (a)-(d)). */
 enum { URG_SYNC_ASYNC = 0, URG_SYNC_EACH = 1, URG_SYNC_BATCHED = 2, URG_SYNC_OVERLAP = 3 };
 
@@ -123,7 +125,8 @@ typedef struct {
 } urg_outputs;
 
 /* Number of int64 words of the aggregate buffer:
- * num_chains * (5 + rt_bins + 101) + 2 (launch events, loop steps). */
+ * num_chains * (5 + rt_bins + 101) + 33 (collision histogram, index = number of colliding
+ * tasks, R24) + 2 (launch events, loop steps). */
 uint64_t urg_agg_words(const urg_workload *w);
 
 /* Bytes of the packed template urg_create_workload copied host -> device

@@ -187,7 +187,7 @@ extern "C" void urg_destroy_workload(urg_workload *w)
 
 extern "C" uint64_t urg_agg_words(const urg_workload *w)
 {
-    return w ? (uint64_t)w->num_chains * (5 + w->rt_bins + 101) + 2 : 0;
+    return w ? (uint64_t)w->num_chains * (5 + w->rt_bins + 101) + URG_COLL_BINS + 2 : 0;
 }
 
 extern "C" uint64_t urg_template_bytes(const urg_workload *w)
@@ -199,7 +199,7 @@ static urg_status validate_call(const urg_workload *w, const urg_policy *p, cons
 {
     if (!w || !p || !b) return fail(URG_EINVAL, "workload, policy and batch must not be NULL");
     if (p->kind > URG_URGENGO) return fail(URG_EINVAL, "policy.kind must be 0..2");
-    if (p->flags > 7) return fail(URG_EINVAL, "policy.flags has unknown bits");
+    if (p->flags > 15) return fail(URG_EINVAL, "policy.flags has unknown bits");
     if (p->sync_mode > URG_SYNC_OVERLAP) return fail(URG_EINVAL, "policy.sync_mode must be 0..3");
     if (p->delta_eval_ns <= 0) return fail(URG_EINVAL, "policy.delta_eval_ns must be > 0");
     if (p->sleep_ns <= 0) return fail(URG_EINVAL, "policy.sleep_ns must be > 0");
@@ -253,7 +253,7 @@ static urg_status geometry(const urg_workload *w, const void *fn, uint64_t count
     if (const char *ew = getenv("URG_WARPS_PER_CTA")) warps = atoi(ew);
     if (warps < 1) warps = 1;
     if (warps > max_w) warps = max_w;
-    smem = smem_fixed + (uint32_t)warps * 32u * 8u;
+    smem = smem_fixed + (uint32_t)warps * 32u * URG_SNAP_BYTES_PER_LANE;
     CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
              "cudaFuncSetAttribute(smem)");
     int per_sm = 0;

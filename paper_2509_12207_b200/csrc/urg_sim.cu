@@ -15,7 +15,7 @@
 #define INF64 0x7FFFFFFFFFFFFFFFLL
 
 enum { K_FIFO = 0, K_STATIC = 1, K_URGENGO = 2 };
-enum { F_BIND = 1, F_DELAY = 2, F_EARLY = 4 };
+enum { F_BIND = 1, F_DELAY = 2, F_EARLY = 4, F_COLL = 8 };
 enum { S_ASYNC = 0, S_EACH = 1, S_BATCHED = 2, S_OVERLAP = 3 };
 // lane program counter; the per-launch states come first so one range test skips the
 // per-task / per-instance states on the common path
@@ -161,10 +161,13 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
     }
     __syncthreads();
 
-    int64_t *snapL = (int64_t *)(sm + P.snap_offset) + warp * 32;   // per-warp Phase B laxity snapshot
+    // per-warp Phase B snapshot (R21): last laxity of each lane, then its stream level
+    int64_t *snapL = (int64_t *)(sm + P.snap_offset) + warp * 64;
+    uint32_t *snapLev = (uint32_t *)(snapL + 32);
     constexpr bool urg = KIND == K_URGENGO;
     constexpr bool f_bind = urg && (FLAGS & F_BIND), f_delay = urg && (FLAGS & F_DELAY),
                    f_early = urg && (FLAGS & F_EARLY);
+    constexpr bool coll = urg && (FLAGS & F_COLL);   // collision metric (R24): not in the schedule
     const int64_t busy_launch = P.launch_ns + (urg ? P.launch_akb_ns : 0);
     const uint32_t stride = P.agg_stride;
     const bool valid = (uint32_t)lane < C;
@@ -281,7 +284,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         // Phase B: this lane's CPU program at t, until it has to wait for time to pass.
         // urgent_m / active_m / snapL are the round snapshot of the other chains (R14, R15).
         // Returns true if the lane's stream got a new head (Phase C must run).
-        auto phase_b = [&](int64_t t, uint32_t urgent_m, uint32_t active_m) -> bool {
+        auto phase_b = [&](int64_t t, uint32_t urgent_m, uint32_t active_m, uint32_t busy_m) -> bool {
             bool newhead = false;
             for (uint32_t guard = 0;; ++guard) {
                 if (guard > (1u << 24)) {
@@ -358,6 +361,17 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     ++launched; ++n_launch;
                     rem_g -= est;
                     if (urg) ++akb;
+                    if (coll && L_last >= 0 && L_last <= P.lax_threshold_ns) {
+                        // R24: less urgent chains with a busy stream at the same or a higher priority
+                        const int64_t own = urgency_key(L_last);
+                        uint32_t mm = busy_m & ~(1u << lane), k = 0;
+                        while (mm) {
+                            const int o = __ffs(mm) - 1;
+                            mm &= mm - 1;
+                            k += (snapLev[o] <= level && urgency_key(snapL[o]) < own) ? 1u : 0u;
+                        }
+                        if (k) atomicAdd(&agg[(uint64_t)C * stride + (k + 1 > 32 ? 32 : k + 1)], 1ull);
+                    }
                     const bool last = launched == task_end;
                     if (last) rem_c -= T.task[cr.task_base + task].cpu_estimate_ns;
                     if (n == task_first) { acc = 0; batch_start = task_first; }
@@ -441,10 +455,16 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         // Round snapshot of the chains' (AKB non-empty, last laxity) for Phase B (R14, R15, R21).
         // `may_bind`: this lane can reach a task's first launch in this phase (else the
         // binding snapshot is not needed).
-        auto snapshot = [&](bool may_bind, uint32_t &urgent_m, uint32_t &active_m) {
-            urgent_m = 0; active_m = 0;
+        auto snapshot = [&](bool may_bind, uint32_t &urgent_m, uint32_t &active_m, uint32_t &busy_m) {
+            urgent_m = 0; active_m = 0; busy_m = 0;
             if (f_delay) urgent_m = __ballot_sync(FULL, akb > 0 && L_last >= 0 && L_last <= P.lax_threshold_ns);
-            if (f_bind && __any_sync(FULL, may_bind)) {
+            if (coll) {
+                busy_m = __ballot_sync(FULL, launched > done);
+                active_m = __ballot_sync(FULL, akb > 0);
+                snapL[lane] = L_last;
+                snapLev[lane] = level;
+                __syncwarp();
+            } else if (f_bind && __any_sync(FULL, may_bind)) {
                 active_m = __ballot_sync(FULL, akb > 0);
                 snapL[lane] = L_last;
                 __syncwarp();
@@ -496,10 +516,10 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
 #ifdef URG_STATS
                 ++st_multi;
 #endif
-                uint32_t urgent_m = 0, active_m = 0;
-                if (urg) snapshot(due && can_bind(), urgent_m, active_m);
+                uint32_t urgent_m = 0, active_m = 0, busy_m = 0;
+                if (urg) snapshot(due && can_bind(), urgent_m, active_m, busy_m);
                 bool nh = false;
-                if (due) nh = phase_b(t, urgent_m, active_m);
+                if (due) nh = phase_b(t, urgent_m, active_m, busy_m);
                 dirty |= __any_sync(FULL, nh);
             }
 
@@ -558,8 +578,8 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         my_launches += __reduce_add_sync(FULL, n_launch);
     }
     if (lane == 0) {
-        atomicAdd(&agg[(uint64_t)C * stride + 0], my_launches);
-        atomicAdd(&agg[(uint64_t)C * stride + 1], my_steps);
+        atomicAdd(&agg[(uint64_t)C * stride + URG_COLL_BINS + 0], my_launches);
+        atomicAdd(&agg[(uint64_t)C * stride + URG_COLL_BINS + 1], my_steps);
 #ifdef URG_STATS
         atomicAdd(&work[4], st_single); atomicAdd(&work[5], st_multi);
         atomicAdd(&work[6], st_dispatch); atomicAdd(&work[7], st_rebase);
@@ -573,14 +593,16 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
 #define URG_I(K, F)                                                                                  \
     (const void *)urg_sim_kernel<K, F, false, false>, (const void *)urg_sim_kernel<K, F, true, false>,     \
         (const void *)urg_sim_kernel<K, F, false, true>, (const void *)urg_sim_kernel<K, F, true, true>
-static const void *const g_sim_kernels[10][4] = {
-    {URG_I(K_FIFO, 0)},    {URG_I(K_STATIC, 0)},  {URG_I(K_URGENGO, 0)}, {URG_I(K_URGENGO, 1)},
-    {URG_I(K_URGENGO, 2)}, {URG_I(K_URGENGO, 3)}, {URG_I(K_URGENGO, 4)}, {URG_I(K_URGENGO, 5)},
-    {URG_I(K_URGENGO, 6)}, {URG_I(K_URGENGO, 7)}};
+static const void *const g_sim_kernels[18][4] = {
+    {URG_I(K_FIFO, 0)},     {URG_I(K_STATIC, 0)},   {URG_I(K_URGENGO, 0)},  {URG_I(K_URGENGO, 1)},
+    {URG_I(K_URGENGO, 2)},  {URG_I(K_URGENGO, 3)},  {URG_I(K_URGENGO, 4)},  {URG_I(K_URGENGO, 5)},
+    {URG_I(K_URGENGO, 6)},  {URG_I(K_URGENGO, 7)},  {URG_I(K_URGENGO, 8)},  {URG_I(K_URGENGO, 9)},
+    {URG_I(K_URGENGO, 10)}, {URG_I(K_URGENGO, 11)}, {URG_I(K_URGENGO, 12)}, {URG_I(K_URGENGO, 13)},
+    {URG_I(K_URGENGO, 14)}, {URG_I(K_URGENGO, 15)}};
 #undef URG_I
 
 const void *urg_sim_kernel_for(uint32_t kind, uint32_t flags, bool kern_q, bool wide)
 {
-    const uint32_t row = kind == K_FIFO ? 0 : kind == K_STATIC ? 1 : 2 + (flags & 7u);
+    const uint32_t row = kind == K_FIFO ? 0 : kind == K_STATIC ? 1 : 2 + (flags & 15u);
     return g_sim_kernels[row][(kern_q ? 1 : 0) + (wide ? 2 : 0)];
 }

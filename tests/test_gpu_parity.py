@@ -238,3 +238,33 @@ def test_throughput_batch_sampled():
         o = O.run(w, p, Batch(seed=b.seed, scenario_begin=s, scenario_count=1, horizon_ns=b.horizon_ns,
                               ftight_permille=400))
         assert np.array_equal(o.records[0], r[s]), f"scenario {s}"
+
+
+@pytest.mark.parametrize("flags", [8, 9, 10, 15])
+def test_w4_collisions(flags):
+    from workloads import w4
+    both(w4(), Policy(kind=URGENGO, flags=flags, sync_mode=SYNC_ASYNC, lax_threshold_ns=5 * MS), Batch(horizon_ns=1 * MS),
+         f"w4 flags={flags}")
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_collisions_random(seed):
+    rng = random.Random(5000 + seed)
+    w = random_workload(rng, C=rng.choice([2, 4, 7, 16]))
+    p = random_policy(rng)
+    p.kind = URGENGO
+    p.flags = rng.randint(0, 7) | 8
+    p.lax_threshold_ns = rng.choice([2 * MS, 8 * MS, 30 * MS])
+    both(w, p, Batch(seed=seed, scenario_count=rng.randint(1, 24), horizon_ns=300 * MS), f"coll seed {seed}")
+
+
+def test_collisions_paper11(wide_build):
+    from workloads.spec import collision_hist
+    cfg = get_config("paper11")
+    w = cfg.workload()
+    for flags in (8 | 7, 8 | 5):     # UrgenGo with and without delayed launching (P:790 comparison)
+        p = Policy(kind=URGENGO, flags=flags, sync_mode=SYNC_OVERLAP,
+                   lax_threshold_ns=cfg.policies["urgengo"].lax_threshold_ns)
+        o, r, a = both(w, p, Batch(seed=cfg.batch.seed, scenario_count=12, horizon_ns=2_000 * MS, ftight_permille=400),
+                       f"paper11 collisions flags={flags}")
+        assert collision_hist(a, w.num_chains, w.rt_bins).sum() > 0
