@@ -1,0 +1,133 @@
+"""Design-option studies of UrgenGo on the batched GPU simulator.
+
+Each study is a list of policy / workload / batch variants of one base configuration,
+run through the same C-ABI call (``urg_simulate_batch``) on the current CUDA device:
+
+* ``sync_modes``   -- launch synchronisation: synchronous, asynchronous, batched, and
+                      UrgenGo's overlapped batches (Fig. fig:9_launch);
+* ``delta_eval``   -- urgency-evaluation interval Delta_eval (fig:10_resolution);
+* ``num_prio``     -- number of binding streams 1..6 (fig:5_stream_num);
+* ``ablation``     -- binding only / delay only / both (fig:4_ablation);
+* ``collisions``   -- kernel collisions of urgent kernels with and without delayed
+                      launching, by number of colliding tasks (fig:8_collision);
+* ``utilisation``  -- UrgenGo vs FIFO vs static priorities over an arrival-rate sweep
+                      (BASELINE.json configs[2]; PAPER.md:679-683 fig:0_overall analogue).
+
+Only argument marshalling and bookkeeping happen here; every simulated step runs
+in liburg.so.  Miss ratios follow Eq. 3 via ``urg_miss_ratios``.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field, replace
+from typing import Dict, List, Optional
+
+import numpy as np
+
+from workloads.spec import (COLL_BINS, F_BIND, F_COLLISIONS, F_DELAY, F_EARLY_EXIT, FIFO, STATIC, SYNC_ASYNC,
+                            SYNC_BATCHED, SYNC_EACH, SYNC_OVERLAP, URGENGO, Batch, Policy, Workload,
+                            collision_hist)
+
+from .urg import DeviceWorkload
+
+
+@dataclass
+class Point:
+    """One variant of a study: what changed, and the batch it ran."""
+    label: str
+    policy: Policy
+    batch: Batch
+    num_prio: Optional[int] = None          # workload override (binding streams)
+
+
+@dataclass
+class Result:
+    label: str
+    overall_miss: float                     # Eq. 3
+    per_chain_miss: List[float]
+    collisions: Dict[int, int]              # number of colliding tasks -> events (R24)
+    launches: int
+    steps: int
+    gpu_ms: float
+    extra: dict = field(default_factory=dict)
+
+
+def sync_modes(base: Policy, b: Batch) -> List[Point]:
+    names = [("sync (each kernel)", SYNC_EACH), ("async", SYNC_ASYNC), ("sync batched", SYNC_BATCHED),
+             ("UrgenGo overlapped", SYNC_OVERLAP)]
+    return [Point(n, replace(base, sync_mode=m), b) for n, m in names]
+
+
+def delta_eval(base: Policy, b: Batch, values_us=(100, 250, 500, 1000, 2000, 4000)) -> List[Point]:
+    return [Point(f"delta_eval {v} us", replace(base, delta_eval_ns=v * 1000), b) for v in values_us]
+
+
+def num_prio(base: Policy, b: Batch, values=(1, 2, 3, 4, 5, 6)) -> List[Point]:
+    return [Point(f"NUM_PRI {n}", base, b, num_prio=n) for n in values]
+
+
+def ablation(base: Policy, b: Batch) -> List[Point]:
+    early = base.flags & F_EARLY_EXIT
+    return [Point("no binding, no delay", replace(base, flags=early), b),
+            Point("binding only", replace(base, flags=early | F_BIND), b),
+            Point("delay only", replace(base, flags=early | F_DELAY), b),
+            Point("binding + delay", replace(base, flags=early | F_BIND | F_DELAY), b)]
+
+
+def collisions(base: Policy, b: Batch) -> List[Point]:
+    f = base.flags | F_COLLISIONS
+    return [Point("UrgenGo without delayed launching", replace(base, flags=f & ~F_DELAY), b),
+            Point("UrgenGo", replace(base, flags=f), b)]
+
+
+def utilisation(base: Policy, batches: List[Batch]) -> List[Point]:
+    pols = [("UrgenGo", base), ("FIFO", Policy(kind=FIFO, flags=0, sync_mode=SYNC_ASYNC)),
+            ("static", Policy(kind=STATIC, flags=0, sync_mode=SYNC_ASYNC))]
+    out = []
+    for bb in batches:
+        u = 1.2082 * bb.fa_num / bb.fa_den
+        for n, p in pols:
+            out.append(Point(f"u={u:.2f} {n}", p, bb))
+    return out
+
+
+STUDIES = ("sync_modes", "delta_eval", "num_prio", "ablation", "collisions")
+
+
+def run(w: Workload, points: List[Point], stream=None) -> List[Result]:
+    """Run every point on the current CUDA device (one urg_simulate_batch per point)."""
+    import torch
+    out = []
+    cache: Dict[int, DeviceWorkload] = {}
+    try:
+        for pt in points:
+            npri = pt.num_prio if pt.num_prio is not None else w.num_prio
+            if npri not in cache:
+                cache[npri] = DeviceWorkload(replace(w, num_prio=npri))
+            dw = cache[npri]
+            agg = torch.zeros(dw.agg_words, dtype=torch.int64, device="cuda")
+            s = stream if stream is not None else torch.cuda.current_stream()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            dw.simulate(pt.policy, pt.batch, agg, None, stream=s)
+            e1.record(s)
+            dw.check(s)
+            a = agg.cpu().numpy()
+            per, overall = dw.miss_ratios(a)
+            h = collision_hist(a, w.num_chains, w.rt_bins)
+            out.append(Result(pt.label, float(overall), [float(x) for x in per],
+                              {int(k): int(h[k]) for k in range(COLL_BINS) if h[k]},
+                              int(a[-2]), int(a[-1]), float(e0.elapsed_time(e1))))
+    finally:
+        for dw in cache.values():
+            dw.close()
+    return out
+
+
+def table(results: List[Result]) -> str:
+    rows = ["| variant | Eq. 3 miss ratio | collisions (tasks: events) | launch events | GPU ms | G events/s |",
+            "|---|---|---|---|---|---|"]
+    for r in results:
+        coll = ", ".join(f"{k}: {v}" for k, v in sorted(r.collisions.items())) or "-"
+        rows.append(f"| {r.label} | {r.overall_miss:.4f} | {coll} | {r.launches} | {r.gpu_ms:.1f} | "
+                    f"{r.launches / max(r.gpu_ms, 1e-9) / 1e6:.3f} |")
+    return "\n".join(rows)

@@ -268,3 +268,22 @@ def test_collisions_paper11(wide_build):
         o, r, a = both(w, p, Batch(seed=cfg.batch.seed, scenario_count=12, horizon_ns=2_000 * MS, ftight_permille=400),
                        f"paper11 collisions flags={flags}")
         assert collision_hist(a, w.num_chains, w.rt_bins).sum() > 0
+
+
+def test_sweep_points_match_oracle():
+    """paper_2509_12207_b200.sweep runs each study point through the C ABI; two points of
+    three studies checked against the oracle's aggregates (Eq. 3 and collisions included)."""
+    from dataclasses import replace as rp
+    from paper_2509_12207_b200 import sweep as SW
+    cfg = get_config("paper11")
+    w, base = cfg.workload(), cfg.policies["urgengo"]
+    b = Batch(seed=cfg.batch.seed, scenario_count=6, horizon_ns=1_000 * MS, ftight_permille=400)
+    pts = [SW.sync_modes(base, b)[0], SW.num_prio(base, b)[1], SW.collisions(base, b)[0]]
+    res = SW.run(w, pts)
+    for pt, r in zip(pts, res):
+        ww = rp(w, num_prio=pt.num_prio) if pt.num_prio else w
+        o = O.run(ww, pt.policy, pt.batch)
+        assert r.launches == o.launches and r.steps == o.steps
+        tot = o.records[:, :, 0].astype(np.int64).sum(0)
+        miss = o.records[:, :, 1].astype(np.int64).sum(0)
+        assert r.overall_miss == O.overall_miss_ratio(miss, tot), pt.label
