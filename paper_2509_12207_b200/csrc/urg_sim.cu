@@ -1,54 +1,7 @@
-// urg_sim.cu -- the B200 (sm_100a) batched UrgenGo launch-policy simulation kernel.
-//
-// One warp simulates one scenario; lane c is task chain c (C <= 32).  Per-chain
-// state lives in registers; the workload template lives in shared memory
-// (staged once per CTA with cp.async.bulk + mbarrier); cross-chain reads use
-// warp votes, REDUX min/add reductions and a per-warp shared-memory snapshot.
-// The rules are DESIGN.md "Model M0" (R0-R23); comments name the rule and the
-// paper passage.  Nothing here is shared with the CPU oracle (oracle/).
-#include <cuda_runtime.h>
-#include <stdint.h>
-
-#include "urg_layout.h"
-
-#define FULL 0xFFFFFFFFu
-#define INF64 0x7FFFFFFFFFFFFFFFLL
-
-enum { K_FIFO = 0, K_STATIC = 1, K_URGENGO = 2 };
-enum { F_BIND = 1, F_DELAY = 2, F_EARLY = 4, F_COLL = 8 };
-enum { S_ASYNC = 0, S_EACH = 1, S_BATCHED = 2, S_OVERLAP = 3 };
-// lane program counter; the per-launch states come first so one range test skips the
-// per-task / per-instance states on the common path
-enum { PC_ENQUEUE = 0, PC_ATTEMPT, PC_CPU_DONE, PC_SYNC_RET, PC_ARRIVE, PC_TASK_START, PC_SYNC_WAIT, PC_DONE };
-enum { ERR_TIME = 1, ERR_GUARD = 2 };
-
-// ---------------------------------------------------------------------------
-// Philox4x32-10 (Salmon et al., SC'11) -- device copy, KAT-tested (tests/test_gpu_*.py)
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k)
-{
-#pragma unroll
-    for (int r = 0; r < 10; ++r) {
-        const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
-        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
-        c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
-        k.x += 0x9E3779B9u;
-        k.y += 0xBB67AE85u;
-    }
-    return c;
-}
-
-// word(tag, c, i, k) of scenario s (R3-R5).  Not inlined: the draws are
-// rare (per arrival, instance, sync call), and an inlined copy lets the compiler
-// hoist ~80 speculative instructions into the per-step path.
-__device__ __noinline__ uint32_t rng_word(uint64_t seed, uint32_t s, uint32_t tag, uint32_t c, uint32_t i,
-                                             uint32_t k)
-{
-    const uint4 o = philox4x32_10(make_uint4(s, (tag << 24) | (c << 16), i, k >> 2),
-                                  make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
-    const uint32_t q = k & 3u;
-    return q == 0 ? o.x : q == 1 ? o.y : q == 2 ? o.z : o.w;
-}
+// urg_sim.cu -- dispatch table of the simulation-kernel instantiations (the kernel itself
+// is urg_sim.cuh, instantiated in parallel slices by urg_sim_part.cu) and the Philox
+// known-answer test kernel.
+#include "urg_sim.cuh"
 
 extern "C" __global__ void urg_philox_kat_kernel(const uint4 *ctr, const uint2 *key, uint4 *out, int n)
 {
@@ -56,553 +9,19 @@ extern "C" __global__ void urg_philox_kat_kernel(const uint4 *ctr, const uint2 *
     if (i < n) out[i] = philox4x32_10(ctr[i], key[i]);
 }
 
-// ---------------------------------------------------------------------------
-// small warp helpers
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ int64_t warp_min_nonneg(int64_t v)    // v >= 0 for every lane
-{
-    const uint32_t hi = (uint32_t)((uint64_t)v >> 32), lo = (uint32_t)v;
-    const uint32_t mh = __reduce_min_sync(FULL, hi);
-    const uint32_t ml = __reduce_min_sync(FULL, hi == mh ? lo : 0xFFFFFFFFu);
-    return (int64_t)(((uint64_t)mh << 32) | ml);
-}
 
-__device__ __forceinline__ int64_t shfl64(int64_t v, int src)
-{
-    return (int64_t)__shfl_sync(FULL, (unsigned long long)v, src);
-}
-
-// urgency key: orders as 1/L, L = 0 saturating (R9)
-__device__ __forceinline__ int64_t urgency_key(int64_t L)
-{
-    return L == 0 ? INF64 : (L > 0 ? (((int64_t)1 << 62) - L) : (-((int64_t)1 << 62) - L));
-}
-
-// ---------------------------------------------------------------------------
-// shared-memory staging helpers (cp.async.bulk + mbarrier)
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void stage_blob(uint8_t *dst, const uint8_t *src, uint32_t bytes, uint64_t *mbar)
-{
-    const uint32_t bar = smem_addr(mbar);
-    if (threadIdx.x == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-        for (uint32_t off = 0; off < bytes; off += 32768u) {
-            const uint32_t n = bytes - off < 32768u ? bytes - off : 32768u;
-            asm volatile(
-                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                    smem_addr(dst + off)),
-                "l"(src + off), "r"(n), "r"(bar)
-                : "memory");
-        }
-    }
-    __syncthreads();   // barrier initialised before anyone waits on it
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "URG_WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
-        "@!p bra URG_WAIT_%=;\n}" ::"r"(bar)
-        : "memory");
-}
-
-// ---------------------------------------------------------------------------
-// the kernel
-// ---------------------------------------------------------------------------
-struct Tmpl {   // shared-memory views of the staged template
-    const UrgChainRec *ch;
-    const UrgTaskRec *task;
-    const UrgKernRec *kern;
-    const int32_t *inst_q;
-    const uint32_t *kern_q;
-};
-
-// One instantiation per (policy kind, UrgenGo flags, per-kernel factor table present):
-// the policy is uniform over a launch, so its branches are resolved at compile time
-// and code a policy never runs (e.g. the per-kernel Philox draw) is not in its loop.
-//
-// WIDE: the throughput build (1024 threads per CTA, so <= 64 registers and 32 warps per
-// SM) for batches that fill the GPU; otherwise the latency build (512 threads, ~100
-// registers), faster per scenario when there are fewer scenarios than warp slots.
-template <int KIND, int FLAGS, bool KQ, bool WIDE>
-__global__ void __launch_bounds__(WIDE ? 1024 : 512, 1)
-urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t *__restrict__ records,
-               unsigned long long *__restrict__ agg, unsigned long long *__restrict__ work,
-               long long *__restrict__ err)
-{
-    extern __shared__ __align__(128) uint8_t sm[];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-
-    // ---- A0: template staging (once per CTA) ----
-    stage_blob(sm, blob, P.blob_bytes, (uint64_t *)(sm + P.mbar_offset));
-    const UrgBlobHeader *hdr = (const UrgBlobHeader *)sm;
-    UrgChainRec *chs = (UrgChainRec *)(sm + hdr->off_chains);
-    Tmpl T;
-    T.ch = chs;
-    T.task = (const UrgTaskRec *)(sm + hdr->off_tasks);
-    T.kern = (const UrgKernRec *)(sm + hdr->off_kerns);
-    T.inst_q = hdr->off_inst_q ? (const int32_t *)(sm + hdr->off_inst_q) : nullptr;
-    T.kern_q = hdr->off_kern_q ? (const uint32_t *)(sm + hdr->off_kern_q) : nullptr;
-    const uint32_t C = P.num_chains;
-    // per-chain totals of the estimates (the remaining-work sums of Eq. 2 start from them)
-    for (uint32_t c = warp; c < C; c += nwarps) {
-        int64_t g = 0, cp = 0;
-        for (uint32_t k = lane; k < chs[c].num_kernels; k += 32) g += T.kern[chs[c].kern_base + k].estimate_ns;
-        for (uint32_t j = lane; j < chs[c].num_tasks; j += 32) cp += T.task[chs[c].task_base + j].cpu_estimate_ns;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            g += (int64_t)__shfl_xor_sync(FULL, (unsigned long long)g, o);
-            cp += (int64_t)__shfl_xor_sync(FULL, (unsigned long long)cp, o);
-        }
-        if (lane == 0) { chs[c].gpu_est_total = g; chs[c].cpu_est_total = cp; }
-    }
-    __syncthreads();
-
-    // per-warp Phase B snapshot (R21): last laxity of each lane, then its stream level
-    int64_t *snapL = (int64_t *)(sm + P.snap_offset) + warp * 64;
-    uint32_t *snapLev = (uint32_t *)(snapL + 32);
-    constexpr bool urg = KIND == K_URGENGO;
-    constexpr bool f_bind = urg && (FLAGS & F_BIND), f_delay = urg && (FLAGS & F_DELAY),
-                   f_early = urg && (FLAGS & F_EARLY);
-    constexpr bool coll = urg && (FLAGS & F_COLL);   // collision metric (R24): not in the schedule
-    const int64_t busy_launch = P.launch_ns + (urg ? P.launch_akb_ns : 0);
-    const uint32_t stride = P.agg_stride;
-    const bool valid = (uint32_t)lane < C;
-    const uint32_t c = lane;
-    unsigned long long my_launches = 0, my_steps = 0;
-#ifdef URG_STATS
-    unsigned long long st_single = 0, st_multi = 0, st_dispatch = 0, st_rebase = 0;   // profiling build only
-#endif
-
-    // static per-chain template data
-    UrgChainRec cr = {};
-    if (valid) cr = chs[c];
-
-    for (;;) {
-        unsigned long long jw = 0;
-        if (lane == 0) jw = atomicAdd(work, 1ull);
-        jw = __shfl_sync(FULL, jw, 0);
-        if (jw >= P.scenario_count) break;
-        const uint32_t s = (uint32_t)(P.scenario_begin + jw);
-
-        // ---- A1: scenario init (R3, R15 STATIC) ----
-        int64_t Pp = 0, Dp = 0;
-        if (valid) {
-            Pp = cr.period_ns * (int64_t)P.fa_den / (int64_t)P.fa_num;
-            Dp = cr.deadline_ns * (int64_t)P.fd_num / (int64_t)P.fd_den;
-        }
-        bool tight = false;
-        if (P.tight_explicit) tight = valid && ((P.tight_mask >> c) & 1u);
-        else if (P.ftight_permille) {
-            const uint32_t n_tight = (P.ftight_permille * C + 999u) / 1000u;
-            const uint32_t w = valid ? rng_word(P.seed, s, URG_TAG_TIGHT, c, 0, 0) : 0xFFFFFFFFu;
-            uint32_t rank = 0;
-            for (uint32_t o = 0; o < C; ++o) {
-                const uint32_t wo = __shfl_sync(FULL, w, o);
-                rank += (wo < w || (wo == w && o < c)) ? 1u : 0u;
-            }
-            tight = valid && rank < n_tight;
-        }
-        if (tight) Dp /= 2;
-        int64_t maxD = Dp;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const int64_t x = (int64_t)__shfl_xor_sync(FULL, (unsigned long long)maxD, o);
-            maxD = x > maxD ? x : maxD;
-        }
-        const int64_t H = P.horizon_ns, H_stop = H + maxD;
-        uint32_t static_level = 0;
-        {
-            uint32_t r = 1;
-            for (uint32_t o = 0; o < C; ++o) {
-                const int64_t Do = shfl64(Dp, o);
-                r += (Do < Dp || (Do == Dp && o < c)) ? 1u : 0u;
-            }
-            if (C > 1 && P.num_prio > 1) static_level = (uint32_t)(((uint64_t)(r - 1) * (P.num_prio - 1)) / (C - 1));
-        }
-
-        // ---- per-lane dynamic state ----
-        int pc = PC_DONE;
-        int64_t cpu_next = INF64;
-        uint32_t inst = 0;
-        int64_t t_arr = 0;
-        uint32_t Fg = 65536u, Fc = 65536u;
-        uint32_t task = 0, launched = 0, done = 0, level = 0;
-        uint32_t task_first = 0, task_end = 0;
-        int64_t rem_g = 0, rem_c = 0;          // sum of estimates of kernels / CPU segments not yet passed
-        int64_t acc = 0;
-        uint32_t batch_start = 0, sync_target = 0, sync_ord = 0;
-        int64_t sync_cost = 0;
-        uint32_t akb = 0;
-        int64_t L_last = 0;
-        int64_t head_end = INF64;              // end of the running kernel, INF64 when the stream runs nothing
-        int64_t head_ready = 0;                // time the waiting head became head (R20 key)
-        uint32_t head_util = 0;                // util of the running kernel
-        uint32_t head_u = 0xFFFFu;             // util of the waiting head (valid while one waits)
-        uint32_t n_total = 0, n_miss = 0, n_early = 0, n_unfin = 0, n_launch = 0, hash = 2166136261u;
-        uint64_t sum_rt = 0;
-
-        auto arrival = [&](uint32_t i) -> int64_t {
-            int64_t jit = 0;
-            if (P.jitter_ns > 0)
-                jit = (int64_t)(rng_word(P.seed, s, URG_TAG_ARR, c, i, 0) % (uint32_t)(P.jitter_ns + 1));
-            return cr.offset_ns + (int64_t)i * Pp + jit;
-        };
-        auto inst_factor = [&](uint32_t w, uint32_t sigma) -> uint32_t {
-            if (!T.inst_q) return 65536u;
-            const int64_t z = T.inst_q[w >> 20];
-            int64_t F = 65536 + (z * (int64_t)sigma) / 1000000;
-            return (uint32_t)(F < 6554 ? 6554 : F);
-        };
-
-        if (valid) {
-            t_arr = arrival(0);
-            if (t_arr < H) { pc = PC_ARRIVE; cpu_next = t_arr; }
-        }
-
-        // ---- lane-local pieces of a loop step (R21); used by the warp-wide
-        //      step and by the single-lane ("solo") steps below ----
-        // Phase A for a lane whose running kernel ends at t (R19)
-        auto retire = [&](int64_t t) {
-            ++done;
-            head_end = INF64;
-            if (launched > done) { head_ready = t; head_u = T.kern[cr.kern_base + done].util_permille; }
-            if (pc == PC_SYNC_WAIT && done >= sync_target) { pc = PC_SYNC_RET; cpu_next = t + sync_cost; }
-        };
-        // Phase C start of this lane's waiting head: non-preemptive, exact duration (R4, R19, R20)
-        auto start_head = [&](int64_t t) {
-            uint64_t G = 65536u;
-            if (KQ) G = T.kern_q[rng_word(P.seed, s, URG_TAG_KERN, c, inst, done) >> 20];
-            uint64_t d = ((((uint64_t)T.kern[cr.kern_base + done].nominal_ns * Fg) >> 16) * G) >> 16;
-            d = d < 1 ? 1 : (d > 0xFFFFFFFFull ? 0xFFFFFFFFull : d);
-            head_util = head_u;
-            head_end = t + (int64_t)d;
-        };
-        // Phase B: this lane's CPU program at t, until it has to wait for time to pass.
-        // urgent_m / active_m / snapL are the round snapshot of the other chains (R14, R15).
-        // Returns true if the lane's stream got a new head (Phase C must run).
-        auto phase_b = [&](int64_t t, uint32_t urgent_m, uint32_t active_m, uint32_t busy_m) -> bool {
-            bool newhead = false;
-            for (uint32_t guard = 0;; ++guard) {
-                if (guard > (1u << 24)) {
-                    if (atomicCAS((unsigned long long *)err, 0ull, (unsigned long long)ERR_GUARD) == 0ull) err[1] = s;
-                    cpu_next = INF64;
-                    break;
-                }
-                if ((uint32_t)(pc - PC_SYNC_RET) <= (uint32_t)(PC_TASK_START - PC_SYNC_RET)) {
-                bool next_inst = false;
-                if (pc == PC_SYNC_RET) {   // sync returned: covered kernels leave the AKB
-                    if (urg) akb = launched - sync_target;
-                    if (launched < task_end) pc = PC_ATTEMPT;
-                    else if (++task < cr.num_tasks) {
-                        task_first = task_end;
-                        task_end += T.task[cr.task_base + task].num_kernels;
-                        pc = PC_TASK_START;
-                    } else {   // instance complete (R18, R22)
-                        const int64_t rt = t - t_arr;
-                        if (rt > Dp) ++n_miss;
-                        sum_rt += (uint64_t)rt;
-                        hash = (hash ^ (uint32_t)rt) * 16777619u;
-                        hash = (hash ^ (uint32_t)((uint64_t)rt >> 32)) * 16777619u;
-                        int64_t bin = rt / P.rt_bin_ns;
-                        if (bin > (int64_t)P.rt_bins - 1) bin = P.rt_bins - 1;
-                        atomicAdd(&agg[(uint64_t)c * stride + 5 + bin], 1ull);
-                        next_inst = true;
-                    }
-                }
-                if (pc == PC_ARRIVE) {   // frame arrival / instance start (R6)
-                    ++n_total;
-                    Fg = inst_factor(rng_word(P.seed, s, URG_TAG_INST, c, inst, 0), cr.gpu_sigma_ppm);
-                    Fc = inst_factor(rng_word(P.seed, s, URG_TAG_INST, c, inst, 1), cr.cpu_sigma_ppm);
-                    task = 0; launched = 0; done = 0; sync_ord = 0;
-                    rem_g = cr.gpu_est_total; rem_c = cr.cpu_est_total;
-                    task_first = 0; task_end = T.task[cr.task_base].num_kernels;
-                    pc = PC_TASK_START;
-                }
-                if (pc == PC_TASK_START) {   // new CPU segment: evaluate, early exit
-                    bool exited = false;
-                    if (urg) {
-                        const int64_t lax = t_arr + Dp - rem_g - rem_c - t;   // Eq. 2 (R9)
-                        L_last = lax;
-                        if (f_early && lax < 0) {
-                            akb = 0;
-                            ++n_early; ++n_miss;
-                            hash = (hash ^ 0xFFFFFFFFu) * 16777619u;
-                            hash = (hash ^ 0xFFFFFFFFu) * 16777619u;
-                            pc = PC_DONE;
-                            next_inst = exited = true;
-                        }
-                    }
-                    if (!exited) {
-                        const int64_t e = (int64_t)(((uint64_t)T.task[cr.task_base + task].cpu_nominal_ns * Fc) >> 16);
-                        pc = PC_CPU_DONE;
-                        cpu_next = t + e;
-                        if (e > 0) break;
-                    }
-                }
-                if (next_inst) {   // advance to the next instance of this chain (R6, R7)
-                    ++inst;
-                    t_arr = arrival(inst);
-                    if (t_arr >= H) { pc = PC_DONE; cpu_next = INF64; break; }   // not admitted
-                    pc = PC_ARRIVE;
-                    cpu_next = t_arr;
-                    if (t_arr > t) break;
-                    continue;
-                }
-                }
-                if (pc == PC_ENQUEUE) {   // the kernel reaches its stream (R16) + sync decision (R17)
-                    const uint32_t n = launched;
-                    const UrgKernRec kr = T.kern[cr.kern_base + n];
-                    const int64_t est = kr.estimate_ns;
-                    if (launched == done) { head_ready = t; head_u = kr.util_permille; newhead = true; }   // stream was empty
-                    ++launched; ++n_launch;
-                    rem_g -= est;
-                    if (urg) ++akb;
-                    if (coll && L_last >= 0 && L_last <= P.lax_threshold_ns) {
-                        // R24: less urgent chains with a busy stream at the same or a higher priority
-                        const int64_t own = urgency_key(L_last);
-                        uint32_t mm = busy_m & ~(1u << lane), k = 0;
-                        while (mm) {
-                            const int o = __ffs(mm) - 1;
-                            mm &= mm - 1;
-                            k += (snapLev[o] <= level && urgency_key(snapL[o]) < own) ? 1u : 0u;
-                        }
-                        if (k) atomicAdd(&agg[(uint64_t)C * stride + (k + 1 > 32 ? 32 : k + 1)], 1ull);
-                    }
-                    const bool last = launched == task_end;
-                    if (last) rem_c -= T.task[cr.task_base + task].cpu_estimate_ns;
-                    if (n == task_first) { acc = 0; batch_start = task_first; }
-                    int32_t target = -1;
-                    if (P.sync_mode == S_ASYNC) {
-                        if (last) target = (int32_t)launched;
-                    } else if (P.sync_mode == S_EACH) {
-                        target = (int32_t)launched;
-                    } else {
-                        acc += est;
-                        const bool closes = acc >= P.delta_eval_ns;
-                        if (closes) acc = 0;
-                        if (last) { acc = 0; target = (int32_t)launched; }
-                        else if (closes) {
-                            if (P.sync_mode == S_BATCHED) target = (int32_t)launched;
-                            else {   // OVERLAP: wait for the previous batch
-                                const uint32_t prev = batch_start;
-                                batch_start = launched;
-                                if (prev != task_first) target = (int32_t)prev;   // first close: not issued
-                            }
-                        }
-                    }
-                    if (target >= 0) {
-                        sync_target = (uint32_t)target;
-                        sync_cost = P.sync_lo_ns;
-                        if (P.sync_hi_ns > P.sync_lo_ns)
-                            sync_cost += (int64_t)(rng_word(P.seed, s, URG_TAG_SYNC, c, inst, sync_ord) %
-                                                   (uint32_t)(P.sync_hi_ns - P.sync_lo_ns + 1));
-                        ++sync_ord;
-                        if (done >= sync_target) {
-                            pc = PC_SYNC_RET;
-                            cpu_next = t + sync_cost;
-                            if (sync_cost > 0) break;
-                            continue;
-                        }
-                        pc = PC_SYNC_WAIT;
-                        cpu_next = INF64;
-                        break;
-                    }
-                    pc = PC_ATTEMPT;
-                }
-                if (pc == PC_CPU_DONE || pc == PC_ATTEMPT) {   // launch attempt for kernel n = launched (R14-R16)
-                    int64_t lax = 0;
-                    if (urg) { lax = t_arr + Dp - rem_g - rem_c - t; L_last = lax; }
-                    const bool own_urgent = lax >= 0 && lax <= P.lax_threshold_ns;
-                    if (f_delay && !own_urgent && (urgent_m & ~(1u << lane)) &&
-                        T.kern[cr.kern_base + launched].util_permille >= P.util_exempt) {
-                        pc = PC_ATTEMPT;
-                        cpu_next = t + P.sleep_ns;
-                        break;
-                    }
-                    if (launched == task_first) {   // task-level stream binding
-                        if (KIND == K_STATIC) level = static_level;
-                        else if (!f_bind) level = P.num_prio - 1;
-                        else if (own_urgent) level = 0;
-                        else {
-                            const int64_t own = urgency_key(lax);
-                            uint32_t mm = active_m & ~(1u << lane);
-                            const uint32_t n_r = 1 + __popc(mm);
-                            uint32_t r = 1;
-                            while (mm) {
-                                const int o = __ffs(mm) - 1;
-                                mm &= mm - 1;
-                                const int64_t k = urgency_key(snapL[o]);
-                                r += (k > own || (k == own && o < lane)) ? 1u : 0u;
-                            }
-                            level = P.num_prio <= 2 ? P.num_prio - 1
-                                    : n_r <= 1      ? 1 + (P.num_prio - 2) / 2
-                                                    : 1 + (uint32_t)(((uint64_t)(r - 1) * (P.num_prio - 2)) / (n_r - 1));
-                        }
-                    }
-                    pc = PC_ENQUEUE;
-                    cpu_next = t + busy_launch;
-                    if (busy_launch > 0) break;
-                    continue;
-                }
-                break;   // PC_SYNC_WAIT / PC_DONE: nothing to do at t
-            }
-            return newhead;
-        };
-        // Round snapshot of the chains' (AKB non-empty, last laxity) for Phase B (R14, R15, R21).
-        // `may_bind`: this lane can reach a task's first launch in this phase (else the
-        // binding snapshot is not needed).
-        auto snapshot = [&](bool may_bind, uint32_t &urgent_m, uint32_t &active_m, uint32_t &busy_m) {
-            urgent_m = 0; active_m = 0; busy_m = 0;
-            if (f_delay) urgent_m = __ballot_sync(FULL, akb > 0 && L_last >= 0 && L_last <= P.lax_threshold_ns);
-            if (coll) {
-                busy_m = __ballot_sync(FULL, launched > done);
-                active_m = __ballot_sync(FULL, akb > 0);
-                snapL[lane] = L_last;
-                snapLev[lane] = level;
-                __syncwarp();
-            } else if (f_bind && __any_sync(FULL, may_bind)) {
-                active_m = __ballot_sync(FULL, akb > 0);
-                snapL[lane] = L_last;
-                __syncwarp();
-            }
-        };
-        // a due lane can bind in this phase unless it is mid-task and the launch cost
-        // makes it yield before reaching the next task's first kernel
-        auto can_bind = [&]() -> bool {
-            return !(busy_launch > 0 && ((pc == PC_ENQUEUE && launched + 1 < task_end) ||
-                                         (pc == PC_ATTEMPT && launched != task_first)));
-        };
-
-        // ---- A2-A10: the event loop (R21) ----
-        // Warp-uniform: t_prev (time of the previous loop step) and `used`, the util
-        // per-mille of the running kernels (kept incrementally).
-        int64_t t_prev = -1;
-        uint32_t used = 0;
-        for (;;) {
-            // A2: next event time.  Every lane's next event is strictly after t_prev, so
-            // the warp minimum is taken on the 32-bit distance (one REDUX); distances that
-            // do not fit 32 bits saturate and fall back to the exact 64-bit minimum.
-            const int64_t mine = head_end < cpu_next ? head_end : cpu_next;
-            const uint64_t dl = (uint64_t)mine - (uint64_t)t_prev;   // exact when mine > t_prev
-            const uint32_t d32 = mine <= t_prev ? 0u : (dl >= 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)dl);
-            const uint32_t m = __reduce_min_sync(FULL, d32);
-            int64_t t;
-            if (m == 0xFFFFFFFFu) t = warp_min_nonneg(mine);
-            else t = t_prev + m;
-            if (t > H_stop) break;
-            if (m == 0u) {   // time must advance (invariant); report and stop this scenario
-                if (lane == 0 && atomicCAS((unsigned long long *)err, 0ull, (unsigned long long)ERR_TIME) == 0ull)
-                    err[1] = s;
-                break;
-            }
-            t_prev = t;
-            ++my_steps;
-
-            // Phase A: retire (R21, R19)
-            const bool ret = head_end == t;
-            bool dirty = __any_sync(FULL, ret);   // GPU state changed: Phase C must run
-            if (dirty) {
-                used -= __reduce_add_sync(FULL, ret ? head_util : 0u);
-                if (ret) retire(t);
-            }
-
-            // Phase B: CPU steps of every chain due at t, against the round snapshot (R21)
-            const bool due = cpu_next == t;
-            if (__any_sync(FULL, due)) {
-#ifdef URG_STATS
-                ++st_multi;
-#endif
-                uint32_t urgent_m = 0, active_m = 0, busy_m = 0;
-                if (urg) snapshot(due && can_bind(), urgent_m, active_m, busy_m);
-                bool nh = false;
-                if (due) nh = phase_b(t, urgent_m, active_m, busy_m);
-                dirty |= __any_sync(FULL, nh);
-            }
-
-
-            // Phase C: dispatch waiting stream heads by (level, ready, chain) under capacity (R20).
-            // Runs only when a kernel retired or a stream got a new head: otherwise every
-            // waiting head was already found not to fit and `used` has not decreased.
-            // The greedy scan in key order starts, each time, the smallest-key head that
-            // fits the capacity left (heads that do not fit stay unfit as `used` grows).
-            if (dirty) {
-#ifdef URG_STATS
-                ++st_dispatch;
-#endif
-                bool waiting = launched > done && head_end == INF64;
-                for (;;) {
-                    const uint32_t fit = __ballot_sync(FULL, waiting && used + head_u <= 1000u);
-                    if (!fit) break;
-                    int wl;
-                    if ((fit & (fit - 1)) == 0) wl = __ffs(fit) - 1;
-                    else {
-                        const bool in = (fit >> lane) & 1u;
-                        const uint64_t key = ((uint64_t)level << 56) | ((uint64_t)head_ready << 5) | (uint64_t)lane;
-                        const uint32_t hi = in ? (uint32_t)(key >> 32) : 0xFFFFFFFFu;
-                        const uint32_t mh = __reduce_min_sync(FULL, hi);
-                        const uint32_t ml = __reduce_min_sync(FULL, (in && hi == mh) ? (uint32_t)key : 0xFFFFFFFFu);
-                        wl = (int)(ml & 31u);
-                    }
-                    used += __shfl_sync(FULL, head_u, wl);
-                    if (lane == wl) { start_head(t); waiting = false; }
-                    if ((fit & (fit - 1)) == 0) break;   // the others did not fit before; `used` only grew
-                }
-            }
-        }
-
-        // ---- A11: end of horizon accounting (R7) and per-scenario records ----
-        if (valid) {
-            uint32_t first_unstarted = inst;
-            if (pc != PC_ARRIVE && pc != PC_DONE) { ++n_unfin; first_unstarted = inst + 1; }
-            if (pc != PC_DONE)
-                for (uint32_t i = first_unstarted; arrival(i) < H; ++i) { ++n_unfin; ++n_total; }
-            n_miss += n_unfin;
-            if (records) {
-                uint4 *r = (uint4 *)(records + ((uint64_t)jw * C + c) * 8);
-                r[0] = make_uint4(n_total, n_miss, n_early, n_unfin);
-                r[1] = make_uint4(n_launch, hash, (uint32_t)sum_rt, (uint32_t)(sum_rt >> 32));
-            }
-            // A12: aggregates (integer sums: order-independent, R23)
-            unsigned long long *a = agg + (uint64_t)c * stride;
-            atomicAdd(&a[0], (unsigned long long)n_total);
-            atomicAdd(&a[1], (unsigned long long)n_miss);
-            atomicAdd(&a[2], (unsigned long long)n_early);
-            atomicAdd(&a[3], (unsigned long long)n_unfin);
-            atomicAdd(&a[4], (unsigned long long)sum_rt);
-            if (n_total) atomicAdd(&a[5 + P.rt_bins + (uint64_t)100 * n_miss / n_total], 1ull);
-        }
-        my_launches += __reduce_add_sync(FULL, n_launch);
-    }
-    if (lane == 0) {
-        atomicAdd(&agg[(uint64_t)C * stride + URG_COLL_BINS + 0], my_launches);
-        atomicAdd(&agg[(uint64_t)C * stride + URG_COLL_BINS + 1], my_steps);
-#ifdef URG_STATS
-        atomicAdd(&work[4], st_single); atomicAdd(&work[5], st_multi);
-        atomicAdd(&work[6], st_dispatch); atomicAdd(&work[7], st_rebase);
-#endif
-    }
-}
-
-// ---------------------------------------------------------------------------
-// instantiation table (host side picks one per launch; see urg_api.cu)
-// ---------------------------------------------------------------------------
-#define URG_I(K, F)                                                                                  \
-    (const void *)urg_sim_kernel<K, F, false, false>, (const void *)urg_sim_kernel<K, F, true, false>,     \
-        (const void *)urg_sim_kernel<K, F, false, true>, (const void *)urg_sim_kernel<K, F, true, true>
-static const void *const g_sim_kernels[18][4] = {
-    {URG_I(K_FIFO, 0)},     {URG_I(K_STATIC, 0)},   {URG_I(K_URGENGO, 0)},  {URG_I(K_URGENGO, 1)},
-    {URG_I(K_URGENGO, 2)},  {URG_I(K_URGENGO, 3)},  {URG_I(K_URGENGO, 4)},  {URG_I(K_URGENGO, 5)},
-    {URG_I(K_URGENGO, 6)},  {URG_I(K_URGENGO, 7)},  {URG_I(K_URGENGO, 8)},  {URG_I(K_URGENGO, 9)},
-    {URG_I(K_URGENGO, 10)}, {URG_I(K_URGENGO, 11)}, {URG_I(K_URGENGO, 12)}, {URG_I(K_URGENGO, 13)},
-    {URG_I(K_URGENGO, 14)}, {URG_I(K_URGENGO, 15)}};
-#undef URG_I
+#define URG_PARTS 6
+#define URG_DECL(k) const void *urg_sim_part##k(uint32_t row, uint32_t col);
+URG_DECL(0) URG_DECL(1) URG_DECL(2) URG_DECL(3) URG_DECL(4) URG_DECL(5)
+#undef URG_DECL
 
 const void *urg_sim_kernel_for(uint32_t kind, uint32_t flags, bool kern_q, bool wide)
 {
     const uint32_t row = kind == K_FIFO ? 0 : kind == K_STATIC ? 1 : 2 + (flags & 15u);
-    return g_sim_kernels[row][(kern_q ? 1 : 0) + (wide ? 2 : 0)];
+    const uint32_t col = (kern_q ? 1u : 0u) + (wide ? 2u : 0u);
+    const void *(*parts[URG_PARTS])(uint32_t, uint32_t) = {urg_sim_part0, urg_sim_part1, urg_sim_part2,
+                                                          urg_sim_part3, urg_sim_part4, urg_sim_part5};
+    for (int k = 0; k < URG_PARTS; ++k)
+        if (const void *f = parts[k](row, col)) return f;
+    return nullptr;
 }
