@@ -11,6 +11,7 @@ Usage: python -m oracle.calibrate
 """
 import json
 import os
+from dataclasses import replace
 
 from oracle import oracle as O
 from workloads.configs import get_config
@@ -20,7 +21,8 @@ OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), 
 
 def main():
     cfg = get_config("paper11")
-    lth, n = O.calibrate(cfg.workload(), cfg.policies["urgengo"], cfg.batch, window_ns=30_000_000_000)
+    b = replace(cfg.batch, scenario_count=1)          # scenario 0 of configs[1] (Q5)
+    lth, n = O.calibrate(cfg.workload(), cfg.policies["urgengo"], b, window_ns=30_000_000_000)
     out = {"paper11": lth, "_samples": {"paper11": n},
            "_how": "python -m oracle.calibrate (PAPER.md:464-465, DESIGN.md Q5)"}
     with open(OUT, "w") as f:

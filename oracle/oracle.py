@@ -150,7 +150,25 @@ def run(w: Workload, p: Policy, b: Batch, trace_cap: int = 0) -> OracleResult:
     return OracleResult(rec, agg, None if tr is None else tr[: tlen.value].copy(), dt)
 
 
+def calibration_samples(w: Workload, p: Policy, b: Batch, window_ns: int = 30_000_000_000):
+    """Per-scenario calibration samples (laxities, in sampling order): list of int64 arrays."""
+    s, keep = _make_input(w, p, b)
+    f = lib().orc_calibration_samples
+    f.restype = ct.c_int
+    f.argtypes = [ct.POINTER(OrcInput), ct.c_int64, ct.c_void_p, ct.c_int64, ct.c_void_p]
+    end = min(b.horizon_ns, window_ns)
+    cap = end // 1_000_000 + 2
+    L = np.zeros((b.scenario_count, cap), np.int64)
+    n = np.zeros(b.scenario_count, np.int64)
+    rc = f(ct.byref(s), window_ns, L.ctypes.data, cap, n.ctypes.data)
+    del keep
+    if rc != 0:
+        raise ValueError(f"oracle rejected input (rc={rc})")
+    return [L[j, : n[j]].copy() for j in range(b.scenario_count)]
+
+
 def calibrate(w: Workload, p: Policy, b: Batch, window_ns: int = 30_000_000_000):
+    """L_th from the samples of every scenario of `b`, pooled."""
     s, keep = _make_input(w, p, b)
     n = ct.c_int64(0)
     lth = lib().orc_calibrate(ct.byref(s), window_ns, ct.byref(n))

@@ -814,26 +814,46 @@ int64_t orc_nearest_rank_lth(int64_t *L, int64_t n, int64_t pct)
     return L[k - 1];
 }
 
-/* TH_urgent calibration (Q5): run scenario
- * scenario_begin with the threshold disabled (L_th = -1), record every 1 ms of
- * the first min(H, window) the highest urgency among the AKB's active kernels,
- * and return the laxity of the nearest-rank 95th percentile of those urgencies.
- * *n_samples receives the number of samples; returns -1 if there were none. */
-int64_t orc_calibrate(const orc_input *in_, int64_t window_ns, int64_t *n_samples)
+/* Calibration samples ("periodically recording the highest urgency
+ * value among all active kernels in AKB"; Q5): each scenario of the batch
+ * is simulated with the threshold disabled (L_th = -1, nothing is truly urgent) and,
+ * every 1 ms of the first min(H, window), the laxity of the most urgent AKB entry is
+ * recorded (no sample when the AKB is empty or that laxity is negative).  Scenario j's
+ * samples go to L_out[j * cap ...], their number to n_out[j]. */
+int orc_calibration_samples(const orc_input *in_, int64_t window_ns, int64_t *L_out, int64_t cap, int64_t *n_out)
 {
     orc_input in = *in_;
     in.lax_threshold_ns = -1;
-    in.scenario_count = 1;
     int64_t end = in.horizon_ns < window_ns ? in.horizon_ns : window_ns;
-    int64_t cap = end / 1000000 + 2;
-    int64_t *L = calloc(cap, sizeof(int64_t));
-    int64_t n = 0;
     uint32_t *rec = calloc((size_t)in.num_chains * REC_WORDS, sizeof(uint32_t));
     int64_t *agg = calloc((size_t)in.num_chains * (AGG_COUNTERS + in.rt_bins + RATIO_BINS) + COLL_BINS + 2,
                           sizeof(int64_t));
-    sim_scenario(&in, in.scenario_begin, rec, agg, 0, 0, 0, L, cap, &n, end);
-    int64_t out = orc_nearest_rank_lth(L, n, 95);
-    if (n_samples) *n_samples = n;
-    free(L); free(rec); free(agg);
+    int rc = 0;
+    for (uint64_t j = 0; j < in.scenario_count && rc == 0; ++j)
+        rc = sim_scenario(&in, in.scenario_begin + j, rec, agg, 0, 0, 0, L_out + (int64_t)j * cap, cap,
+                          &n_out[j], end);
+    free(rec); free(agg);
+    return rc;
+}
+
+/* TH_urgent calibration (Q5): the samples of every
+ * scenario of the batch pooled, and the laxity of their nearest-rank 95th percentile
+ * urgency returned.  *n_samples receives the number of samples; -1 if none. */
+int64_t orc_calibrate(const orc_input *in, int64_t window_ns, int64_t *n_samples)
+{
+    int64_t end = in->horizon_ns < window_ns ? in->horizon_ns : window_ns;
+    int64_t cap = end / 1000000 + 2;
+    uint64_t cnt = in->scenario_count ? in->scenario_count : 1;
+    orc_input one = *in;
+    one.scenario_count = cnt;
+    int64_t *L = calloc((size_t)(cap * (int64_t)cnt), sizeof(int64_t));
+    int64_t *n = calloc(cnt, sizeof(int64_t));
+    orc_calibration_samples(&one, window_ns, L, cap, n);
+    int64_t m = 0;                                     /* pool: concatenate the scenarios' samples */
+    for (uint64_t j = 0; j < cnt; ++j)
+        for (int64_t i = 0; i < n[j]; ++i) L[m++] = L[(int64_t)j * cap + i];
+    int64_t out = orc_nearest_rank_lth(L, m, 95);
+    if (n_samples) *n_samples = m;
+    free(L); free(n);
     return out;
 }

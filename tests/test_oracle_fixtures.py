@@ -182,3 +182,37 @@ def test_collisions_need_concurrency():
         b = O.run(w, Policy(kind=URGENGO, flags=7, sync_mode=SYNC_ASYNC, lax_threshold_ns=lth), Batch(horizon_ns=1 * MS))
         assert not collision_hist(a.agg, 1, w.rt_bins).any()
         assert np.array_equal(a.records, b.records)
+
+
+def test_calibration_samples_w1():
+    """TH_urgent sampling (Q5) on W1 with H = 20 ms, threshold disabled.
+    Hand-derived: no AKB entry at 0 ms; A holds entries with last laxity 4 ms (its k1 attempt at
+    t = 1 ms) from 1 ms until its final sync returns at 10 ms, and is always more urgent than B
+    (92 ms) -> one 4 ms sample at each of 1..9 ms; nothing after.  A 5 ms window keeps 1..4 ms."""
+    p = Policy(kind=URGENGO, flags=7, sync_mode=SYNC_ASYNC, lax_threshold_ns=5 * MS)
+    s = O.calibration_samples(w1(), p, Batch(horizon_ns=20 * MS))
+    assert s[0].tolist() == [4 * MS] * 9
+    assert O.calibration_samples(w1(), p, Batch(horizon_ns=20 * MS), window_ns=5 * MS)[0].tolist() == [4 * MS] * 4
+    assert O.calibrate(w1(), p, Batch(horizon_ns=20 * MS)) == (4 * MS, 9)
+
+
+def test_calibration_skips_negative_laxity_w3():
+    """W3 with the threshold disabled: the only AKB entry (k0, t = 1..2.8 ms) has laxity
+    4.5 - 2 - 2 - 1 = -0.5 ms < 0, so every sample is skipped (SPEC.md:328 'negatives
+    excluded') and the calibration has no threshold (-1)."""
+    p = Policy(kind=URGENGO, flags=7, sync_mode=SYNC_ASYNC, lax_threshold_ns=5 * MS)
+    assert O.calibration_samples(w3(), p, Batch(horizon_ns=20 * MS))[0].tolist() == []
+    assert O.calibrate(w3(), p, Batch(horizon_ns=20 * MS)) == (-1, 0)
+
+
+def test_calibration_pools_scenarios():
+    """A batch's threshold is the nearest-rank percentile of all its scenarios' samples."""
+    from workloads import get_config
+    cfg = get_config("paper11")
+    b = Batch(seed=cfg.batch.seed, scenario_begin=3, scenario_count=3, horizon_ns=2_000 * MS, ftight_permille=400)
+    p = cfg.policies["urgengo"]
+    per = O.calibration_samples(cfg.workload(), p, b)
+    assert all(len(x) > 0 for x in per)
+    lth, n = O.calibrate(cfg.workload(), p, b)
+    assert n == sum(len(x) for x in per)
+    assert lth == O.nearest_rank_lth(np.concatenate(per))
