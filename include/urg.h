@@ -149,6 +149,21 @@ urg_status urg_simulate_batch_host(const urg_workload *w, const urg_policy *p, c
  * earlier urg_simulate_batch (URG_EINTERNAL, *scenario_out = offending scenario). */
 urg_status urg_check(const urg_workload *w, void *cuda_stream, int64_t *scenario_out);
 
+/* TH_urgent calibration ("periodically recording the highest urgency
+ * value among all active kernels in AKB ... the 95th percentile"; Q5).
+ * Every scenario of b is simulated under p (UrgenGo) with the threshold disabled; every
+ * 1 ms of the first min(H, window_ns) the laxity of the most urgent AKB entry is
+ * sampled (none when the AKB is empty or that laxity is negative); the samples of all
+ * scenarios are pooled and the laxity of their nearest-rank 95th-percentile urgency
+ * (rank floor(0.95 m) + 1 in ascending urgency) is L_th = 1/TH_urgent.
+ * scratch: DEVICE int64[urg_calibration_words(w, b, window_ns)]; after the call it holds
+ *          [count] per-scenario sample counts, then [count][cap] samples in time order.
+ * result:  DEVICE int64[2] = {L_th (or -1 with no sample), number of samples m}.
+ * Asynchronous on cuda_stream; URG_ERANGE if scratch is too small. */
+uint64_t urg_calibration_words(const urg_workload *w, const urg_batch *b, int64_t window_ns);
+urg_status urg_calibrate(const urg_workload *w, const urg_policy *p, const urg_batch *b, int64_t window_ns,
+                         int64_t *scratch, uint64_t scratch_words, int64_t *result, void *cuda_stream);
+
 /* Eq. 3 from a HOST aggregate buffer: per_chain_out[c] =
  * M_miss/M_total (0 when M_total = 0); overall = mean over chains with M_total > 0. */
 urg_status urg_miss_ratios(const urg_workload *w, const int64_t *agg_host, double *per_chain_out,

@@ -19,7 +19,10 @@
 
 typedef void (*urg_sim_fn)(const uint8_t *blob, const UrgSimParams P, uint32_t *records, unsigned long long *agg,
                            unsigned long long *work, long long *err);
-const void *urg_sim_kernel_for(uint32_t kind, uint32_t flags, bool kern_q, bool wide);   // urg_sim.cu
+const void *urg_sim_kernel_for(uint32_t kind, uint32_t flags, bool kern_q, bool wide, bool cal);   // urg_sim.cu
+extern "C" __global__ void urg_cal_hist_kernel(const int64_t *buf, uint64_t count, uint64_t cap, long long *ws,
+                                               int pass);
+extern "C" __global__ void urg_cal_pick_kernel(long long *ws, int pass, int pct, long long *result);
 extern "C" __global__ void urg_philox_kat_kernel(const uint4 *ctr, const uint2 *key, uint4 *out, int n);
 
 struct urg_workload {
@@ -282,7 +285,7 @@ extern "C" urg_status urg_simulate_batch(const urg_workload *w, const urg_policy
     bool wide = b->scenario_count > (uint64_t)w->num_sms * 16u;
     if (const char *ev = getenv("URG_WIDE")) wide = atoi(ev) != 0;
     const urg_sim_fn fn = (urg_sim_fn)urg_sim_kernel_for(p->kind, p->kind == URG_URGENGO ? p->flags : 0,
-                                                         w->has_kern_q, wide);
+                                                         w->has_kern_q, wide, false);
     P.blob_bytes = (uint32_t)w->blob.size();
     P.mbar_offset = align16(P.blob_bytes);
     P.snap_offset = align16(P.mbar_offset + 16);
@@ -293,6 +296,58 @@ extern "C" urg_status urg_simulate_batch(const urg_workload *w, const urg_policy
     fn<<<ctas, warps * 32, P.smem_bytes, s>>>(w->d_blob, P, o->records, (unsigned long long *)o->agg, w->d_work,
                                               w->d_err);
     CUDA_TRY(cudaGetLastError(), "launching urg_sim_kernel");
+    return URG_OK;
+}
+
+// ---- TH_urgent calibration (Q5) ----
+static int64_t cal_end(const urg_batch *b, int64_t window_ns) { return b->horizon_ns < window_ns ? b->horizon_ns : window_ns; }
+static uint64_t cal_cap(const urg_batch *b, int64_t window_ns) { return (uint64_t)(cal_end(b, window_ns) / 1000000) + 2; }
+
+extern "C" uint64_t urg_calibration_words(const urg_workload *w, const urg_batch *b, int64_t window_ns)
+{
+    if (!w || !b || window_ns < 0) return 0;
+    return b->scenario_count + b->scenario_count * cal_cap(b, window_ns) + 260;
+}
+
+extern "C" urg_status urg_calibrate(const urg_workload *w, const urg_policy *p, const urg_batch *b, int64_t window_ns,
+                                    int64_t *scratch, uint64_t scratch_words, int64_t *result, void *cuda_stream)
+{
+    g_err.clear();
+    urg_status st = validate_call(w, p, b);
+    if (st != URG_OK) return st;
+    if (p->kind != URG_URGENGO) return fail(URG_EINVAL, "policy.kind must be URG_URGENGO (the AKB is UrgenGo's)");
+    if (window_ns < 0) return fail(URG_EINVAL, "window_ns must be >= 0");
+    if (!scratch || !result) return fail(URG_EINVAL, "scratch and result must not be NULL");
+    if (b->scenario_count == 0) return fail(URG_EINVAL, "batch.scenario_count must be >= 1");
+    const uint64_t need = urg_calibration_words(w, b, window_ns);
+    if (scratch_words < need) return fail(URG_ERANGE, "scratch has %llu words, calibration needs %llu",
+                                          (unsigned long long)scratch_words, (unsigned long long)need);
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    urg_policy pc = *p;
+    pc.lax_threshold_ns = -1;                                   // nothing is truly urgent while sampling
+    UrgSimParams P;
+    fill_params(w, &pc, b, P);
+    P.cal_end = cal_end(b, window_ns);
+    P.cal_cap = cal_cap(b, window_ns);
+    P.cal_buf = scratch;
+    const urg_sim_fn fn = (urg_sim_fn)urg_sim_kernel_for(URG_URGENGO, pc.flags, w->has_kern_q, false, true);
+    P.blob_bytes = (uint32_t)w->blob.size();
+    P.mbar_offset = align16(P.blob_bytes);
+    P.snap_offset = align16(P.mbar_offset + 16);
+    int warps, ctas;
+    st = geometry(w, (const void *)fn, b->scenario_count, P.snap_offset, warps, ctas, P.smem_bytes);
+    if (st != URG_OK) return st;
+    long long *ws = (long long *)(scratch + b->scenario_count + b->scenario_count * P.cal_cap);
+    CUDA_TRY(cudaMemsetAsync(ws, 0, 260 * 8, s), "cudaMemsetAsync(select workspace)");
+    CUDA_TRY(cudaMemsetAsync(w->d_work, 0, 8, s), "cudaMemsetAsync(work counter)");
+    fn<<<ctas, warps * 32, P.smem_bytes, s>>>(w->d_blob, P, nullptr, nullptr, w->d_work, w->d_err);
+    CUDA_TRY(cudaGetLastError(), "launching the calibration simulation");
+    int grid = (int)(b->scenario_count < (uint64_t)w->num_sms * 4 ? b->scenario_count : (uint64_t)w->num_sms * 4);
+    for (int pass = 7; pass >= 0; --pass) {
+        urg_cal_hist_kernel<<<grid, 256, 0, s>>>(scratch, b->scenario_count, P.cal_cap, ws, pass);
+        urg_cal_pick_kernel<<<1, 32, 0, s>>>(ws, pass, 95, (long long *)result);
+    }
+    CUDA_TRY(cudaGetLastError(), "launching the nearest-rank selection");
     return URG_OK;
 }
 

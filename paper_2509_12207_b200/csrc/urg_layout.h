@@ -51,4 +51,9 @@ struct UrgSimParams {
     uint32_t fa_num, fa_den, fd_num, fd_den, ftight_permille, tight_explicit, tight_mask;
     // staging
     uint32_t blob_bytes, snap_offset, mbar_offset, smem_bytes;
+    // TH_urgent calibration build only: sampling end, sample rows ([count] counts, then
+    // [count][cal_cap] laxities)
+    int64_t cal_end;
+    int64_t *cal_buf;
+    uint64_t cal_cap;
 };

@@ -126,7 +126,11 @@ struct Tmpl {   // shared-memory views of the staged template
 // WIDE: the throughput build (1024 threads per CTA, so <= 64 registers and 32 warps per
 // SM) for batches that fill the GPU; otherwise the latency build (512 threads, ~100
 // registers), faster per scenario when there are fewer scenarios than warp slots.
-template <int KIND, int FLAGS, bool KQ, bool WIDE>
+//
+// CAL: the TH_urgent calibration build (Q5): every 1 ms of
+// simulated time before P.cal_end the laxity of the most urgent AKB entry is appended
+// to the scenario's sample row; no records or aggregates are written.
+template <int KIND, int FLAGS, bool KQ, bool WIDE, bool CAL = false>
 __global__ void __launch_bounds__(WIDE ? 1024 : 512, 1)
 urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t *__restrict__ records,
                unsigned long long *__restrict__ agg, unsigned long long *__restrict__ work,
@@ -308,7 +312,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                         hash = (hash ^ (uint32_t)((uint64_t)rt >> 32)) * 16777619u;
                         int64_t bin = rt / P.rt_bin_ns;
                         if (bin > (int64_t)P.rt_bins - 1) bin = P.rt_bins - 1;
-                        atomicAdd(&agg[(uint64_t)c * stride + 5 + bin], 1ull);
+                        if (!CAL) atomicAdd(&agg[(uint64_t)c * stride + 5 + bin], 1ull);
                         next_inst = true;
                     }
                 }
@@ -369,7 +373,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                             mm &= mm - 1;
                             k += (snapLev[o] <= level && urgency_key(snapL[o]) < own) ? 1u : 0u;
                         }
-                        if (k) atomicAdd(&agg[(uint64_t)C * stride + (k + 1 > 32 ? 32 : k + 1)], 1ull);
+                        if (k && !CAL) atomicAdd(&agg[(uint64_t)C * stride + (k + 1 > 32 ? 32 : k + 1)], 1ull);
                     }
                     const bool last = launched == task_end;
                     if (last) rem_c -= T.task[cr.task_base + task].cpu_estimate_ns;
@@ -481,6 +485,8 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         // per-mille of the running kernels (kept incrementally).
         int64_t t_prev = -1;
         uint32_t used = 0;
+        int64_t cal_next = 0;                   // CAL: next sampling time
+        uint32_t cal_n = 0;                     // CAL: samples of this scenario
         for (;;) {
             // A2: next event time.  Every lane's next event is strictly after t_prev, so
             // the warp minimum is taken on the 32-bit distance (one REDUX); distances that
@@ -492,6 +498,25 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             int64_t t;
             if (m == 0xFFFFFFFFu) t = warp_min_nonneg(mine);
             else t = t_prev + m;
+            if (CAL && cal_next < P.cal_end && cal_next < t) {
+                // the state between two steps is constant: one warp max of the AKB urgency
+                // keys (order-preserving unsigned), then one sample per elapsed 1 ms tick
+                const bool act = valid && akb > 0;
+                const uint64_t u = act ? ((uint64_t)urgency_key(L_last) ^ 0x8000000000000000ull) : 0ull;
+                const uint32_t mh = __reduce_max_sync(FULL, (uint32_t)(u >> 32));
+                const uint32_t ml = __reduce_max_sync(FULL, (uint32_t)(u >> 32) == mh ? (uint32_t)u : 0u);
+                const int64_t key = (int64_t)((((uint64_t)mh << 32) | ml) ^ 0x8000000000000000ull);
+                const bool have = __any_sync(FULL, act);
+                const bool keep = have && key >= 0;                   // skip none / negative laxity
+                const int64_t bestL = key == INF64 ? 0 : ((int64_t)1 << 62) - key;
+                for (; cal_next < P.cal_end && cal_next < t; cal_next += 1000000) {
+                    if (keep) {
+                        if (lane == 0 && cal_n < P.cal_cap) P.cal_buf[P.scenario_count + jw * P.cal_cap + cal_n] = bestL;
+                        ++cal_n;
+                    }
+                }
+            }
+            if (CAL && cal_next >= P.cal_end) break;   // no sample left to take
             if (t > H_stop) break;
             if (m == 0u) {   // time must advance (invariant); report and stop this scenario
                 if (lane == 0 && atomicCAS((unsigned long long *)err, 0ull, (unsigned long long)ERR_TIME) == 0ull)
@@ -553,6 +578,10 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             }
         }
 
+        if (CAL) {   // sample count of this scenario; no records or aggregates
+            if (lane == 0) P.cal_buf[jw] = (int64_t)cal_n;
+            continue;
+        }
         // ---- A11: end of horizon accounting (R7) and per-scenario records ----
         if (valid) {
             uint32_t first_unstarted = inst;
@@ -577,6 +606,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         my_launches += __reduce_add_sync(FULL, n_launch);
     }
     if (lane == 0) {
+        if (CAL) return;
         atomicAdd(&agg[(uint64_t)C * stride + URG_COLL_BINS + 0], my_launches);
         atomicAdd(&agg[(uint64_t)C * stride + URG_COLL_BINS + 1], my_steps);
 #ifdef URG_STATS
@@ -591,18 +621,25 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
 // instantiation rows: 0 FIFO, 1 STATIC, 2 + f UrgenGo with flags f (0..15);
 // columns: (per-kernel factor table) + 2 * (throughput build)
 // ---------------------------------------------------------------------------
-#define URG_SIM_ROWS 18
+// rows 18 + f: the calibration build of UrgenGo with flags f (latency build only)
+#define URG_SIM_ROWS 34
 template <int ROW>
 struct UrgRow {
     static constexpr int K = ROW == 0 ? K_FIFO : ROW == 1 ? K_STATIC : K_URGENGO;
-    static constexpr int F = ROW < 2 ? 0 : ROW - 2;
+    static constexpr int F = ROW < 2 ? 0 : ROW < 18 ? ROW - 2 : ROW - 18;
+    static constexpr bool C = ROW >= 18;
     static const void *get(uint32_t col)
     {
-        switch (col) {
-        case 0: return (const void *)urg_sim_kernel<K, F, false, false>;
-        case 1: return (const void *)urg_sim_kernel<K, F, true, false>;
-        case 2: return (const void *)urg_sim_kernel<K, F, false, true>;
-        default: return (const void *)urg_sim_kernel<K, F, true, true>;
+        if constexpr (C) {   // the calibration build exists in the latency variant only
+            return (col & 1u) ? (const void *)urg_sim_kernel<K, F, true, false, true>
+                              : (const void *)urg_sim_kernel<K, F, false, false, true>;
+        } else {
+            switch (col) {
+            case 0: return (const void *)urg_sim_kernel<K, F, false, false>;
+            case 1: return (const void *)urg_sim_kernel<K, F, true, false>;
+            case 2: return (const void *)urg_sim_kernel<K, F, false, true>;
+            default: return (const void *)urg_sim_kernel<K, F, true, true>;
+            }
         }
     }
 };

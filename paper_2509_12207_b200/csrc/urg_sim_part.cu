@@ -19,7 +19,9 @@ const void *URG_PART_FN(uint32_t row, uint32_t col)
     switch (row) {
         URG_ROW(0) URG_ROW(1) URG_ROW(2) URG_ROW(3) URG_ROW(4) URG_ROW(5) URG_ROW(6) URG_ROW(7) URG_ROW(8)
         URG_ROW(9) URG_ROW(10) URG_ROW(11) URG_ROW(12) URG_ROW(13) URG_ROW(14) URG_ROW(15) URG_ROW(16)
-        URG_ROW(17)
+        URG_ROW(17) URG_ROW(18) URG_ROW(19) URG_ROW(20) URG_ROW(21) URG_ROW(22) URG_ROW(23) URG_ROW(24)
+        URG_ROW(25) URG_ROW(26) URG_ROW(27) URG_ROW(28) URG_ROW(29) URG_ROW(30) URG_ROW(31) URG_ROW(32)
+        URG_ROW(33)
     default: return nullptr;
     }
 }

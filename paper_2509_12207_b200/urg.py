@@ -66,7 +66,8 @@ class OutputsS(ct.Structure):
 
 
 SYMBOLS = ["urg_create_workload", "urg_destroy_workload", "urg_agg_words", "urg_template_bytes", "urg_simulate_batch",
-           "urg_simulate_batch_host", "urg_check", "urg_miss_ratios", "urg_last_error"]
+           "urg_simulate_batch_host", "urg_check", "urg_miss_ratios", "urg_last_error",
+           "urg_calibration_words", "urg_calibrate"]
 
 _lib = None
 
@@ -89,6 +90,11 @@ def lib():
         L.urg_agg_words.argtypes = [ct.c_void_p]
         L.urg_template_bytes.restype = ct.c_uint64
         L.urg_template_bytes.argtypes = [ct.c_void_p]
+        L.urg_calibration_words.restype = ct.c_uint64
+        L.urg_calibration_words.argtypes = [ct.c_void_p, ct.POINTER(BatchS), ct.c_int64]
+        L.urg_calibrate.restype = ct.c_int
+        L.urg_calibrate.argtypes = [ct.c_void_p, ct.POINTER(PolicyS), ct.POINTER(BatchS), ct.c_int64, ct.c_void_p,
+                                    ct.c_uint64, ct.c_void_p, ct.c_void_p]
         for f in (L.urg_simulate_batch, L.urg_simulate_batch_host):
             f.restype = ct.c_int
             f.argtypes = [ct.c_void_p, ct.POINTER(PolicyS), ct.POINTER(BatchS), ct.POINTER(OutputsS), ct.c_void_p]
@@ -190,6 +196,24 @@ class DeviceWorkload:
         o = OutputsS(None if records is None else records.ctypes.data, agg.ctypes.data)
         _check(lib().urg_simulate_batch_host(self.handle, ct.byref(policy_struct(p)), ct.byref(batch_struct(b)),
                                              ct.byref(o), _stream_handle(stream)))
+
+    def calibrate(self, p: Policy, b: Batch, window_ns: int = 30_000_000_000, stream=None):
+        """urg_calibrate: L_th = 1/TH_urgent from the batch's pooled samples.
+        Returns (L_th, number of samples, per-scenario sample lists)."""
+        import torch
+        bs = batch_struct(b)
+        words = int(lib().urg_calibration_words(self.handle, ct.byref(bs), window_ns))
+        scratch = torch.zeros(words, dtype=torch.int64, device="cuda")
+        res = torch.zeros(2, dtype=torch.int64, device="cuda")
+        _check(lib().urg_calibrate(self.handle, ct.byref(policy_struct(p)), ct.byref(bs), window_ns,
+                                   scratch.data_ptr(), words, res.data_ptr(), _stream_handle(stream)))
+        self.check(stream)
+        r = res.cpu().numpy()
+        sc = scratch.cpu().numpy()
+        cnt = b.scenario_count
+        cap = (min(b.horizon_ns, window_ns) // 1_000_000) + 2
+        rows = [sc[cnt + j * cap: cnt + j * cap + int(sc[j])] for j in range(cnt)]
+        return int(r[0]), int(r[1]), rows
 
     def check(self, stream=None) -> None:
         s = ct.c_int64(0)

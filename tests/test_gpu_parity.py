@@ -287,3 +287,48 @@ def test_sweep_points_match_oracle():
         tot = o.records[:, :, 0].astype(np.int64).sum(0)
         miss = o.records[:, :, 1].astype(np.int64).sum(0)
         assert r.overall_miss == O.overall_miss_ratio(miss, tot), pt.label
+
+
+def _gpu_calibrate(w, p, b, window_ns=30_000_000_000):
+    from paper_2509_12207_b200.urg import DeviceWorkload
+    with DeviceWorkload(w) as dw:
+        return dw.calibrate(p, b, window_ns)
+
+
+def test_calibration_fixtures():
+    """urg_calibrate on the hand-worked W1 / W3 sampling pins."""
+    p = Policy(kind=URGENGO, flags=7, sync_mode=SYNC_ASYNC, lax_threshold_ns=5 * MS)
+    lth, n, rows = _gpu_calibrate(w1(), p, Batch(horizon_ns=20 * MS))
+    assert (lth, n) == (4 * MS, 9) and rows[0].tolist() == [4 * MS] * 9
+    lth, n, rows = _gpu_calibrate(w1(), p, Batch(horizon_ns=20 * MS), window_ns=5 * MS)
+    assert n == 4
+    assert _gpu_calibrate(w3(), p, Batch(horizon_ns=20 * MS))[:2] == (-1, 0)
+
+
+def test_calibration_paper11_matches_stored_threshold():
+    """configs[1] scenario 0, 30 s window (10 s horizon): the GPU reproduces the oracle's
+    samples one by one and the stored L_th (workloads/calibrated.json)."""
+    import json
+    import os
+    cfg = get_config("paper11")
+    w, p = cfg.workload(), cfg.policies["urgengo"]
+    b = Batch(seed=cfg.batch.seed, scenario_count=1, horizon_ns=cfg.batch.horizon_ns, ftight_permille=400)
+    lth, n, rows = _gpu_calibrate(w, p, b)
+    stored = json.load(open(os.path.join(os.path.dirname(os.path.dirname(__file__)), "workloads", "calibrated.json")))
+    assert (lth, n) == (stored["paper11"], stored["_samples"]["paper11"])
+    assert np.array_equal(rows[0], O.calibration_samples(w, p, b)[0])
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_calibration_pooled_random(seed):
+    rng = random.Random(7000 + seed)
+    w = random_workload(rng, C=rng.choice([2, 5, 11, 32]))
+    p = random_policy(rng)
+    p.kind = URGENGO
+    b = Batch(seed=seed, scenario_begin=rng.randint(0, 100), scenario_count=rng.randint(1, 30),
+              horizon_ns=rng.choice([200, 500]) * MS, ftight_permille=rng.choice([0, 400]))
+    win = rng.choice([50 * MS, 30_000 * MS])
+    lth, n, rows = _gpu_calibrate(w, p, b, win)
+    orows = O.calibration_samples(w, p, b, win)
+    assert [r.tolist() for r in rows] == [r.tolist() for r in orows]
+    assert (lth, n) == O.calibrate(w, p, b, win)
