@@ -51,6 +51,7 @@ class OrcInput(ct.Structure):
         ("kind", ct.c_uint32), ("flags", ct.c_uint32), ("sync_mode", ct.c_uint32),
         ("delta_eval_ns", ct.c_int64), ("lax_threshold_ns", ct.c_int64), ("sleep_ns", ct.c_int64),
         ("util_exempt_permille", ct.c_uint32),
+        ("noise_permille", ct.c_uint32), ("cpu_ma_window", ct.c_uint32),
         ("seed", ct.c_uint64), ("scenario_begin", ct.c_uint64), ("scenario_count", ct.c_uint64),
         ("horizon_ns", ct.c_int64),
         ("fa_num", ct.c_uint32), ("fa_den", ct.c_uint32), ("fd_num", ct.c_uint32), ("fd_den", ct.c_uint32),
@@ -111,6 +112,7 @@ def _make_input(w: Workload, p: Policy, b: Batch):
         inst_q16=_ptr(inst), kern_q16=_ptr(kern), rt_bin_ns=w.rt_bin_ns, rt_bins=w.rt_bins,
         kind=p.kind, flags=p.flags, sync_mode=p.sync_mode, delta_eval_ns=p.delta_eval_ns,
         lax_threshold_ns=p.lax_threshold_ns, sleep_ns=p.sleep_ns, util_exempt_permille=p.util_exempt_permille,
+        noise_permille=p.noise_permille, cpu_ma_window=p.cpu_ma_window,
         seed=b.seed, scenario_begin=b.scenario_begin, scenario_count=b.scenario_count, horizon_ns=b.horizon_ns,
         fa_num=b.fa_num, fa_den=b.fa_den, fd_num=b.fd_num, fd_den=b.fd_den,
         ftight_permille=b.ftight_permille, tight_explicit=b.tight_explicit, tight_mask=b.tight_mask,

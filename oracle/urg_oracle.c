@@ -55,6 +55,8 @@ typedef struct {
     uint32_t kind, flags, sync_mode;
     int64_t delta_eval_ns, lax_threshold_ns, sleep_ns;
     uint32_t util_exempt_permille;
+    uint32_t noise_permille;    /* urgency-estimation noise epsilon, per task instance (R25) */
+    uint32_t cpu_ma_window;     /* CPU-segment moving-average window W, 0 = profiled estimate (R26) */
     /* batch */
     uint64_t seed, scenario_begin, scenario_count;
     int64_t horizon_ns;
@@ -64,7 +66,7 @@ typedef struct {
 enum { ORC_FIFO = 0, ORC_STATIC = 1, ORC_URGENGO = 2 };
 enum { ORC_BIND = 1, ORC_DELAY = 2, ORC_EARLY_EXIT = 4, ORC_COLLISIONS = 8 };
 enum { ORC_ASYNC = 0, ORC_EACH = 1, ORC_BATCHED = 2, ORC_OVERLAP = 3 };
-enum { TAG_ARR = 1, TAG_TIGHT = 2, TAG_INST = 3, TAG_KERN = 4, TAG_SYNC = 5 };
+enum { TAG_ARR = 1, TAG_TIGHT = 2, TAG_INST = 3, TAG_KERN = 4, TAG_SYNC = 5, TAG_NOISE = 6 };
 
 /* trace kinds */
 enum { TR_STEP = 1, TR_INST_START, TR_TASK_START, TR_EVAL, TR_DELAY, TR_BIND, TR_ENQUEUE,
@@ -236,6 +238,10 @@ typedef struct {
     uint32_t batch_start;           /* first kernel of the open batch */
     uint32_t sync_target, sync_ord;
     int64_t sync_cost;
+    /* CPU-segment predictor (R26): measured durations per task, newest last */
+    uint32_t *cpu_hist;             /* [M][W] ring of measurements */
+    uint32_t *cpu_hist_n;           /* [M] measurements recorded so far */
+    uint32_t *cpu_pred;             /* [M] ~E^cpu_j used by the current instance */
     /* AKB instance of the chain */
     orc_akb_entry *akb;
     uint32_t akb_n;
@@ -326,12 +332,28 @@ static int64_t sync_cost(const orc_sim *S, uint32_t c, uint32_t i, uint32_t ord)
 }
 
 /* ---- urgency evaluation trigger (R8): Eq. 2 + AKB refresh ---- */
+/* Urgency-estimation noise ("noise to the estimated execution times
+ * used to calculate task urgency ... uniformly sampled for each task instance";
+ * DESIGN.md R25): the remaining estimated work of Eq. 2 during task tau of instance i
+ * is scaled by (1000 + n)/1000, n uniform in [-eps, eps] per-mille, floor division. */
+static int64_t noisy_laxity(const orc_sim *S, uint32_t c, int64_t t_arr, int64_t D, int64_t t, int64_t lax)
+{
+    const orc_input *in = S->in;
+    const orc_lane *L = &S->lane[c];
+    if (in->noise_permille == 0) return lax;
+    uint32_t w = orc_word(in->seed, S->s, TAG_NOISE, c, L->inst, L->task);
+    int64_t n = (int64_t)(w % (2 * in->noise_permille + 1)) - (int64_t)in->noise_permille;
+    int64_t remaining = t_arr + D - t - lax;           /* sum of the remaining estimates (>= 0) */
+    return t_arr + D - (remaining * (1000 + n)) / 1000 - t;
+}
+
 static int64_t evaluate(orc_sim *S, uint32_t c, int64_t t)
 {
     orc_lane *L = &S->lane[c];
     const orc_input *in = S->in;
     int64_t lax = orc_eq2_laxity(L->t_arr, L->Dp, in->k_est + L->kbase, L->N, L->launched,
-                                 in->t_cpu_est + L->tbase, L->M, L->cpu_idx, t);
+                                 L->cpu_pred, L->M, L->cpu_idx, t);
+    lax = noisy_laxity(S, c, L->t_arr, L->Dp, t, lax);
     L->T_last = t; L->L_last = lax;
     for (uint32_t e = 0; e < L->akb_n; ++e) { L->akb[e].T = t; L->akb[e].L = lax; }
     tr(S, t, TR_EVAL, c, L->inst, lax, L->launched);
@@ -404,6 +426,18 @@ static void start_instance(orc_sim *S, uint32_t c, int64_t t)
     L->Fc = inst_factor(S, c, L->inst, 1, S->in->ch_cpu_sigma[c]);
     L->task = 0; L->launched = 0; L->cpu_idx = 0; L->done = 0; L->sync_ord = 0;
     L->q_head = L->q_tail = 0;
+    /* ~E^cpu_j for this instance ("moving averages across recent instances";
+     * DESIGN.md R26): mean of the last min(W, h_j) measured durations of task j, floor;
+     * the profiled estimate while task j has no measurement or W = 0 */
+    const orc_input *in = S->in;
+    for (uint32_t j = 0; j < L->M; ++j) {
+        uint32_t W = in->cpu_ma_window, h = L->cpu_hist_n[j];
+        if (W == 0 || h == 0) { L->cpu_pred[j] = in->t_cpu_est[L->tbase + j]; continue; }
+        uint32_t k = h < W ? h : W;
+        uint64_t sum = 0;
+        for (uint32_t q = 0; q < k; ++q) sum += L->cpu_hist[j * W + (h - 1 - q) % W];
+        L->cpu_pred[j] = (uint32_t)(sum / k);
+    }
     tr(S, t, TR_INST_START, c, L->inst, L->t_arr, 0);
 }
 
@@ -487,6 +521,11 @@ static void lane_step(orc_sim *S, uint32_t c, int64_t t)
                 }
             }
             int64_t e = cpu_duration(S, c);
+            if (in->cpu_ma_window) {                     /* measured segment time (clock_gettime) */
+                uint32_t W = in->cpu_ma_window;
+                L->cpu_hist[L->task * W + L->cpu_hist_n[L->task] % W] = (uint32_t)e;
+                L->cpu_hist_n[L->task]++;
+            }
             L->pc = PC_CPU_DONE; L->cpu_next = t + e;
             if (e > 0) return;
             continue;
@@ -679,6 +718,10 @@ static int sim_scenario(const orc_input *in, uint64_t s, uint32_t *rec, int64_t 
         for (uint32_t j = 0; j < L->M; ++j) L->N += in->t_nk[tb + j];
         tb += L->M; kb += L->N;
         L->akb = calloc(L->N, sizeof(orc_akb_entry));
+        L->cpu_hist = calloc((size_t)L->M * (in->cpu_ma_window ? in->cpu_ma_window : 1), sizeof(uint32_t));
+        L->cpu_hist_n = calloc(L->M, sizeof(uint32_t));
+        L->cpu_pred = calloc(L->M, sizeof(uint32_t));
+        for (uint32_t j = 0; j < L->M; ++j) L->cpu_pred[j] = in->t_cpu_est[L->tbase + j];
         L->q = calloc(L->N, sizeof(orc_stream_entry));
         L->hash = 2166136261u;
     }
@@ -762,7 +805,7 @@ static int sim_scenario(const orc_input *in, uint64_t s, uint32_t *rec, int64_t 
         int64_t *a = agg + (int64_t)c * stride;
         a[0] += L->total; a[1] += L->miss; a[2] += L->early; a[3] += L->unfin; a[4] += (int64_t)L->sum_rt;
         if (L->total) a[AGG_COUNTERS + in->rt_bins + (uint64_t)100 * L->miss / L->total] += 1;
-        free(L->akb); free(L->q);
+        free(L->akb); free(L->q); free(L->cpu_hist); free(L->cpu_hist_n); free(L->cpu_pred);
     }
     agg[(int64_t)S.C * stride + COLL_BINS + 0] += S.launches;
     agg[(int64_t)S.C * stride + COLL_BINS + 1] += S.steps;

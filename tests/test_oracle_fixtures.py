@@ -216,3 +216,70 @@ def test_calibration_pools_scenarios():
     lth, n = O.calibrate(cfg.workload(), p, b)
     assert n == sum(len(x) for x in per)
     assert lth == O.nearest_rank_lth(np.concatenate(per))
+
+
+def _evals(r, chain):
+    return [(int(t), int(a)) for t, k, c, i, a, b in r.trace if k == O.TRACE_CODES["EVAL"] and c == chain]
+
+
+@pytest.mark.parametrize("eps", [1, 300, 500])
+def test_noise_w1_laxities(eps):
+    """R25: during task tau of instance i the remaining estimated work R of
+    Eq. 2 is scaled by (1000 + n)/1000, n = (w mod (2 eps + 1)) - eps, w the Philox word
+    (tag 6, chain, instance, tau) -- drawn here with the KAT-pinned Philox primitive.  W1's
+    chain A at t = 1 ms: R = 4 + 1 = 5 ms (k0 attempt) and 2 + 1 = 3 ms (k1 attempt)."""
+    b = Batch(seed=77, horizon_ns=1 * MS)
+    p = Policy(kind=URGENGO, flags=0, sync_mode=SYNC_ASYNC, lax_threshold_ns=5 * MS, noise_permille=eps)
+    r = O.run(w1(), p, b, trace_cap=1000)
+    w = int(O.philox([0, (6 << 24) | (0 << 16), 0, 0], [b.seed & 0xFFFFFFFF, b.seed >> 32])[0])
+    n = w % (2 * eps + 1) - eps
+    want = [(0, 8 * MS - (5 * MS * (1000 + n)) // 1000),            # task start, R = 4 + 1 ms
+            (1 * MS, 8 * MS - (5 * MS * (1000 + n)) // 1000 - 1 * MS),
+            (1 * MS, 8 * MS - (3 * MS * (1000 + n)) // 1000 - 1 * MS)]
+    assert _evals(r, 0)[:3] == want
+
+
+def test_noise_zero_is_exact_eq2():
+    from workloads import get_config
+    cfg = get_config("paper11")
+    b = Batch(seed=cfg.batch.seed, scenario_count=2, horizon_ns=1_000 * MS, ftight_permille=400)
+    p = cfg.policies["urgengo"]
+    a = O.run(cfg.workload(), p, b)
+    q = Policy(**{**p.__dict__, "noise_permille": 0})
+    assert np.array_equal(O.run(cfg.workload(), q, b).records, a.records)
+
+
+def test_cpu_predictor_moving_average():
+    """R26: one chain, CPU segment actually 1 ms but profiled at 5 ms.  Instance 0
+    uses the profiled 5 ms (no measurement yet): L(task start) = 50 - 2 - 5 = 43 ms.  Instance 1
+    (t_arr = 100 ms) uses the mean of the one measurement, 1 ms: L = 150 - 2 - 1 - 100 = 47 ms.
+    Without the predictor both instances use 5 ms (43 ms)."""
+    ch = Chain(100 * MS, 50 * MS, 0, [Task(1 * MS, 5 * MS, [Kernel(2 * MS, 2 * MS, 1000)])])
+    w = Workload(chains=[ch], num_prio=6, launch_ns=0, launch_akb_ns=0, sync_lo_ns=0, sync_hi_ns=0, jitter_ns=0)
+    b = Batch(horizon_ns=150 * MS)
+    on = O.run(w, Policy(kind=URGENGO, flags=0, sync_mode=SYNC_ASYNC, cpu_ma_window=8), b, trace_cap=1000)
+    off = O.run(w, Policy(kind=URGENGO, flags=0, sync_mode=SYNC_ASYNC), b, trace_cap=1000)
+    assert (0, 43 * MS) in _evals(on, 0) and (100 * MS, 47 * MS) in _evals(on, 0)
+    assert (100 * MS, 43 * MS) in _evals(off, 0)
+
+
+@pytest.mark.parametrize("W", [1, 3, 8])
+def test_cpu_predictor_replayed_from_trace(W):
+    """R26 recomputed independently from the trace: measured CPU durations are the gaps between
+    a task start and the chain's next evaluation (its launch attempt, lambda aside); the estimate
+    of instance i is the floor mean of the last min(W, h) measurements of earlier instances."""
+    from workloads.quantiles import inst_z_table
+    ch = Chain(20 * MS, 40 * MS, 0, [Task(3 * MS, 3 * MS, [Kernel(1 * MS, 1 * MS, 500)])], cpu_sigma_ppm=300_000)
+    w = Workload(chains=[ch], num_prio=6, launch_ns=0, launch_akb_ns=0, sync_lo_ns=0, sync_hi_ns=0, jitter_ns=0,
+                 inst_quantiles_q16=inst_z_table())
+    r = O.run(w, Policy(kind=URGENGO, flags=0, sync_mode=SYNC_ASYNC, cpu_ma_window=W),
+              Batch(seed=5, horizon_ns=400 * MS), trace_cap=10000)
+    ev = _evals(r, 0)
+    starts = [int(t) for t, k, c, i, a, b in r.trace if k == O.TRACE_CODES["TASK_START"]]
+    hist = []
+    for i, ts in enumerate(starts):
+        pred = 3 * MS if not hist else sum(hist[-W:]) // len(hist[-W:])
+        t_arr = i * 20 * MS
+        assert (ts, t_arr + 40 * MS - 1 * MS - pred - ts) in ev, i
+        nxt = min(t for t, a in ev if t > ts)          # the launch attempt ends the CPU segment
+        hist.append(nxt - ts)

@@ -112,6 +112,8 @@ class Policy:
     lax_threshold_ns: int = 20 * MS    # L_th = 1/TH_urgent; configs override
     sleep_ns: int = 1 * MS             # delay-loop sleep
     util_exempt_permille: int = 100    # U < 0.1 never delayed
+    noise_permille: int = 0            # urgency-estimation noise, uniform per task instance (R25)
+    cpu_ma_window: int = 0             # CPU-segment moving-average window W (R26), 0 = profiled
 
 
 @dataclass
