@@ -101,6 +101,11 @@ typedef struct {
     int64_t lax_threshold_ns;      /* L_th = 1/TH_urgent; < 0 disables urgency */
     int64_t sleep_ns;              /* delay-loop sleep (1 ms), > 0 */
     uint32_t util_exempt_permille; /* kernels below this are never delayed (100) */
+    uint32_t noise_permille;       /* urgency-estimation noise eps <= 1000, uniform per task instance
+                                      (R25); 0 = exact estimates */
+    uint32_t cpu_ma_window;        /* CPU-segment moving-average window W <= 64 (R26);
+                                      0 = profiled estimates; needs max_tasks*(W+2)*4 B of shared
+                                      memory per warp lane (URG_ERANGE if it does not fit) */
 } urg_policy;
 
 typedef struct {

@@ -36,6 +36,7 @@ struct urg_workload {
     int device = 0;
     int num_sms = 148;
     bool has_kern_q = false;          // per-kernel factor table present (selects the kernel instantiation)
+    uint32_t max_tasks = 0;           // most tasks of any chain (CPU predictor state size, R26)
 };
 
 static thread_local std::string g_err;
@@ -158,6 +159,7 @@ extern "C" urg_status urg_create_workload(const urg_workload_desc *d, urg_worklo
             local += t.num_kernels;
         }
         r.num_kernels = local;
+        if (ch.num_tasks > w->max_tasks) w->max_tasks = ch.num_tasks;
         tb += ch.num_tasks; kb += local;
         w->period.push_back(ch.period_ns);
         w->deadline.push_back(ch.deadline_ns);
@@ -206,6 +208,8 @@ static urg_status validate_call(const urg_workload *w, const urg_policy *p, cons
     if (p->sync_mode > URG_SYNC_OVERLAP) return fail(URG_EINVAL, "policy.sync_mode must be 0..3");
     if (p->delta_eval_ns <= 0) return fail(URG_EINVAL, "policy.delta_eval_ns must be > 0");
     if (p->sleep_ns <= 0) return fail(URG_EINVAL, "policy.sleep_ns must be > 0");
+    if (p->noise_permille > 1000) return fail(URG_EINVAL, "policy.noise_permille must be <= 1000");
+    if (p->cpu_ma_window > 64) return fail(URG_EINVAL, "policy.cpu_ma_window must be <= 64");
     if (b->fa_num == 0 || b->fa_den == 0) return fail(URG_EINVAL, "batch.fa_num and batch.fa_den must be > 0");
     if (b->fd_num == 0 || b->fd_den == 0) return fail(URG_EINVAL, "batch.fd_num and batch.fd_den must be > 0");
     if (b->ftight_permille > 1000) return fail(URG_EINVAL, "batch.ftight_permille must be <= 1000");
@@ -233,6 +237,7 @@ static void fill_params(const urg_workload *w, const urg_policy *p, const urg_ba
     P.jitter_ns = w->jitter_ns; P.rt_bin_ns = w->rt_bin_ns;
     P.kind = p->kind; P.flags = p->flags; P.sync_mode = p->sync_mode; P.util_exempt = p->util_exempt_permille;
     P.delta_eval_ns = p->delta_eval_ns; P.lax_threshold_ns = p->lax_threshold_ns; P.sleep_ns = p->sleep_ns;
+    P.noise_pm = p->noise_permille; P.ma_w = p->cpu_ma_window;
     P.seed = b->seed; P.scenario_begin = b->scenario_begin; P.scenario_count = b->scenario_count;
     P.horizon_ns = b->horizon_ns;
     P.fa_num = b->fa_num; P.fa_den = b->fa_den; P.fd_num = b->fd_num; P.fd_den = b->fd_den;
@@ -244,8 +249,8 @@ static void fill_params(const urg_workload *w, const urg_policy *p, const urg_ba
 // (the batch is latency-bound: fewer warps per scheduler, same per-scenario time).
 // Many scenarios: the largest CTA the kernel allows, as many CTAs per SM as
 // registers and shared memory (the staged template is per CTA) let reside.
-static urg_status geometry(const urg_workload *w, const void *fn, uint64_t count, uint32_t smem_fixed, int &warps,
-                           int &ctas, uint32_t &smem)
+static urg_status geometry(const urg_workload *w, const void *fn, uint64_t count, uint32_t smem_fixed,
+                           uint32_t per_lane, int &warps, int &ctas, uint32_t &smem)
 {
     cudaFuncAttributes fa;
     CUDA_TRY(cudaFuncGetAttributes(&fa, fn), "cudaFuncGetAttributes");
@@ -256,7 +261,7 @@ static urg_status geometry(const urg_workload *w, const void *fn, uint64_t count
     if (const char *ew = getenv("URG_WARPS_PER_CTA")) warps = atoi(ew);
     if (warps < 1) warps = 1;
     if (warps > max_w) warps = max_w;
-    smem = smem_fixed + (uint32_t)warps * 32u * URG_SNAP_BYTES_PER_LANE;
+    smem = smem_fixed + (uint32_t)warps * 32u * per_lane;
     CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
              "cudaFuncSetAttribute(smem)");
     int per_sm = 0;
@@ -269,6 +274,32 @@ static urg_status geometry(const urg_workload *w, const void *fn, uint64_t count
     return URG_OK;
 }
 
+// Parameters, kernel instantiation and geometry of one simulation launch.  Shared memory:
+// the template blob, its mbarrier, then per lane the Phase B snapshot (16 B) and, with the
+// CPU predictor (R26), max_tasks x (W + 2) words of predictor state.
+static urg_status prepare_launch(const urg_workload *w, const urg_policy *p, const urg_batch *b, bool wide, bool cal,
+                                 UrgSimParams &P, urg_sim_fn &fn, int &warps, int &ctas)
+{
+    fill_params(w, p, b, P);
+    fn = (urg_sim_fn)urg_sim_kernel_for(p->kind, p->kind == URG_URGENGO ? p->flags : 0, w->has_kern_q, wide && !cal,
+                                        cal);
+    if (!fn) return fail(URG_EINTERNAL, "no kernel instantiation for kind %u flags %u", p->kind, p->flags);
+    P.blob_bytes = (uint32_t)w->blob.size();
+    P.mbar_offset = align16(P.blob_bytes);
+    P.snap_offset = align16(P.mbar_offset + 16);
+    uint32_t per_lane = URG_SNAP_BYTES_PER_LANE;
+    if (p->kind == URG_URGENGO && P.ma_w) {
+        P.ma_max_tasks = w->max_tasks;
+        P.ma_slot = w->max_tasks * (P.ma_w + 2);
+        per_lane += P.ma_slot * 4u;
+    }
+    urg_status st = geometry(w, (const void *)fn, b->scenario_count, P.snap_offset, per_lane, warps, ctas,
+                             P.smem_bytes);
+    if (st != URG_OK) return st;
+    P.ma_offset = P.snap_offset + (uint32_t)warps * 32u * URG_SNAP_BYTES_PER_LANE;
+    return URG_OK;
+}
+
 extern "C" urg_status urg_simulate_batch(const urg_workload *w, const urg_policy *p, const urg_batch *b,
                                          const urg_outputs *o, void *cuda_stream)
 {
@@ -278,19 +309,14 @@ extern "C" urg_status urg_simulate_batch(const urg_workload *w, const urg_policy
     if (!o || !o->agg) return fail(URG_EINVAL, "outputs.agg must not be NULL");
     if (b->scenario_count == 0) return URG_OK;
     cudaStream_t s = (cudaStream_t)cuda_stream;
-    UrgSimParams P;
-    fill_params(w, p, b, P);
     // throughput build once the batch needs more than 16 warps per SM (bench: paper11's 1000
     // scenarios use the latency build, configs[2]-[4]'s 1e5-1e8 the throughput build)
     bool wide = b->scenario_count > (uint64_t)w->num_sms * 16u;
     if (const char *ev = getenv("URG_WIDE")) wide = atoi(ev) != 0;
-    const urg_sim_fn fn = (urg_sim_fn)urg_sim_kernel_for(p->kind, p->kind == URG_URGENGO ? p->flags : 0,
-                                                         w->has_kern_q, wide, false);
-    P.blob_bytes = (uint32_t)w->blob.size();
-    P.mbar_offset = align16(P.blob_bytes);
-    P.snap_offset = align16(P.mbar_offset + 16);
+    UrgSimParams P;
+    urg_sim_fn fn;
     int warps, ctas;
-    st = geometry(w, (const void *)fn, b->scenario_count, P.snap_offset, warps, ctas, P.smem_bytes);
+    st = prepare_launch(w, p, b, wide, false, P, fn, warps, ctas);
     if (st != URG_OK) return st;
     CUDA_TRY(cudaMemsetAsync(w->d_work, 0, 8, s), "cudaMemsetAsync(work counter)");
     fn<<<ctas, warps * 32, P.smem_bytes, s>>>(w->d_blob, P, o->records, (unsigned long long *)o->agg, w->d_work,
@@ -326,17 +352,13 @@ extern "C" urg_status urg_calibrate(const urg_workload *w, const urg_policy *p, 
     urg_policy pc = *p;
     pc.lax_threshold_ns = -1;                                   // nothing is truly urgent while sampling
     UrgSimParams P;
-    fill_params(w, &pc, b, P);
+    urg_sim_fn fn;
+    int warps, ctas;
+    st = prepare_launch(w, &pc, b, false, true, P, fn, warps, ctas);
+    if (st != URG_OK) return st;
     P.cal_end = cal_end(b, window_ns);
     P.cal_cap = cal_cap(b, window_ns);
     P.cal_buf = scratch;
-    const urg_sim_fn fn = (urg_sim_fn)urg_sim_kernel_for(URG_URGENGO, pc.flags, w->has_kern_q, false, true);
-    P.blob_bytes = (uint32_t)w->blob.size();
-    P.mbar_offset = align16(P.blob_bytes);
-    P.snap_offset = align16(P.mbar_offset + 16);
-    int warps, ctas;
-    st = geometry(w, (const void *)fn, b->scenario_count, P.snap_offset, warps, ctas, P.smem_bytes);
-    if (st != URG_OK) return st;
     long long *ws = (long long *)(scratch + b->scenario_count + b->scenario_count * P.cal_cap);
     CUDA_TRY(cudaMemsetAsync(ws, 0, 260 * 8, s), "cudaMemsetAsync(select workspace)");
     CUDA_TRY(cudaMemsetAsync(w->d_work, 0, 8, s), "cudaMemsetAsync(work counter)");

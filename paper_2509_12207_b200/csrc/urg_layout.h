@@ -12,7 +12,7 @@
 #define URG_COLL_BINS 33             // aggregate: kernel-collision histogram bins (R24)
 #define URG_SNAP_BYTES_PER_LANE 16u  // Phase B snapshot in shared memory: laxity (8 B) + level (4 B, padded)
 
-enum { URG_TAG_ARR = 1, URG_TAG_TIGHT = 2, URG_TAG_INST = 3, URG_TAG_KERN = 4, URG_TAG_SYNC = 5 };
+enum { URG_TAG_ARR = 1, URG_TAG_TIGHT = 2, URG_TAG_INST = 3, URG_TAG_KERN = 4, URG_TAG_SYNC = 5, URG_TAG_NOISE = 6 };
 
 struct __align__(16) UrgChainRec {     // 64 B
     int64_t period_ns, deadline_ns, offset_ns;
@@ -51,6 +51,8 @@ struct UrgSimParams {
     uint32_t fa_num, fa_den, fd_num, fd_den, ftight_permille, tight_explicit, tight_mask;
     // staging
     uint32_t blob_bytes, snap_offset, mbar_offset, smem_bytes;
+    // estimation noise (R25) and CPU moving-average predictor (R26)
+    uint32_t noise_pm, ma_w, ma_max_tasks, ma_slot, ma_offset;
     // TH_urgent calibration build only: sampling end, sample rows ([count] counts, then
     // [count][cal_cap] laxities)
     int64_t cal_end;

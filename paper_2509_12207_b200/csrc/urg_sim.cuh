@@ -171,6 +171,13 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
     constexpr bool f_bind = urg && (FLAGS & F_BIND), f_delay = urg && (FLAGS & F_DELAY),
                    f_early = urg && (FLAGS & F_EARLY);
     constexpr bool coll = urg && (FLAGS & F_COLL);   // collision metric (R24): not in the schedule
+    const bool noise = urg && P.noise_pm > 0;          // R25 (runtime: off in the benchmarked policies)
+    const bool ma = urg && P.ma_w > 0;                 // R26
+    // R26 predictor state of this lane's chain in shared memory: [max_tasks][W] ring of
+    // measured CPU durations, [max_tasks] counts, [max_tasks] this instance's estimates
+    uint32_t *ma_ring = (uint32_t *)(sm + P.ma_offset) + (size_t)threadIdx.x * P.ma_slot;
+    uint32_t *ma_cnt = ma_ring + P.ma_max_tasks * P.ma_w;
+    uint32_t *ma_pred = ma_cnt + P.ma_max_tasks;
     const int64_t busy_launch = P.launch_ns + (urg ? P.launch_akb_ns : 0);
     const uint32_t stride = P.agg_stride;
     const bool valid = (uint32_t)lane < C;
@@ -228,6 +235,8 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         }
 
         // ---- per-lane dynamic state ----
+        if (ma)
+            for (uint32_t j = 0; j < P.ma_max_tasks; ++j) ma_cnt[j] = 0;
         int pc = PC_DONE;
         int64_t cpu_next = INF64;
         uint32_t inst = 0;
@@ -236,6 +245,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         uint32_t task = 0, launched = 0, done = 0, level = 0;
         uint32_t task_first = 0, task_end = 0;
         int64_t rem_g = 0, rem_c = 0;          // sum of estimates of kernels / CPU segments not yet passed
+        int32_t nz = 0;                        // R25: estimation noise of the current task instance, per-mille
         int64_t acc = 0;
         uint32_t batch_start = 0, sync_target = 0, sync_ord = 0;
         int64_t sync_cost = 0;
@@ -259,6 +269,13 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             const int64_t z = T.inst_q[w >> 20];
             int64_t F = 65536 + (z * (int64_t)sigma) / 1000000;
             return (uint32_t)(F < 6554 ? 6554 : F);
+        };
+        // Eq. 2 laxity (R9), with the remaining estimated work scaled by the task
+        // instance's noise (R25; floor division, identity when noise is off)
+        auto laxity = [&](int64_t t) -> int64_t {
+            int64_t rem = rem_g + rem_c;
+            if (noise) rem = rem * (1000 + nz) / 1000;
+            return t_arr + Dp - rem - t;
         };
 
         if (valid) {
@@ -322,13 +339,31 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     Fc = inst_factor(rng_word(P.seed, s, URG_TAG_INST, c, inst, 1), cr.cpu_sigma_ppm);
                     task = 0; launched = 0; done = 0; sync_ord = 0;
                     rem_g = cr.gpu_est_total; rem_c = cr.cpu_est_total;
+                    if (ma) {   // R26: this instance's ~E^cpu_j, floor mean of the last min(W, h_j) measurements
+                        rem_c = 0;
+                        for (uint32_t j = 0; j < cr.num_tasks; ++j) {
+                            const uint32_t h = ma_cnt[j];
+                            uint32_t pred = T.task[cr.task_base + j].cpu_estimate_ns;
+                            if (h) {
+                                const uint32_t k = h < P.ma_w ? h : P.ma_w;
+                                uint64_t sum = 0;
+                                for (uint32_t q = 0; q < k; ++q) sum += ma_ring[j * P.ma_w + (h - 1 - q) % P.ma_w];
+                                pred = (uint32_t)(sum / k);
+                            }
+                            ma_pred[j] = pred;
+                            rem_c += pred;
+                        }
+                    }
                     task_first = 0; task_end = T.task[cr.task_base].num_kernels;
                     pc = PC_TASK_START;
                 }
                 if (pc == PC_TASK_START) {   // new CPU segment: evaluate, early exit
                     bool exited = false;
                     if (urg) {
-                        const int64_t lax = t_arr + Dp - rem_g - rem_c - t;   // Eq. 2 (R9)
+                        if (noise)
+                            nz = (int32_t)(rng_word(P.seed, s, URG_TAG_NOISE, c, inst, task) %
+                                           (2u * P.noise_pm + 1u)) - (int32_t)P.noise_pm;
+                        const int64_t lax = laxity(t);   // Eq. 2 (R9)
                         L_last = lax;
                         if (f_early && lax < 0) {
                             akb = 0;
@@ -341,6 +376,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     }
                     if (!exited) {
                         const int64_t e = (int64_t)(((uint64_t)T.task[cr.task_base + task].cpu_nominal_ns * Fc) >> 16);
+                        if (ma) { ma_ring[task * P.ma_w + ma_cnt[task] % P.ma_w] = (uint32_t)e; ++ma_cnt[task]; }
                         pc = PC_CPU_DONE;
                         cpu_next = t + e;
                         if (e > 0) break;
@@ -376,7 +412,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                         if (k && !CAL) atomicAdd(&agg[(uint64_t)C * stride + (k + 1 > 32 ? 32 : k + 1)], 1ull);
                     }
                     const bool last = launched == task_end;
-                    if (last) rem_c -= T.task[cr.task_base + task].cpu_estimate_ns;
+                    if (last) rem_c -= ma ? ma_pred[task] : T.task[cr.task_base + task].cpu_estimate_ns;
                     if (n == task_first) { acc = 0; batch_start = task_first; }
                     int32_t target = -1;
                     if (P.sync_mode == S_ASYNC) {
@@ -418,7 +454,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                 }
                 if (pc == PC_CPU_DONE || pc == PC_ATTEMPT) {   // launch attempt for kernel n = launched (R14-R16)
                     int64_t lax = 0;
-                    if (urg) { lax = t_arr + Dp - rem_g - rem_c - t; L_last = lax; }
+                    if (urg) { lax = laxity(t); L_last = lax; }
                     const bool own_urgent = lax >= 0 && lax <= P.lax_threshold_ns;
                     if (f_delay && !own_urgent && (urgent_m & ~(1u << lane)) &&
                         T.kern[cr.kern_base + launched].util_permille >= P.util_exempt) {

@@ -51,7 +51,8 @@ class WorkloadDesc(ct.Structure):
 class PolicyS(ct.Structure):
     _fields_ = [("kind", ct.c_uint32), ("flags", ct.c_uint32), ("sync_mode", ct.c_uint32),
                 ("delta_eval_ns", ct.c_int64), ("lax_threshold_ns", ct.c_int64), ("sleep_ns", ct.c_int64),
-                ("util_exempt_permille", ct.c_uint32)]
+                ("util_exempt_permille", ct.c_uint32), ("noise_permille", ct.c_uint32),
+                ("cpu_ma_window", ct.c_uint32)]
 
 
 class BatchS(ct.Structure):
@@ -120,7 +121,7 @@ def _check(status: int):
 
 def policy_struct(p: Policy) -> PolicyS:
     return PolicyS(p.kind, p.flags, p.sync_mode, p.delta_eval_ns, p.lax_threshold_ns, p.sleep_ns,
-                   p.util_exempt_permille)
+                   p.util_exempt_permille, p.noise_permille, p.cpu_ma_window)
 
 
 def batch_struct(b: Batch) -> BatchS:

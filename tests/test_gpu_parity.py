@@ -332,3 +332,35 @@ def test_calibration_pooled_random(seed):
     orows = O.calibration_samples(w, p, b, win)
     assert [r.tolist() for r in rows] == [r.tolist() for r in orows]
     assert (lth, n) == O.calibrate(w, p, b, win)
+
+
+@pytest.mark.parametrize("eps,W", [(300, 0), (0, 8), (500, 3), (1000, 1)])
+def test_noise_and_predictor_paper11(eps, W):
+    """R25 estimation noise and R26 CPU moving average on configs[1], both builds."""
+    cfg = get_config("paper11")
+    p = Policy(**{**cfg.policies["urgengo"].__dict__, "noise_permille": eps, "cpu_ma_window": W})
+    b = Batch(seed=cfg.batch.seed, scenario_begin=40, scenario_count=10, horizon_ns=2_000 * MS, ftight_permille=400)
+    both(cfg.workload(), p, b, f"paper11 eps={eps} W={W}")
+
+
+def test_noise_and_predictor_wide(wide_build):
+    cfg = get_config("paper11")
+    p = Policy(**{**cfg.policies["urgengo"].__dict__, "noise_permille": 300, "cpu_ma_window": 8})
+    both(cfg.workload(), p, Batch(seed=cfg.batch.seed, scenario_count=9, horizon_ns=2_000 * MS, ftight_permille=400),
+         "wide noise+ma")
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_noise_and_predictor_random(seed):
+    rng = random.Random(9000 + seed)
+    w = random_workload(rng, C=rng.choice([1, 3, 6, 13]))
+    if rng.random() < 0.5:
+        from workloads.quantiles import inst_z_table
+        w.inst_quantiles_q16 = inst_z_table()
+        for ch in w.chains:
+            ch.cpu_sigma_ppm = rng.randint(0, 400_000)
+    p = random_policy(rng)
+    p.kind = URGENGO
+    p.noise_permille = rng.choice([0, 1, 250, 1000])
+    p.cpu_ma_window = rng.choice([0, 1, 2, 8, 64])
+    both(w, p, Batch(seed=seed, scenario_count=rng.randint(1, 20), horizon_ns=300 * MS), f"noise/ma seed {seed}")
