@@ -232,3 +232,12 @@ def nearest_rank_lth(laxities, pct: int = 95) -> int:
     f.restype = ct.c_int64
     f.argtypes = [ct.c_void_p, ct.c_int64, ct.c_int64]
     return int(f(a.ctypes.data, len(a), pct))
+
+
+def classical_rank(kind: int, tarr, D, R, G, Pp, self_idx: int, t: int) -> int:
+    """Rank of item self_idx (chain id = index) under a classical policy (R27)."""
+    f = lib().orc_classical_rank
+    f.restype = ct.c_uint32
+    f.argtypes = [ct.c_uint32] + [ct.c_void_p] * 5 + [ct.c_uint32, ct.c_uint32, ct.c_int64]
+    arrs = [np.ascontiguousarray(x, np.int64) for x in (tarr, D, R, G, Pp)]
+    return int(f(kind, *[a.ctypes.data for a in arrs], len(arrs[0]), self_idx, t))

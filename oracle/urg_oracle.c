@@ -63,7 +63,7 @@ typedef struct {
     uint32_t fa_num, fa_den, fd_num, fd_den, ftight_permille, tight_explicit, tight_mask;
 } orc_input;
 
-enum { ORC_FIFO = 0, ORC_STATIC = 1, ORC_URGENGO = 2 };
+enum { ORC_FIFO = 0, ORC_STATIC = 1, ORC_URGENGO = 2, ORC_EDF = 3, ORC_SJF = 4, ORC_HRRN = 5, ORC_LCUF = 6 };
 enum { ORC_BIND = 1, ORC_DELAY = 2, ORC_EARLY_EXIT = 4, ORC_COLLISIONS = 8 };
 enum { ORC_ASYNC = 0, ORC_EACH = 1, ORC_BATCHED = 2, ORC_OVERLAP = 3 };
 enum { TAG_ARR = 1, TAG_TIGHT = 2, TAG_INST = 3, TAG_KERN = 4, TAG_SYNC = 5, TAG_NOISE = 6 };
@@ -267,6 +267,8 @@ typedef struct {
     uint32_t *snap_n;
     uint32_t *snap_level;           /* stream level of each chain's current task, same snapshot */
     uint8_t *snap_busy;             /* the chain's stream holds a kernel (waiting or running) */
+    int64_t *snap_tarr;             /* arrival time of the chain's current instance, same snapshot */
+    int64_t *snap_R;                /* its remaining estimated work (kernels + CPU segments, Eq. 2 sums) */
     int64_t *akb_L_view;            /* scratch */
     int64_t *trace; int64_t trace_cap; int64_t trace_len;
     int64_t *agg;
@@ -361,6 +363,52 @@ static int64_t evaluate(orc_sim *S, uint32_t c, int64_t t)
 }
 
 static int urgengo(const orc_sim *S) { return S->in->kind == ORC_URGENGO; }
+/* classical policies of the paper's policy study (R27) */
+static int classical(const orc_sim *S) { return S->in->kind >= ORC_EDF; }
+
+/* Remaining estimated work of chain c's current instance: the two sums of Eq. 2. */
+static int64_t remaining_work(const orc_sim *S, uint32_t c)
+{
+    const orc_lane *L = &S->lane[c];
+    int64_t r = 0;
+    for (uint32_t k = L->launched; k < L->N; ++k) r += S->in->k_est[L->kbase + k];
+    for (uint32_t j = L->cpu_idx; j < L->M; ++j) r += L->cpu_pred[j];
+    return r;
+}
+
+/* "a ranks before b" under the classical policy (R27), ties by smaller chain id:
+ * EDF absolute deadline t_arr + D' ascending; SJF remaining work R ascending; HRRN response
+ * ratio (t - t_arr + R) / R descending (R = 0: infinite); LCUF chain utilisation
+ * sum(~E^gpu) / P' ascending.  Ratios compare by exact 128-bit cross-multiplication. */
+typedef struct { uint32_t chain; int64_t tarr, D, R, G, Pp; } orc_cl_item;
+
+static int orc_cl_before(const orc_sim *S, const orc_cl_item *a, const orc_cl_item *b, int64_t t)
+{
+    switch (S->in->kind) {
+    case ORC_EDF:
+        if (a->tarr + a->D != b->tarr + b->D) return a->tarr + a->D < b->tarr + b->D;
+        break;
+    case ORC_SJF:
+        if (a->R != b->R) return a->R < b->R;
+        break;
+    case ORC_HRRN: {
+        if (a->R == 0 || b->R == 0) {
+            if (a->R == 0 && b->R != 0) return 1;
+            if (b->R == 0 && a->R != 0) return 0;
+            break;
+        }
+        __int128 x = (__int128)(t - a->tarr + a->R) * b->R, y = (__int128)(t - b->tarr + b->R) * a->R;
+        if (x != y) return x > y;
+        break;
+    }
+    case ORC_LCUF: {
+        __int128 x = (__int128)a->G * b->Pp, y = (__int128)b->G * a->Pp;
+        if (x != y) return x < y;
+        break;
+    }
+    }
+    return a->chain < b->chain;
+}
 static int flag(const orc_sim *S, uint32_t f) { return urgengo(S) && (S->in->flags & f); }
 
 /* Delayed launching (R14): delay kernel K iff its
@@ -380,11 +428,54 @@ static int should_delay(const orc_sim *S, uint32_t c, uint32_t util, int64_t own
 }
 
 /* Task-level stream binding with reservation (R15). */
-static uint32_t bind_level(orc_sim *S, uint32_t c, int64_t own_L)
+/* Rank (1-based) of item `self` among n items under classical policy `kind` at time t
+ * (test export of orc_cl_before: the pure ordering of DESIGN.md R27). */
+uint32_t orc_classical_rank(uint32_t kind, const int64_t *tarr, const int64_t *D, const int64_t *R, const int64_t *G,
+                            const int64_t *Pp, uint32_t n, uint32_t self, int64_t t)
+{
+    orc_input in;
+    memset(&in, 0, sizeof in);
+    in.kind = kind;
+    orc_sim S;
+    memset(&S, 0, sizeof S);
+    S.in = &in;
+    orc_cl_item it[64];
+    for (uint32_t i = 0; i < n && i < 64; ++i) {
+        it[i].chain = i; it[i].tarr = tarr[i]; it[i].D = D[i]; it[i].R = R[i]; it[i].G = G[i]; it[i].Pp = Pp[i];
+    }
+    uint32_t r = 1;
+    for (uint32_t i = 0; i < n; ++i)
+        if (i != self && orc_cl_before(&S, &it[i], &it[self], t)) ++r;
+    return r;
+}
+
+static uint32_t bind_level(orc_sim *S, uint32_t c, int64_t own_L, int64_t t)
 {
     const orc_input *in = S->in;
     if (in->kind == ORC_FIFO) return in->num_prio - 1;
     if (in->kind == ORC_STATIC) return S->lane[c].static_level;
+    if (classical(S)) {
+        /* rank among the chain itself and every other chain with active kernels (read view),
+         * normalised like UrgenGo's non-urgent ranks (R15) */
+        orc_cl_item it[64];
+        uint32_t n = 0;
+        for (uint32_t o = 0; o < S->C; ++o) {
+            if (o != c && S->snap_n[o] == 0) continue;
+            orc_cl_item *x = &it[n++];
+            const orc_lane *L = &S->lane[o];
+            x->chain = o; x->D = L->Dp; x->Pp = L->Pp;
+            x->G = 0;
+            for (uint32_t k = 0; k < L->N; ++k) x->G += in->k_est[L->kbase + k];
+            if (o == c) { x->tarr = L->t_arr; x->R = remaining_work(S, c); }   /* own, current */
+            else { x->tarr = S->snap_tarr[o]; x->R = S->snap_R[o]; }
+        }
+        uint32_t r = 1;
+        const orc_cl_item *self = 0;
+        for (uint32_t i = 0; i < n; ++i) if (it[i].chain == c) self = &it[i];
+        for (uint32_t i = 0; i < n; ++i)
+            if (it[i].chain != c && orc_cl_before(S, &it[i], self, t)) ++r;
+        return orc_normalise_level(r, n, in->num_prio);
+    }
     if (!(in->flags & ORC_BIND)) return in->num_prio - 1;
     if (orc_is_urgent(own_L, in->lax_threshold_ns)) return 0;
     int64_t keys[64]; uint32_t chains[64], ranks[64], n = 0;
@@ -542,7 +633,7 @@ static void lane_step(orc_sim *S, uint32_t c, int64_t t)
                 return;
             }
             if (n == task_first_kernel(S, c)) {          /* first kernel of the task: bind */
-                L->level = bind_level(S, c, lax);
+                L->level = bind_level(S, c, lax, t);
                 tr(S, t, TR_BIND, c, L->inst, L->level, n);
             }
             int64_t busy = in->launch_ns + (urgengo(S) ? in->launch_akb_ns : 0);
@@ -558,7 +649,7 @@ static void lane_step(orc_sim *S, uint32_t c, int64_t t)
             if (L->q_head == L->q_tail) { L->head_running = 0; L->head_ready = t; }
             L->q[L->q_tail].K = n; L->q[L->q_tail].t_enq = t; L->q_tail++;
             L->launched++; L->launches++; S->launches++;
-            if (urgengo(S)) {                            /* updateAKB: a new active kernel */
+            if (urgengo(S) || classical(S)) {            /* updateAKB: a new active kernel */
                 orc_akb_entry *a = &L->akb[L->akb_n++];
                 a->K = n; a->U = in->k_util[L->kbase + n]; a->S = L->level; a->C = c;
                 a->T = L->T_last; a->L = L->L_last;
@@ -711,6 +802,8 @@ static int sim_scenario(const orc_input *in, uint64_t s, uint32_t *rec, int64_t 
     S.snap_n = calloc(S.C, sizeof(uint32_t));
     S.snap_level = calloc(S.C, sizeof(uint32_t));
     S.snap_busy = calloc(S.C, sizeof(uint8_t));
+    S.snap_tarr = calloc(S.C, sizeof(int64_t));
+    S.snap_R = calloc(S.C, sizeof(int64_t));
     uint32_t kb = 0, tb = 0;
     for (uint32_t c = 0; c < S.C; ++c) {
         orc_lane *L = &S.lane[c];
@@ -784,6 +877,7 @@ static int sim_scenario(const orc_input *in, uint64_t s, uint32_t *rec, int64_t 
         for (uint32_t c = 0; c < S.C; ++c) {
             S.snap_L[c] = S.lane[c].L_last; S.snap_n[c] = S.lane[c].akb_n;
             S.snap_level[c] = S.lane[c].level; S.snap_busy[c] = S.lane[c].q_head < S.lane[c].q_tail;
+            S.snap_tarr[c] = S.lane[c].t_arr; S.snap_R[c] = remaining_work(&S, c);
         }
         for (uint32_t c = 0; c < S.C; ++c)                               /* Phase B */
             if (S.lane[c].cpu_next == t) lane_step(&S, c, t);
@@ -811,7 +905,8 @@ static int sim_scenario(const orc_input *in, uint64_t s, uint32_t *rec, int64_t 
     agg[(int64_t)S.C * stride + COLL_BINS + 1] += S.steps;
     if (trace_len) *trace_len = S.trace_len;
     if (cal_n) *cal_n = S.cal_n;
-    free(S.lane); free(S.snap_L); free(S.snap_n); free(S.snap_level); free(S.snap_busy);
+    free(S.lane); free(S.snap_L); free(S.snap_n); free(S.snap_level); free(S.snap_busy); free(S.snap_tarr);
+    free(S.snap_R);
     return rc;
 }
 

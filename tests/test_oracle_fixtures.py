@@ -283,3 +283,17 @@ def test_cpu_predictor_replayed_from_trace(W):
         assert (ts, t_arr + 40 * MS - 1 * MS - pred - ts) in ev, i
         nxt = min(t for t, a in ev if t > ts)          # the launch attempt ends the CPU segment
         hist.append(nxt - ts)
+
+
+@pytest.mark.parametrize("kind", [3, 4, 5, 6])
+def test_w1_classical_policies(kind):
+    """W1 with NUM_PRI = 3 under EDF / SJF / HRRN / LCUF (R27).  Hand-derived: A binds
+    alone at 1 ms (level 1); at 1.5 ms B ranks 2nd of {A, B} under every policy -- A's deadline
+    8 < 100 ms (EDF), its remaining work 0 < 6.5 ms (SJF), infinite response ratio (HRRN) and
+    utilisation 4/1000 < 5/1000 (LCUF) -- so B takes level 2; at 3 ms A1 (level 1) beats B0
+    (level 2): A1 3-5 ms, B0 5-10 ms, the STATIC timeline."""
+    w = w1()
+    w.num_prio = 3
+    r = O.run(w, Policy(kind=kind, flags=0, sync_mode=SYNC_ASYNC), Batch(horizon_ns=1 * MS))
+    assert [_sum_rt(r.records[0][c]) for c in range(2)] == [5 * MS, 10 * MS]
+    assert r.launches == 3

@@ -228,3 +228,52 @@ def test_nearest_rank_brute_force():
         assert _ul(got) == _ul(pos[k - 1])
         # at most 5 % of the samples are strictly more urgent than the threshold sample
         assert sum(1 for x in pos if _ul(x) > _ul(got)) * 100 <= 5 * len(pos)
+
+
+# ---- classical policies (R27) ----
+def _brute_rank(kind, tarr, D, R, G, Pp, self_idx, t):
+    from fractions import Fraction
+    INF = float("inf")
+
+    def key(i):
+        if kind == 3:
+            return (tarr[i] + D[i], i)
+        if kind == 4:
+            return (R[i], i)
+        if kind == 5:   # response ratio descending; R = 0 -> infinite ratio
+            ratio = INF if R[i] == 0 else Fraction(t - tarr[i] + R[i], R[i])
+            return (-ratio, i)
+        return (Fraction(G[i], Pp[i]), i)
+    order = sorted(range(len(tarr)), key=key)
+    return order.index(self_idx) + 1
+
+
+def test_classical_rank_spec_examples():
+    MSs = 1_000_000
+    # EDF: deadlines at t+50 ms and t+80 ms -> the former first
+    assert O.classical_rank(3, [0, 0], [50 * MSs, 80 * MSs], [1, 1], [1, 1], [1, 1], 0, 0) == 1
+    assert O.classical_rank(3, [0, 0], [50 * MSs, 80 * MSs], [1, 1], [1, 1], [1, 1], 1, 0) == 2
+    # SJF: equal remaining work -> smaller chain id first
+    assert O.classical_rank(4, [0, 0], [1, 1], [7, 7], [1, 1], [1, 1], 0, 0) == 1
+    assert O.classical_rank(4, [0, 0], [1, 1], [7, 7], [1, 1], [1, 1], 1, 0) == 2
+    # HRRN: a just-arrived instance has ratio 1.0: it ranks after one that waited
+    assert O.classical_rank(5, [0, 5], [1, 1], [10, 10], [1, 1], [1, 1], 1, 5) == 2
+    # LCUF: utilisation 4/150 < 5/150
+    assert O.classical_rank(6, [0, 0], [1, 1], [1, 1], [4, 5], [150, 150], 0, 0) == 1
+
+
+@pytest.mark.parametrize("kind", [3, 4, 5, 6])
+def test_classical_rank_brute_force(kind):
+    rng = np.random.default_rng(kind)
+    for _ in range(2000):
+        n = int(rng.integers(1, 7))
+        t = int(rng.integers(0, 10**9))
+        tarr = [int(t - rng.integers(0, 10**8)) for _ in range(n)]
+        D = [int(rng.choice([60, 120, 200])) * 10**6 for _ in range(n)]
+        R = [int(rng.choice([0, rng.integers(1, 5 * 10**7)])) for _ in range(n)]
+        G = [int(rng.integers(1, 5 * 10**7)) for _ in range(n)]
+        Pp = [int(rng.choice([150, 200, 500, 5000])) * 10**6 for _ in range(n)]
+        if rng.random() < 0.3 and n > 1:   # exact ties
+            tarr[1], D[1], R[1], G[1], Pp[1] = tarr[0], D[0], R[0], G[0], Pp[0]
+        s = int(rng.integers(0, n))
+        assert O.classical_rank(kind, tarr, D, R, G, Pp, s, t) == _brute_rank(kind, tarr, D, R, G, Pp, s, t)

@@ -381,3 +381,88 @@ def test_collision_histogram_replayed_from_trace(seed):
     plain = O.run(w, Policy(kind=p.kind, flags=p.flags & 7, sync_mode=p.sync_mode, delta_eval_ns=p.delta_eval_ns,
                             lax_threshold_ns=p.lax_threshold_ns, sleep_ns=p.sleep_ns), b)
     assert np.array_equal(plain.records, r.records)   # a metric: the schedule is unchanged
+
+
+def _norm_level(r, n_r, num_prio):
+    if num_prio <= 2:
+        return num_prio - 1
+    if n_r <= 1:
+        return 1 + (num_prio - 2) // 2
+    return 1 + ((r - 1) * (num_prio - 2)) // (n_r - 1)
+
+
+def _replay_classical_binds(w, kind, trace):
+    """Recompute every BIND level of a classical policy (R27) from the trace: the rank
+    of the binding chain among itself and the chains with active kernels at the round snapshot,
+    keyed by the chains' arrival, remaining estimated work and utilisation."""
+    from tests.test_oracle_pins import _brute_rank
+    C = w.num_chains
+    est = [[k.estimate_ns for t in ch.tasks for k in t.kernels] for ch in w.chains]
+    cpu = [[t.cpu_estimate_ns for t in ch.tasks] for ch in w.chains]
+    ends = [np.cumsum([len(t.kernels) for t in ch.tasks]).tolist() for ch in w.chains]
+    G = [sum(e) for e in est]
+    launched, cpu_idx, akb, tarr = [0] * C, [0] * C, [0] * C, [0] * C
+    snap, checked = None, 0
+
+    def R(c):
+        return sum(est[c][launched[c]:]) + sum(cpu[c][cpu_idx[c]:])
+
+    for t, kind_, c, i, a, bb in trace:
+        k, c, a, bb, t = int(kind_), int(c), int(a), int(bb), int(t)
+        if k == K["STEP"]:
+            snap = None
+            continue
+        if k == K["RETIRE"]:
+            continue
+        if snap is None:
+            snap = [(akb[o] > 0, tarr[o], R(o)) for o in range(C)]
+        if k == K["INST_START"]:
+            launched[c], cpu_idx[c], akb[c], tarr[c] = 0, 0, 0, a
+        elif k == K["ENQUEUE"]:
+            launched[c] = a + 1
+            akb[c] += 1
+            if launched[c] in ends[c]:
+                cpu_idx[c] = ends[c].index(launched[c]) + 1
+        elif k == K["SYNC_RET"]:
+            akb[c] = launched[c] - a
+        elif k == K["BIND"]:
+            members = [o for o in range(C) if o == c or snap[o][0]]
+            ta = [tarr[o] if o == c else snap[o][1] for o in members]
+            RR = [R(c) if o == c else snap[o][2] for o in members]
+            D = [w._Dp[o] for o in members]
+            Pp = [w._Pp[o] for o in members]
+            GG = [G[o] for o in members]
+            # ties break by chain id: members are in chain order, so list index order = id order
+            r = _brute_rank(kind, ta, D, RR, GG, Pp, members.index(c), t)
+            assert a == _norm_level(r, len(members), w.num_prio), (t, c, a, r, len(members))
+            checked += 1
+    return checked
+
+
+@pytest.mark.parametrize("kind", [3, 4, 5, 6])
+@pytest.mark.parametrize("seed", range(4))
+def test_classical_binding_replayed_from_trace(kind, seed):
+    rng = random.Random(300 + 10 * kind + seed)
+    w = random_workload(rng, C=rng.randint(2, 6))
+    w.num_prio = rng.choice([3, 4, 6])
+    w.jitter_ns = 0
+    p = random_policy(rng)
+    p.kind = kind
+    b = Batch(seed=seed, scenario_count=1, horizon_ns=300 * MS)
+    r = O.run(w, p, b, trace_cap=500_000)
+    assert len(r.trace) < 500_000
+    w._Dp = [ch.deadline_ns for ch in w.chains]       # f_d = 1, no tight set
+    w._Pp = [ch.period_ns for ch in w.chains]         # f_a = 1
+    assert _replay_classical_binds(w, kind, r.trace) > 0
+
+
+@pytest.mark.parametrize("kind", [3, 4, 5, 6])
+def test_classical_single_chain_is_fifo(kind):
+    """With one chain nothing contends, so every policy gives FIFO's records."""
+    rng = random.Random(kind)
+    w = random_workload(rng, C=1)
+    b = Batch(seed=1, scenario_count=3, horizon_ns=300 * MS)
+    base = Policy(kind=FIFO, flags=0, sync_mode=SYNC_OVERLAP)
+    a = O.run(w, base, b)
+    c = O.run(w, Policy(kind=kind, flags=0, sync_mode=SYNC_OVERLAP), b)
+    assert np.array_equal(a.records, c.records)

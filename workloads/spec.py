@@ -24,6 +24,7 @@ import numpy as np
 
 # ---- policy / mode identifiers (values of the C-ABI enums in include/urg.h) ----
 FIFO, STATIC, URGENGO = 0, 1, 2
+EDF, SJF, HRRN, LCUF = 3, 4, 5, 6   # classical policies of the policy study (R27)
 F_BIND, F_DELAY, F_EARLY_EXIT = 1, 2, 4
 F_COLLISIONS = 8           # count kernel collisions of urgent kernels (metric only; R24)
 F_ALL = F_BIND | F_DELAY | F_EARLY_EXIT
