@@ -84,8 +84,9 @@ typedef struct urg_workload urg_workload; /* opaque; immutable after create; own
 urg_status urg_create_workload(const urg_workload_desc *d, urg_workload **out);
 void urg_destroy_workload(urg_workload *w);
 
-/* Policies (§4.4; baselines P:614-615). */
-enum { URG_FIFO = 0, URG_STATIC = 1, URG_URGENGO = 2 };
+/* Policies (§4.4; baselines P:614-615; classical policies of the policy study
+ * EDF, SJF, HRRN, lowest chain utilisation first, R27). */
+enum { URG_FIFO = 0, URG_STATIC = 1, URG_URGENGO = 2, URG_EDF = 3, URG_SJF = 4, URG_HRRN = 5, URG_LCUF = 6 };
 /* UrgenGo mechanisms: stream binding, delayed launching, early exit;
  * URG_F_COLLISIONS counts kernel collisions of urgent kernels (R24) into the
  * aggregate's collision histogram -- a metric only, the schedule is unchanged. */

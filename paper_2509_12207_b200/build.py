@@ -23,8 +23,8 @@ STATS_OUT = os.path.join(HERE, "liburg_stats.so")   # profiling variant (-DURG_S
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CFLAGS = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
-ROWS = 34                                            # URG_SIM_ROWS in urg_sim.cuh
-PARTS = [(0, 3), (3, 6), (6, 9), (9, 12), (12, 15), (15, 18), (18, 26), (26, 34)]   # urg_sim_part0..7
+ROWS = 38                                            # URG_SIM_ROWS in urg_sim.cuh
+PARTS = [(0, 3), (3, 6), (6, 9), (9, 12), (12, 15), (15, 18), (18, 26), (26, 34), (34, 38)]   # urg_sim_part0..8
 
 
 def needs_build(out: str = OUT) -> bool:

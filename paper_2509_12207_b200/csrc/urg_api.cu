@@ -203,7 +203,7 @@ extern "C" uint64_t urg_template_bytes(const urg_workload *w)
 static urg_status validate_call(const urg_workload *w, const urg_policy *p, const urg_batch *b)
 {
     if (!w || !p || !b) return fail(URG_EINVAL, "workload, policy and batch must not be NULL");
-    if (p->kind > URG_URGENGO) return fail(URG_EINVAL, "policy.kind must be 0..2");
+    if (p->kind > URG_LCUF) return fail(URG_EINVAL, "policy.kind must be 0..6");
     if (p->flags > 15) return fail(URG_EINVAL, "policy.flags has unknown bits");
     if (p->sync_mode > URG_SYNC_OVERLAP) return fail(URG_EINVAL, "policy.sync_mode must be 0..3");
     if (p->delta_eval_ns <= 0) return fail(URG_EINVAL, "policy.delta_eval_ns must be > 0");
@@ -288,7 +288,7 @@ static urg_status prepare_launch(const urg_workload *w, const urg_policy *p, con
     P.mbar_offset = align16(P.blob_bytes);
     P.snap_offset = align16(P.mbar_offset + 16);
     uint32_t per_lane = URG_SNAP_BYTES_PER_LANE;
-    if (p->kind == URG_URGENGO && P.ma_w) {
+    if (p->kind >= URG_URGENGO && P.ma_w) {   // UrgenGo and the R27 policies estimate remaining work
         P.ma_max_tasks = w->max_tasks;
         P.ma_slot = w->max_tasks * (P.ma_w + 2);
         per_lane += P.ma_slot * 4u;

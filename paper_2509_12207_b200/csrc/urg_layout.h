@@ -10,7 +10,7 @@
 #define URG_QTABLE 4096              // quantile-table entries (12-bit index)
 #define URG_MAX_BLOB_BYTES (160u * 1024u)
 #define URG_COLL_BINS 33             // aggregate: kernel-collision histogram bins (R24)
-#define URG_SNAP_BYTES_PER_LANE 16u  // Phase B snapshot in shared memory: laxity (8 B) + level (4 B, padded)
+#define URG_SNAP_BYTES_PER_LANE 32u  // Phase B snapshot: laxity, two policy keys (8 B each), level (4 B, padded)
 
 enum { URG_TAG_ARR = 1, URG_TAG_TIGHT = 2, URG_TAG_INST = 3, URG_TAG_KERN = 4, URG_TAG_SYNC = 5, URG_TAG_NOISE = 6 };
 

@@ -18,7 +18,7 @@
 #define FULL 0xFFFFFFFFu
 #define INF64 0x7FFFFFFFFFFFFFFFLL
 
-enum { K_FIFO = 0, K_STATIC = 1, K_URGENGO = 2 };
+enum { K_FIFO = 0, K_STATIC = 1, K_URGENGO = 2, K_EDF = 3, K_SJF = 4, K_HRRN = 5, K_LCUF = 6 };
 enum { F_BIND = 1, F_DELAY = 2, F_EARLY = 4, F_COLL = 8 };
 enum { S_ASYNC = 0, S_EACH = 1, S_BATCHED = 2, S_OVERLAP = 3 };
 // lane program counter; the per-launch states come first so one range test skips the
@@ -165,14 +165,18 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
     __syncthreads();
 
     // per-warp Phase B snapshot (R21): last laxity of each lane, then its stream level
-    int64_t *snapL = (int64_t *)(sm + P.snap_offset) + warp * 64;
-    uint32_t *snapLev = (uint32_t *)(snapL + 32);
+    // per-warp Phase B snapshot (R21), 1 KB: last laxity, two policy keys, stream level
+    int64_t *snapL = (int64_t *)(sm + P.snap_offset) + warp * 128;
+    int64_t *snapA = snapL + 32, *snapB = snapL + 64;
+    uint32_t *snapLev = (uint32_t *)(snapL + 96);
     constexpr bool urg = KIND == K_URGENGO;
+    constexpr bool cls = KIND >= K_EDF;        // classical policies (R27): AKB-tracking, no urgency
+    constexpr bool akb_on = urg || cls;
     constexpr bool f_bind = urg && (FLAGS & F_BIND), f_delay = urg && (FLAGS & F_DELAY),
                    f_early = urg && (FLAGS & F_EARLY);
     constexpr bool coll = urg && (FLAGS & F_COLL);   // collision metric (R24): not in the schedule
     const bool noise = urg && P.noise_pm > 0;          // R25 (runtime: off in the benchmarked policies)
-    const bool ma = urg && P.ma_w > 0;                 // R26
+    const bool ma = akb_on && P.ma_w > 0;              // R26 (every policy that estimates remaining work)
     // R26 predictor state of this lane's chain in shared memory: [max_tasks][W] ring of
     // measured CPU durations, [max_tasks] counts, [max_tasks] this instance's estimates
     uint32_t *ma_ring = (uint32_t *)(sm + P.ma_offset) + (size_t)threadIdx.x * P.ma_slot;
@@ -277,6 +281,31 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             if (noise) rem = rem * (1000 + nz) / 1000;
             return t_arr + Dp - rem - t;
         };
+        // R27 policy keys of this chain: EDF (t_arr + D', -), SJF (-, R), HRRN (t_arr, R),
+        // LCUF (P', sum of kernel estimates); R = the remaining estimated work of Eq. 2
+        auto cls_key_a = [&]() -> int64_t {
+            return KIND == K_EDF ? t_arr + Dp : KIND == K_HRRN ? t_arr : KIND == K_LCUF ? Pp : 0;
+        };
+        auto cls_key_b = [&]() -> int64_t { return KIND == K_LCUF ? cr.gpu_est_total : rem_g + rem_c; };
+        // "chain o ranks before chain s" (ties by smaller chain id; exact 128-bit ratios)
+        auto cls_before = [&](int64_t oA, int64_t oB, int o, int64_t sA, int64_t sB, int sl, int64_t t) -> bool {
+            if (KIND == K_EDF || KIND == K_SJF) {
+                const int64_t ko = KIND == K_EDF ? oA : oB, ks = KIND == K_EDF ? sA : sB;
+                if (ko != ks) return ko < ks;
+            } else if (KIND == K_HRRN) {
+                if (oB == 0 || sB == 0) {
+                    if (oB == 0 && sB != 0) return true;
+                    if (sB == 0 && oB != 0) return false;
+                } else {
+                    const __int128 x = (__int128)(t - oA + oB) * sB, y = (__int128)(t - sA + sB) * oB;
+                    if (x != y) return x > y;
+                }
+            } else if (KIND == K_LCUF) {
+                const __int128 x = (__int128)oB * sA, y = (__int128)sB * oA;
+                if (x != y) return x < y;
+            }
+            return o < sl;
+        };
 
         if (valid) {
             t_arr = arrival(0);
@@ -315,7 +344,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                 if ((uint32_t)(pc - PC_SYNC_RET) <= (uint32_t)(PC_TASK_START - PC_SYNC_RET)) {
                 bool next_inst = false;
                 if (pc == PC_SYNC_RET) {   // sync returned: covered kernels leave the AKB
-                    if (urg) akb = launched - sync_target;
+                    if (akb_on) akb = launched - sync_target;
                     if (launched < task_end) pc = PC_ATTEMPT;
                     else if (++task < cr.num_tasks) {
                         task_first = task_end;
@@ -399,7 +428,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     if (launched == done) { head_ready = t; head_u = kr.util_permille; newhead = true; }   // stream was empty
                     ++launched; ++n_launch;
                     rem_g -= est;
-                    if (urg) ++akb;
+                    if (akb_on) ++akb;
                     if (coll && L_last >= 0 && L_last <= P.lax_threshold_ns) {
                         // R24: less urgent chains with a busy stream at the same or a higher priority
                         const int64_t own = urgency_key(L_last);
@@ -464,6 +493,20 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     }
                     if (launched == task_first) {   // task-level stream binding
                         if (KIND == K_STATIC) level = static_level;
+                        else if (cls) {   // R27: rank among itself and the AKB-active chains
+                            uint32_t mm = active_m & ~(1u << lane);
+                            const uint32_t n_r = 1 + __popc(mm);
+                            const int64_t ownA = cls_key_a(), ownB = cls_key_b();
+                            uint32_t r = 1;
+                            while (mm) {
+                                const int o = __ffs(mm) - 1;
+                                mm &= mm - 1;
+                                r += cls_before(snapA[o], snapB[o], o, ownA, ownB, lane, t) ? 1u : 0u;
+                            }
+                            level = P.num_prio <= 2 ? P.num_prio - 1
+                                    : n_r <= 1      ? 1 + (P.num_prio - 2) / 2
+                                                    : 1 + (uint32_t)(((uint64_t)(r - 1) * (P.num_prio - 2)) / (n_r - 1));
+                        }
                         else if (!f_bind) level = P.num_prio - 1;
                         else if (own_urgent) level = 0;
                         else {
@@ -506,6 +549,11 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             } else if (f_bind && __any_sync(FULL, may_bind)) {
                 active_m = __ballot_sync(FULL, akb > 0);
                 snapL[lane] = L_last;
+                __syncwarp();
+            } else if (cls && __any_sync(FULL, may_bind)) {
+                active_m = __ballot_sync(FULL, akb > 0);
+                snapA[lane] = cls_key_a();
+                snapB[lane] = cls_key_b();
                 __syncwarp();
             }
         };
@@ -577,7 +625,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                 ++st_multi;
 #endif
                 uint32_t urgent_m = 0, active_m = 0, busy_m = 0;
-                if (urg) snapshot(due && can_bind(), urgent_m, active_m, busy_m);
+                if (urg || cls) snapshot(due && can_bind(), urgent_m, active_m, busy_m);
                 bool nh = false;
                 if (due) nh = phase_b(t, urgent_m, active_m, busy_m);
                 dirty |= __any_sync(FULL, nh);
@@ -657,13 +705,14 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
 // instantiation rows: 0 FIFO, 1 STATIC, 2 + f UrgenGo with flags f (0..15);
 // columns: (per-kernel factor table) + 2 * (throughput build)
 // ---------------------------------------------------------------------------
-// rows 18 + f: the calibration build of UrgenGo with flags f (latency build only)
-#define URG_SIM_ROWS 34
+// rows 18 + f: the calibration build of UrgenGo with flags f (latency build only);
+// rows 34..37: the classical policies EDF, SJF, HRRN, LCUF (R27)
+#define URG_SIM_ROWS 38
 template <int ROW>
 struct UrgRow {
-    static constexpr int K = ROW == 0 ? K_FIFO : ROW == 1 ? K_STATIC : K_URGENGO;
-    static constexpr int F = ROW < 2 ? 0 : ROW < 18 ? ROW - 2 : ROW - 18;
-    static constexpr bool C = ROW >= 18;
+    static constexpr int K = ROW == 0 ? K_FIFO : ROW == 1 ? K_STATIC : ROW < 34 ? K_URGENGO : K_EDF + (ROW - 34);
+    static constexpr int F = ROW < 2 || ROW >= 34 ? 0 : ROW < 18 ? ROW - 2 : ROW - 18;
+    static constexpr bool C = ROW >= 18 && ROW < 34;
     static const void *get(uint32_t col)
     {
         if constexpr (C) {   // the calibration build exists in the latency variant only

@@ -21,7 +21,7 @@ const void *URG_PART_FN(uint32_t row, uint32_t col)
         URG_ROW(9) URG_ROW(10) URG_ROW(11) URG_ROW(12) URG_ROW(13) URG_ROW(14) URG_ROW(15) URG_ROW(16)
         URG_ROW(17) URG_ROW(18) URG_ROW(19) URG_ROW(20) URG_ROW(21) URG_ROW(22) URG_ROW(23) URG_ROW(24)
         URG_ROW(25) URG_ROW(26) URG_ROW(27) URG_ROW(28) URG_ROW(29) URG_ROW(30) URG_ROW(31) URG_ROW(32)
-        URG_ROW(33)
+        URG_ROW(33) URG_ROW(34) URG_ROW(35) URG_ROW(36) URG_ROW(37)
     default: return nullptr;
     }
 }

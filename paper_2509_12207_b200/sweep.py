@@ -10,6 +10,8 @@ run through the same C-ABI call (``urg_simulate_batch``) on the current CUDA dev
 * ``ablation``     -- binding only / delay only / both (PAPER.md:774-776, fig:4_ablation);
 * ``collisions``   -- kernel collisions of urgent kernels with and without delayed
                       launching, by number of colliding tasks (PAPER.md:790-791, fig:8_collision);
+* ``policies``     -- UrgenGo against the vanilla (FIFO), PAAM-like static, EDF, SJF, HRRN
+                      and lowest-chain-utilisation-first policies (PAPER.md:782-784, fig:6_policy);
 * ``utilisation``  -- UrgenGo vs FIFO vs static priorities over an arrival-rate sweep
                       (BASELINE.json configs[2]; PAPER.md:679-683 fig:0_overall analogue).
 
@@ -23,7 +25,8 @@ from typing import Dict, List, Optional
 
 import numpy as np
 
-from workloads.spec import (COLL_BINS, F_BIND, F_COLLISIONS, F_DELAY, F_EARLY_EXIT, FIFO, STATIC, SYNC_ASYNC,
+from workloads.spec import (COLL_BINS, EDF, F_BIND, F_COLLISIONS, F_DELAY, F_EARLY_EXIT, FIFO, HRRN, LCUF, SJF,
+                            STATIC, SYNC_ASYNC,
                             SYNC_BATCHED, SYNC_EACH, SYNC_OVERLAP, URGENGO, Batch, Policy, Workload,
                             collision_hist)
 
@@ -79,6 +82,14 @@ def collisions(base: Policy, b: Batch) -> List[Point]:
             Point("UrgenGo", replace(base, flags=f), b)]
 
 
+def policies(base: Policy, b: Batch) -> List[Point]:
+    out = [Point("UrgenGo", base, b), Point("FIFO (vanilla)", Policy(kind=FIFO, flags=0, sync_mode=SYNC_ASYNC), b),
+           Point("static (PAAM-like)", Policy(kind=STATIC, flags=0, sync_mode=SYNC_ASYNC), b)]
+    for n, k in (("EDF", EDF), ("SJF", SJF), ("HRRN", HRRN), ("LCUF", LCUF)):
+        out.append(Point(n, Policy(kind=k, flags=0, sync_mode=base.sync_mode, delta_eval_ns=base.delta_eval_ns), b))
+    return out
+
+
 def utilisation(base: Policy, batches: List[Batch]) -> List[Point]:
     pols = [("UrgenGo", base), ("FIFO", Policy(kind=FIFO, flags=0, sync_mode=SYNC_ASYNC)),
             ("static", Policy(kind=STATIC, flags=0, sync_mode=SYNC_ASYNC))]
@@ -90,7 +101,7 @@ def utilisation(base: Policy, batches: List[Batch]) -> List[Point]:
     return out
 
 
-STUDIES = ("sync_modes", "delta_eval", "num_prio", "ablation", "collisions")
+STUDIES = ("sync_modes", "delta_eval", "num_prio", "ablation", "collisions", "policies")
 
 
 def run(w: Workload, points: List[Point], stream=None) -> List[Result]:

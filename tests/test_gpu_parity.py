@@ -364,3 +364,28 @@ def test_noise_and_predictor_random(seed):
     p.noise_permille = rng.choice([0, 1, 250, 1000])
     p.cpu_ma_window = rng.choice([0, 1, 2, 8, 64])
     both(w, p, Batch(seed=seed, scenario_count=rng.randint(1, 20), horizon_ns=300 * MS), f"noise/ma seed {seed}")
+
+
+@pytest.mark.parametrize("kind", [3, 4, 5, 6])
+def test_classical_policies(kind):
+    """R27 classical policies: W1 (NUM_PRI 3), random workloads, configs[1] in both builds."""
+    w = w1()
+    w.num_prio = 3
+    both(w, Policy(kind=kind, flags=0, sync_mode=SYNC_ASYNC), Batch(horizon_ns=1 * MS), f"w1 kind {kind}")
+    rng = random.Random(11000 + kind)
+    for _ in range(4):
+        wr = random_workload(rng, C=rng.choice([2, 5, 9, 32]))
+        pr = random_policy(rng)
+        pr.kind = kind
+        pr.cpu_ma_window = rng.choice([0, 4])
+        both(wr, pr, Batch(seed=kind, scenario_count=rng.randint(1, 12), horizon_ns=300 * MS), f"rand kind {kind}")
+    cfg = get_config("paper11")
+    b = Batch(seed=cfg.batch.seed, scenario_count=8, horizon_ns=2_000 * MS, ftight_permille=400)
+    both(cfg.workload(), Policy(kind=kind, flags=0, sync_mode=SYNC_OVERLAP), b, f"paper11 kind {kind}")
+
+
+def test_classical_policies_wide(wide_build):
+    cfg = get_config("paper11")
+    b = Batch(seed=cfg.batch.seed, scenario_begin=100, scenario_count=8, horizon_ns=2_000 * MS, ftight_permille=400)
+    for kind in (3, 4, 5, 6):
+        both(cfg.workload(), Policy(kind=kind, flags=0, sync_mode=SYNC_ASYNC), b, f"wide kind {kind}")

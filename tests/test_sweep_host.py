@@ -22,3 +22,10 @@ def test_studies_vary_one_knob():
     assert [bool(p.policy.flags & F_DELAY) for p in co] == [False, True]
     us = SW.utilisation(base, get_config("usweep").sweep)
     assert len(us) == 8 * 3
+
+
+def test_policy_study_kinds():
+    from paper_2509_12207_b200 import sweep as SW
+    cfg = get_config("paper11")
+    kinds = [p.policy.kind for p in SW.policies(cfg.policies["urgengo"], cfg.batch)]
+    assert kinds == [2, 0, 1, 3, 4, 5, 6]

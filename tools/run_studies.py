@@ -30,6 +30,7 @@ studies = {
     "num_prio (PAPER.md:779-780)": SW.num_prio(base, b),
     "ablation (PAPER.md:774-776)": SW.ablation(base, b),
     "collisions (PAPER.md:790-791)": SW.collisions(base, b),
+    "policies (PAPER.md:782-784)": SW.policies(base, b),
 }
 cfg3 = get_config("usweep")
 studies["utilisation sweep (configs[2])"] = SW.utilisation(base, [replace(x, scenario_count=SU) for x in cfg3.sweep])
