@@ -23,7 +23,8 @@ _LIB = os.path.join(_HERE, "liburg_oracle.so")
 
 TRACE_KINDS = {1: "STEP", 2: "INST_START", 3: "TASK_START", 4: "EVAL", 5: "DELAY", 6: "BIND", 7: "ENQUEUE",
                8: "DISPATCH", 9: "RETIRE", 10: "SYNC_CALL", 11: "SYNC_RET", 12: "FREE_CLOSE",
-               13: "INST_DONE", 14: "EARLY_EXIT", 15: "COLLISION"}
+               13: "INST_DONE", 14: "EARLY_EXIT", 15: "COLLISION", 16: "FREE_CALL", 17: "FREE_START",
+               18: "FREE_RET"}
 TRACE_CODES = {v: k for k, v in TRACE_KINDS.items()}
 
 
@@ -41,13 +42,13 @@ class OrcInput(ct.Structure):
         ("num_chains", ct.c_uint32),
         ("ch_period", ct.c_void_p), ("ch_deadline", ct.c_void_p), ("ch_offset", ct.c_void_p),
         ("ch_ntasks", ct.c_void_p), ("ch_cpu_sigma", ct.c_void_p), ("ch_gpu_sigma", ct.c_void_p),
-        ("t_cpu_nom", ct.c_void_p), ("t_cpu_est", ct.c_void_p), ("t_nk", ct.c_void_p),
+        ("t_cpu_nom", ct.c_void_p), ("t_cpu_est", ct.c_void_p), ("t_nk", ct.c_void_p), ("t_flags", ct.c_void_p),
         ("k_nom", ct.c_void_p), ("k_est", ct.c_void_p), ("k_util", ct.c_void_p),
         ("num_prio", ct.c_uint32),
         ("launch_ns", ct.c_int64), ("launch_akb_ns", ct.c_int64), ("sync_lo_ns", ct.c_int64),
         ("sync_hi_ns", ct.c_int64), ("jitter_ns", ct.c_int64),
         ("inst_q16", ct.c_void_p), ("kern_q16", ct.c_void_p),
-        ("rt_bin_ns", ct.c_int64), ("rt_bins", ct.c_uint32),
+        ("rt_bin_ns", ct.c_int64), ("rt_bins", ct.c_uint32), ("free_ns", ct.c_int64),
         ("kind", ct.c_uint32), ("flags", ct.c_uint32), ("sync_mode", ct.c_uint32),
         ("delta_eval_ns", ct.c_int64), ("lax_threshold_ns", ct.c_int64), ("sleep_ns", ct.c_int64),
         ("util_exempt_permille", ct.c_uint32),
@@ -105,11 +106,11 @@ def _make_input(w: Workload, p: Policy, b: Batch):
         num_chains=w.num_chains,
         ch_period=_ptr(f["ch_period"]), ch_deadline=_ptr(f["ch_deadline"]), ch_offset=_ptr(f["ch_offset"]),
         ch_ntasks=_ptr(f["ch_ntasks"]), ch_cpu_sigma=_ptr(f["ch_cpu_sigma"]), ch_gpu_sigma=_ptr(f["ch_gpu_sigma"]),
-        t_cpu_nom=_ptr(f["t_cpu_nom"]), t_cpu_est=_ptr(f["t_cpu_est"]), t_nk=_ptr(f["t_nk"]),
+        t_cpu_nom=_ptr(f["t_cpu_nom"]), t_cpu_est=_ptr(f["t_cpu_est"]), t_nk=_ptr(f["t_nk"]), t_flags=_ptr(f["t_flags"]),
         k_nom=_ptr(f["k_nom"]), k_est=_ptr(f["k_est"]), k_util=_ptr(f["k_util"]),
         num_prio=w.num_prio, launch_ns=w.launch_ns, launch_akb_ns=w.launch_akb_ns,
         sync_lo_ns=w.sync_lo_ns, sync_hi_ns=w.sync_hi_ns, jitter_ns=w.jitter_ns,
-        inst_q16=_ptr(inst), kern_q16=_ptr(kern), rt_bin_ns=w.rt_bin_ns, rt_bins=w.rt_bins,
+        inst_q16=_ptr(inst), kern_q16=_ptr(kern), rt_bin_ns=w.rt_bin_ns, rt_bins=w.rt_bins, free_ns=w.free_ns,
         kind=p.kind, flags=p.flags, sync_mode=p.sync_mode, delta_eval_ns=p.delta_eval_ns,
         lax_threshold_ns=p.lax_threshold_ns, sleep_ns=p.sleep_ns, util_exempt_permille=p.util_exempt_permille,
         noise_permille=p.noise_permille, cpu_ma_window=p.cpu_ma_window,

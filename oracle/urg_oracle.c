@@ -43,6 +43,7 @@ typedef struct {
     const int64_t *ch_period, *ch_deadline, *ch_offset;
     const uint32_t *ch_ntasks, *ch_cpu_sigma, *ch_gpu_sigma;
     const uint32_t *t_cpu_nom, *t_cpu_est, *t_nk;   /* all tasks, chain-major */
+    const uint32_t *t_flags;                        /* bit 0: the task ends with cudaFree (R28) */
     const uint32_t *k_nom, *k_est;                  /* all kernels, chain-major */
     const uint16_t *k_util;
     uint32_t num_prio;
@@ -51,6 +52,7 @@ typedef struct {
     const uint32_t *kern_q16;   /* 4096 factor quantiles or NULL */
     int64_t rt_bin_ns;
     uint32_t rt_bins;
+    int64_t free_ns;            /* cudaFree cost once the device is idle (Table 5) */
     /* policy */
     uint32_t kind, flags, sync_mode;
     int64_t delta_eval_ns, lax_threshold_ns, sleep_ns;
@@ -71,7 +73,7 @@ enum { TAG_ARR = 1, TAG_TIGHT = 2, TAG_INST = 3, TAG_KERN = 4, TAG_SYNC = 5, TAG
 /* trace kinds */
 enum { TR_STEP = 1, TR_INST_START, TR_TASK_START, TR_EVAL, TR_DELAY, TR_BIND, TR_ENQUEUE,
        TR_DISPATCH, TR_RETIRE, TR_SYNC_CALL, TR_SYNC_RET, TR_FREE_CLOSE, TR_INST_DONE,
-       TR_EARLY_EXIT, TR_COLLISION };
+       TR_EARLY_EXIT, TR_COLLISION, TR_FREE_CALL, TR_FREE_START, TR_FREE_RET };
 
 #define REC_WORDS 8
 #define AGG_COUNTERS 5
@@ -215,7 +217,8 @@ typedef struct {            /* one AKB entry */
 
 typedef struct { uint32_t K; int64_t t_enq; } orc_stream_entry;
 
-enum { PC_ARRIVE = 0, PC_CPU_DONE, PC_ATTEMPT, PC_ENQUEUE, PC_SYNC_WAIT, PC_SYNC_RET, PC_DONE };
+enum { PC_ARRIVE = 0, PC_CPU_DONE, PC_ATTEMPT, PC_ENQUEUE, PC_SYNC_WAIT, PC_SYNC_RET, PC_FREE_WAIT, PC_FREE_RET,
+       PC_DONE };
 
 typedef struct {
     /* static per scenario */
@@ -251,6 +254,7 @@ typedef struct {
     uint32_t q_head, q_tail;        /* entries [q_head, q_tail) */
     int head_running;
     int64_t head_ready, head_end;
+    int64_t free_req;               /* time of this chain's pending cudaFree request (R28) */
     /* results */
     uint32_t total, miss, early, unfin, launches, hash;
     uint64_t sum_rt;
@@ -707,6 +711,19 @@ static void lane_step(orc_sim *S, uint32_t c, int64_t t)
             if (urgengo(S)) evaluate(S, c, t);            /* periodic evaluation */
             uint32_t end = task_first_kernel(S, c) + in->t_nk[L->tbase + L->task];
             if (L->launched < end) { L->pc = PC_ATTEMPT; continue; }
+            if (in->t_flags && (in->t_flags[L->tbase + L->task] & 1u)) {
+                /* the task ends with cudaFree: a device-wide barrier request (R28) */
+                L->pc = PC_FREE_WAIT; L->cpu_next = ORC_INF; L->free_req = t;
+                tr(S, t, TR_FREE_CALL, c, L->inst, L->task, 0);
+                return;
+            }
+            goto task_done;
+        }
+        case PC_FREE_RET: {
+            tr(S, t, TR_FREE_RET, c, L->inst, L->task, 0);
+            goto task_done;
+        }
+        task_done: {
             L->task++;
             if (L->task < L->M) goto task_start;
             record_outcome(S, c, t, 0);                  /* instance complete (R18) */
@@ -730,10 +747,38 @@ static int orc_cand_cmp(const void *a, const void *b)
     return x->chain < y->chain ? -1 : (x->chain > y->chain);
 }
 
+/* cudaFree device barriers ("cudaFree calls introduce global
+ * synchronization"; R28): requests queue in (request time,
+ * chain) order; while any is queued or being served the GPU starts no kernel; the queue
+ * head is served once no kernel runs, costing free_ns, after which its chain resumes.
+ * Returns 1 if a barrier is queued or in service (no dispatch at t). */
+static int barrier(orc_sim *S, int64_t t)
+{
+    int queued = 0, serving = 0, running = 0;
+    int32_t head = -1;
+    for (uint32_t c = 0; c < S->C; ++c) {
+        const orc_lane *L = &S->lane[c];
+        if (L->pc == PC_FREE_RET) serving = 1;
+        if (L->pc == PC_FREE_WAIT) {
+            queued = 1;
+            if (head < 0 || L->free_req < S->lane[head].free_req) head = (int32_t)c;   /* ties: smaller id */
+        }
+        if (L->q_head < L->q_tail && L->head_running) running = 1;
+    }
+    if (!queued && !serving) return 0;
+    if (!serving && !running) {                      /* the device is idle: serve the head */
+        orc_lane *L = &S->lane[head];
+        L->pc = PC_FREE_RET; L->cpu_next = t + S->in->free_ns;
+        tr(S, t, TR_FREE_START, head, L->inst, L->cpu_next, 0);
+    }
+    return 1;
+}
+
 static void dispatch(orc_sim *S, int64_t t)
 {
     orc_cand cand[64];
     uint32_t n = 0;
+    if (barrier(S, t)) return;
     for (uint32_t c = 0; c < S->C; ++c) {
         orc_lane *L = &S->lane[c];
         if (L->q_head < L->q_tail && !L->head_running) {

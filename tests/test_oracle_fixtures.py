@@ -10,7 +10,7 @@ import pytest
 
 from oracle import oracle as O
 from workloads import w1, w2, w3
-from workloads.spec import (FIFO, MS, REC_EARLY, REC_LAUNCH, REC_MISS, REC_SUMRT_HI, REC_SUMRT_LO,
+from workloads.spec import (US, FIFO, MS, REC_EARLY, REC_LAUNCH, REC_MISS, REC_SUMRT_HI, REC_SUMRT_LO,
                             REC_TOTAL, SYNC_ASYNC, SYNC_BATCHED, SYNC_EACH, SYNC_OVERLAP, URGENGO,
                             F_EARLY_EXIT, Batch, Chain, Kernel, Policy, Task, Workload)
 
@@ -297,3 +297,25 @@ def test_w1_classical_policies(kind):
     r = O.run(w, Policy(kind=kind, flags=0, sync_mode=SYNC_ASYNC), Batch(horizon_ns=1 * MS))
     assert [_sum_rt(r.records[0][c]) for c in range(2)] == [5 * MS, 10 * MS]
     assert r.launches == 3
+
+
+@pytest.mark.parametrize("case", _gold("w6.json")["cases"], ids=lambda c: c["name"])
+def test_w6_cudafree_barrier(case):
+    """R28 device barrier: hand-worked response times under every policy kind (the barrier
+    does not depend on priorities here)."""
+    from workloads import w6
+    w = w6(case["two_chains"])
+    for kind in (FIFO, URGENGO):
+        r = O.run(w, Policy(kind=kind, flags=0, sync_mode=SYNC_ASYNC, lax_threshold_ns=-1), Batch(horizon_ns=1 * MS))
+        assert [_sum_rt(r.records[0][c]) for c in range(w.num_chains)] == [int(round(x * MS)) for x in case["rt_ms"]]
+
+
+def test_cudafree_serialises_requests():
+    """Two chains each ending with cudaFree at the same time: requests are served one after
+    the other in chain order, each costing free_ns once the device is idle (R28)."""
+    t = Task(1 * MS, 1 * MS, [Kernel(1 * MS, 1 * MS, 400)], frees=True)
+    w = Workload(chains=[Chain(1000 * MS, 100 * MS, 0, [t]), Chain(1000 * MS, 100 * MS, 0, [t])], num_prio=2,
+                 launch_ns=0, launch_akb_ns=0, sync_lo_ns=0, sync_hi_ns=0, jitter_ns=0, free_ns=300 * US)
+    r = O.run(w, Policy(kind=FIFO, flags=0, sync_mode=SYNC_ASYNC), Batch(horizon_ns=1 * MS))
+    # both kernels run 1-2 ms (u 400 + 400); both frees requested at 2 ms: chain 0 served 2-2.3, chain 1 2.3-2.6
+    assert [_sum_rt(r.records[0][c]) for c in range(2)] == [2_300_000, 2_600_000]

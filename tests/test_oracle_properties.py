@@ -466,3 +466,43 @@ def test_classical_single_chain_is_fifo(kind):
     a = O.run(w, base, b)
     c = O.run(w, Policy(kind=kind, flags=0, sync_mode=SYNC_OVERLAP), b)
     assert np.array_equal(a.records, c.records)
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_cudafree_barrier_invariants(seed):
+    """R28 on random workloads with cudaFree tasks: while a request is pending or served no
+    kernel starts; a request is served only when no kernel runs; a served request returns
+    exactly free_ns later; requests are served in (request time, chain) order."""
+    rng = random.Random(4000 + seed)
+    w = random_workload(rng, C=rng.randint(2, 6))
+    for ch in w.chains:
+        for t in ch.tasks:
+            t.frees = rng.random() < 0.4
+    w.free_ns = rng.choice([50 * US, 188 * US, 2 * MS])
+    p = random_policy(rng)
+    r = O.run(w, p, Batch(seed=seed, scenario_count=1, horizon_ns=300 * MS), trace_cap=400_000)
+    pending, serving, running = {}, None, set()
+    served = []
+    for t, k, c, i, a, bb in r.trace:
+        t, k, c, i, a = int(t), int(k), int(c), int(i), int(a)
+        name = O.TRACE_KINDS[k]
+        if name == "FREE_CALL":
+            pending[c] = t
+        elif name == "FREE_START":
+            assert not running, "a cudaFree is served only on an idle device"
+            assert serving is None
+            head = min(pending, key=lambda x: (pending[x], x))
+            assert c == head, "requests are served in (time, chain) order"
+            assert a == t + w.free_ns
+            serving = (c, a)
+            del pending[c]
+            served.append(c)
+        elif name == "FREE_RET":
+            assert serving is not None and serving == (c, t)
+            serving = None
+        elif name == "DISPATCH":
+            assert not pending and serving is None, "no kernel starts during a barrier"
+            running.add((c, i, a))
+        elif name == "RETIRE":
+            running.discard((c, i, a))
+    assert r.records[0][:, 0].sum() > 0

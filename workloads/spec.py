@@ -47,6 +47,7 @@ class Task:
     cpu_nominal_ns: int        # CPU segment actual time (before per-scenario factor)
     cpu_estimate_ns: int       # ~E^cpu_j used by Eq. 2
     kernels: List[Kernel]
+    frees: bool = False        # the task ends with cudaFree: a device-wide barrier (R28)
 
 
 @dataclass
@@ -72,6 +73,7 @@ class Workload:
     kern_quantiles_q16: Optional[np.ndarray] = None   # uint32[4096] per-kernel factor quantiles, Q16.16
     rt_bin_ns: int = 1 * MS
     rt_bins: int = 1024
+    free_ns: int = 188 * US            # cudaFree cost on an idle device (Table 5; R28)
 
     @property
     def num_chains(self) -> int:
@@ -83,13 +85,14 @@ class Workload:
     def flat(self) -> dict:
         """Flatten to SoA numpy arrays (chains, then tasks in chain order, then kernels)."""
         ch_period, ch_deadline, ch_offset, ch_ntasks, ch_csig, ch_gsig = [], [], [], [], [], []
-        t_cpu_nom, t_cpu_est, t_nk = [], [], []
+        t_cpu_nom, t_cpu_est, t_nk, t_flags = [], [], [], []
         k_nom, k_est, k_util, k_flags = [], [], [], []
         for c in self.chains:
             ch_period.append(c.period_ns); ch_deadline.append(c.deadline_ns); ch_offset.append(c.offset_ns)
             ch_ntasks.append(len(c.tasks)); ch_csig.append(c.cpu_sigma_ppm); ch_gsig.append(c.gpu_sigma_ppm)
             for t in c.tasks:
                 t_cpu_nom.append(t.cpu_nominal_ns); t_cpu_est.append(t.cpu_estimate_ns); t_nk.append(len(t.kernels))
+                t_flags.append(1 if t.frees else 0)
                 for k in t.kernels:
                     k_nom.append(k.nominal_ns); k_est.append(k.estimate_ns)
                     k_util.append(k.util_permille); k_flags.append(k.flags)
@@ -98,7 +101,7 @@ class Workload:
             ch_offset=np.asarray(ch_offset, np.int64), ch_ntasks=np.asarray(ch_ntasks, np.uint32),
             ch_cpu_sigma=np.asarray(ch_csig, np.uint32), ch_gpu_sigma=np.asarray(ch_gsig, np.uint32),
             t_cpu_nom=np.asarray(t_cpu_nom, np.uint32), t_cpu_est=np.asarray(t_cpu_est, np.uint32),
-            t_nk=np.asarray(t_nk, np.uint32),
+            t_nk=np.asarray(t_nk, np.uint32), t_flags=np.asarray(t_flags, np.uint32),
             k_nom=np.asarray(k_nom, np.uint32), k_est=np.asarray(k_est, np.uint32),
             k_util=np.asarray(k_util, np.uint16), k_flags=np.asarray(k_flags, np.uint16),
         )

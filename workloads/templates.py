@@ -152,3 +152,11 @@ def w4() -> Workload:
     b2 = Chain(1000 * MS, 100 * MS, 0, [Task(600 * US, 600 * US, [Kernel(4 * MS, 4 * MS, 1000)])])
     return Workload(chains=[a, b, b2], num_prio=2, launch_ns=0, launch_akb_ns=0, sync_lo_ns=0, sync_hi_ns=0,
                     jitter_ns=0)
+
+
+def w6(two_chains: bool = True) -> Workload:
+    """Fixture W6 (tests/golden/w6.json): cudaFree device barriers (R28)."""
+    a = Chain(1000 * MS, 100 * MS, 0, [Task(1 * MS, 1 * MS, [Kernel(2 * MS, 2 * MS, 500)], frees=True)])
+    b = Chain(1000 * MS, 100 * MS, 0, [Task(500 * US, 500 * US, [Kernel(5 * MS, 5 * MS, 500), Kernel(1 * MS, 1 * MS, 500)])])
+    return Workload(chains=[a, b] if two_chains else [a], num_prio=2, launch_ns=0, launch_akb_ns=0, sync_lo_ns=0,
+                    sync_hi_ns=0, jitter_ns=0, free_ns=188 * US)
