@@ -49,7 +49,10 @@ typedef struct {
     uint32_t cpu_estimate_ns;  /* ~E^cpu_j used in Eq. 2 */
     uint32_t num_kernels;
     const urg_kernel_desc *kernels;
+    uint32_t flags;            /* bit 0 (URG_TASK_FREE): the task ends with cudaFree, a device-wide
+                                  barrier (R28); other bits must be 0 */
 } urg_task_desc;
+enum { URG_TASK_FREE = 1 };
 
 /* A periodic task chain with an end-to-end deadline (Table 2). */
 typedef struct {
@@ -75,6 +78,8 @@ typedef struct {
     const uint32_t *kern_quantiles_q16;   /* host, 4096 per-kernel factor quantiles (Q16.16) or NULL */
     int64_t rt_bin_ns;                    /* response-time histogram bin width (> 0) */
     uint32_t rt_bins;                     /* number of bins B (>= 1; last bin is open-ended) */
+    int64_t free_ns;                      /* cudaFree cost on an idle device (Table 5: 188 us);
+                                             must be > 0 when any task ends with cudaFree */
 } urg_workload_desc;
 
 typedef struct urg_workload urg_workload; /* opaque; immutable after create; owns its device copy */

@@ -963,6 +963,11 @@ int orc_run(const orc_input *in, uint32_t *records, int64_t *agg,
 {
     if (!in || in->num_chains == 0 || in->num_chains > 32) return -1;
     if (in->fa_num == 0 || in->fa_den == 0 || in->fd_den == 0 || in->rt_bins == 0 || in->rt_bin_ns <= 0) return -1;
+    if (in->t_flags) {                                /* a served cudaFree takes time (R28) */
+        uint32_t nt = 0;
+        for (uint32_t c = 0; c < in->num_chains; ++c) nt += in->ch_ntasks[c];
+        for (uint32_t j = 0; j < nt; ++j) if ((in->t_flags[j] & 1u) && in->free_ns <= 0) return -1;
+    }
     for (uint32_t c = 0; c < in->num_chains; ++c)     /* arrivals strictly increasing: P' > J (R3) */
         if (in->ch_period[c] * (int64_t)in->fa_den / (int64_t)in->fa_num <= in->jitter_ns) return -2;
     if (trace_len) *trace_len = 0;

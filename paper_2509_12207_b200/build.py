@@ -24,7 +24,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CFLAGS = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
 ROWS = 38                                            # URG_SIM_ROWS in urg_sim.cuh
-PARTS = [(0, 3), (3, 6), (6, 9), (9, 12), (12, 15), (15, 18), (18, 26), (26, 34), (34, 38)]   # urg_sim_part0..8
+PARTS = [(r, r + 2) for r in range(0, 18, 2)] + [(18, 26), (26, 34), (34, 36), (36, 38)]   # urg_sim_part0..12
 
 
 def needs_build(out: str = OUT) -> bool:

@@ -19,7 +19,7 @@
 
 typedef void (*urg_sim_fn)(const uint8_t *blob, const UrgSimParams P, uint32_t *records, unsigned long long *agg,
                            unsigned long long *work, long long *err);
-const void *urg_sim_kernel_for(uint32_t kind, uint32_t flags, bool kern_q, bool wide, bool cal);   // urg_sim.cu
+const void *urg_sim_kernel_for(uint32_t kind, uint32_t flags, bool kern_q, bool wide, bool cal, bool ext);   // urg_sim.cu
 extern "C" __global__ void urg_cal_hist_kernel(const int64_t *buf, uint64_t count, uint64_t cap, long long *ws,
                                                int pass);
 extern "C" __global__ void urg_cal_pick_kernel(long long *ws, int pass, int pct, long long *result);
@@ -37,6 +37,8 @@ struct urg_workload {
     int num_sms = 148;
     bool has_kern_q = false;          // per-kernel factor table present (selects the kernel instantiation)
     uint32_t max_tasks = 0;           // most tasks of any chain (CPU predictor state size, R26)
+    bool has_free = false;            // some task ends with cudaFree (R28)
+    int64_t free_ns = 0;
 };
 
 static thread_local std::string g_err;
@@ -85,8 +87,13 @@ extern "C" urg_status urg_create_workload(const urg_workload_desc *d, urg_worklo
     if (d->jitter_ns < 0 || d->jitter_ns >= 0xFFFFFFFFLL) return fail(URG_EINVAL, "jitter_ns must be in [0, 2^32 - 1)");
     if (d->rt_bin_ns <= 0) return fail(URG_EINVAL, "rt_bin_ns must be > 0");
     if (d->rt_bins < 1 || d->rt_bins > (1u << 20)) return fail(URG_EINVAL, "rt_bins must be in 1..2^20");
+    if (d->free_ns < 0 || d->free_ns >= (1LL << 40)) return fail(URG_EINVAL, "free_ns must be in [0, 2^40)");
 
     uint32_t n_tasks = 0, n_kern = 0;
+    for (uint32_t c = 0; c < d->num_chains && d->chains; ++c)
+        for (uint32_t j = 0; j < d->chains[c].num_tasks && d->chains[c].tasks; ++j)
+            if ((d->chains[c].tasks[j].flags & 1u) && d->free_ns <= 0)
+                return fail(URG_EINVAL, "chains[%u].tasks[%u] ends with cudaFree: free_ns must be > 0", c, j);
     for (uint32_t c = 0; c < d->num_chains; ++c) {
         const urg_chain_desc &ch = d->chains[c];
         if (ch.period_ns <= 0) return fail(URG_EINVAL, "chains[%u].period_ns must be > 0", c);
@@ -99,6 +106,7 @@ extern "C" urg_status urg_create_workload(const urg_workload_desc *d, urg_worklo
         for (uint32_t j = 0; j < ch.num_tasks; ++j) {
             const urg_task_desc &t = ch.tasks[j];
             if (t.num_kernels < 1) return fail(URG_EINVAL, "chains[%u].tasks[%u].num_kernels must be >= 1", c, j);
+            if (t.flags > 1) return fail(URG_EINVAL, "chains[%u].tasks[%u].flags has unknown bits", c, j);
             if (!t.kernels) return fail(URG_EINVAL, "chains[%u].tasks[%u].kernels must not be NULL", c, j);
             for (uint32_t k = 0; k < t.num_kernels; ++k) {
                 const urg_kernel_desc &kd = t.kernels[k];
@@ -137,6 +145,7 @@ extern "C" urg_status urg_create_workload(const urg_workload_desc *d, urg_worklo
     w->sync_lo_ns = d->sync_lo_ns; w->sync_hi_ns = d->sync_hi_ns;
     w->jitter_ns = d->jitter_ns; w->rt_bin_ns = d->rt_bin_ns;
     w->has_kern_q = d->kern_quantiles_q16 != nullptr;
+    w->free_ns = d->free_ns;
     w->blob.assign(off, 0);
     memcpy(w->blob.data(), &h, sizeof h);
     UrgChainRec *chs = (UrgChainRec *)(w->blob.data() + h.off_chains);
@@ -152,7 +161,8 @@ extern "C" urg_status urg_create_workload(const urg_workload_desc *d, urg_worklo
         uint32_t local = 0;
         for (uint32_t j = 0; j < ch.num_tasks; ++j) {
             const urg_task_desc &t = ch.tasks[j];
-            tks[tb + j] = UrgTaskRec{t.cpu_nominal_ns, t.cpu_estimate_ns, t.num_kernels, local};
+            tks[tb + j] = UrgTaskRec{t.cpu_nominal_ns, t.cpu_estimate_ns, t.num_kernels, t.flags};
+            if (t.flags & 1u) w->has_free = true;
             for (uint32_t k = 0; k < t.num_kernels; ++k)
                 krs[kb + local + k] = UrgKernRec{t.kernels[k].nominal_ns, t.kernels[k].estimate_ns,
                                                  t.kernels[k].util_permille, 0};
@@ -238,6 +248,7 @@ static void fill_params(const urg_workload *w, const urg_policy *p, const urg_ba
     P.kind = p->kind; P.flags = p->flags; P.sync_mode = p->sync_mode; P.util_exempt = p->util_exempt_permille;
     P.delta_eval_ns = p->delta_eval_ns; P.lax_threshold_ns = p->lax_threshold_ns; P.sleep_ns = p->sleep_ns;
     P.noise_pm = p->noise_permille; P.ma_w = p->cpu_ma_window;
+    P.has_free = w->has_free ? 1u : 0u; P.free_ns = w->free_ns;
     P.seed = b->seed; P.scenario_begin = b->scenario_begin; P.scenario_count = b->scenario_count;
     P.horizon_ns = b->horizon_ns;
     P.fa_num = b->fa_num; P.fa_den = b->fa_den; P.fd_num = b->fd_num; P.fd_den = b->fd_den;
@@ -281,8 +292,12 @@ static urg_status prepare_launch(const urg_workload *w, const urg_policy *p, con
                                  UrgSimParams &P, urg_sim_fn &fn, int &warps, int &ctas)
 {
     fill_params(w, p, b, P);
+    // the extended-model build only when the batch uses noise, the CPU predictor or cudaFree
+    bool ext = (p->kind == URG_URGENGO && p->noise_permille) || (p->kind >= URG_URGENGO && p->cpu_ma_window) ||
+               w->has_free;
+    if (const char *ee = getenv("URG_EXT")) ext = ext || atoi(ee) != 0;   // test hook: force the extended build
     fn = (urg_sim_fn)urg_sim_kernel_for(p->kind, p->kind == URG_URGENGO ? p->flags : 0, w->has_kern_q, wide && !cal,
-                                        cal);
+                                        cal, ext);
     if (!fn) return fail(URG_EINTERNAL, "no kernel instantiation for kind %u flags %u", p->kind, p->flags);
     P.blob_bytes = (uint32_t)w->blob.size();
     P.mbar_offset = align16(P.blob_bytes);

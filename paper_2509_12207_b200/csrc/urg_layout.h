@@ -24,7 +24,7 @@ struct __align__(16) UrgChainRec {     // 64 B
 };
 
 struct __align__(16) UrgTaskRec {      // 16 B
-    uint32_t cpu_nominal_ns, cpu_estimate_ns, num_kernels, first_kernel;   // first_kernel: chain-local
+    uint32_t cpu_nominal_ns, cpu_estimate_ns, num_kernels, flags;   // flags bit 0: ends with cudaFree (R28)
 };
 
 struct __align__(16) UrgKernRec {      // 16 B: one LDS.128 per access
@@ -53,6 +53,9 @@ struct UrgSimParams {
     uint32_t blob_bytes, snap_offset, mbar_offset, smem_bytes;
     // estimation noise (R25) and CPU moving-average predictor (R26)
     uint32_t noise_pm, ma_w, ma_max_tasks, ma_slot, ma_offset;
+    // cudaFree barriers (R28)
+    uint32_t has_free;
+    int64_t free_ns;
     // TH_urgent calibration build only: sampling end, sample rows ([count] counts, then
     // [count][cal_cap] laxities)
     int64_t cal_end;

@@ -23,7 +23,8 @@ enum { F_BIND = 1, F_DELAY = 2, F_EARLY = 4, F_COLL = 8 };
 enum { S_ASYNC = 0, S_EACH = 1, S_BATCHED = 2, S_OVERLAP = 3 };
 // lane program counter; the per-launch states come first so one range test skips the
 // per-task / per-instance states on the common path
-enum { PC_ENQUEUE = 0, PC_ATTEMPT, PC_CPU_DONE, PC_SYNC_RET, PC_ARRIVE, PC_TASK_START, PC_SYNC_WAIT, PC_DONE };
+enum { PC_ENQUEUE = 0, PC_ATTEMPT, PC_CPU_DONE, PC_SYNC_RET, PC_FREE_RET, PC_ARRIVE, PC_TASK_START, PC_SYNC_WAIT,
+       PC_FREE_WAIT, PC_DONE };
 enum { ERR_TIME = 1, ERR_GUARD = 2 };
 
 // ---------------------------------------------------------------------------
@@ -130,7 +131,11 @@ struct Tmpl {   // shared-memory views of the staged template
 // CAL: the TH_urgent calibration build (Q5): every 1 ms of
 // simulated time before P.cal_end the laxity of the most urgent AKB entry is appended
 // to the scenario's sample row; no records or aggregates are written.
-template <int KIND, int FLAGS, bool KQ, bool WIDE, bool CAL = false>
+//
+// EXT: the extended-model build (estimation noise R25, CPU predictor R26, cudaFree
+// barriers R28 resolved at run time); the core build has none of their branches (the
+// policies of the benchmarks use none of them and run ~9 % faster without).
+template <int KIND, int FLAGS, bool KQ, bool WIDE, bool CAL = false, bool EXT = true>
 __global__ void __launch_bounds__(WIDE ? 1024 : 512, 1)
 urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t *__restrict__ records,
                unsigned long long *__restrict__ agg, unsigned long long *__restrict__ work,
@@ -175,8 +180,9 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
     constexpr bool f_bind = urg && (FLAGS & F_BIND), f_delay = urg && (FLAGS & F_DELAY),
                    f_early = urg && (FLAGS & F_EARLY);
     constexpr bool coll = urg && (FLAGS & F_COLL);   // collision metric (R24): not in the schedule
-    const bool noise = urg && P.noise_pm > 0;          // R25 (runtime: off in the benchmarked policies)
-    const bool ma = akb_on && P.ma_w > 0;              // R26 (every policy that estimates remaining work)
+    const bool noise = EXT && urg && P.noise_pm > 0;       // R25
+    const bool ma = EXT && akb_on && P.ma_w > 0;           // R26 (every policy that estimates remaining work)
+    const bool has_free = EXT && P.has_free != 0;          // R28: some task ends with cudaFree
     // R26 predictor state of this lane's chain in shared memory: [max_tasks][W] ring of
     // measured CPU durations, [max_tasks] counts, [max_tasks] this instance's estimates
     uint32_t *ma_ring = (uint32_t *)(sm + P.ma_offset) + (size_t)threadIdx.x * P.ma_slot;
@@ -250,6 +256,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         uint32_t task_first = 0, task_end = 0;
         int64_t rem_g = 0, rem_c = 0;          // sum of estimates of kernels / CPU segments not yet passed
         int32_t nz = 0;                        // R25: estimation noise of the current task instance, per-mille
+        int64_t free_req = 0;                  // R28: time of this chain's pending cudaFree request
         int64_t acc = 0;
         uint32_t batch_start = 0, sync_target = 0, sync_ord = 0;
         int64_t sync_cost = 0;
@@ -343,10 +350,21 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                 }
                 if ((uint32_t)(pc - PC_SYNC_RET) <= (uint32_t)(PC_TASK_START - PC_SYNC_RET)) {
                 bool next_inst = false;
+                bool task_done = false;
                 if (pc == PC_SYNC_RET) {   // sync returned: covered kernels leave the AKB
                     if (akb_on) akb = launched - sync_target;
                     if (launched < task_end) pc = PC_ATTEMPT;
-                    else if (++task < cr.num_tasks) {
+                    else if (has_free && (T.task[cr.task_base + task].flags & 1u)) {
+                        // R28: the task ends with cudaFree -- request the device barrier and block
+                        pc = PC_FREE_WAIT;
+                        free_req = t;
+                        cpu_next = INF64;
+                        break;
+                    } else task_done = true;
+                }
+                if (pc == PC_FREE_RET) task_done = true;   // R28: the barrier was served
+                if (task_done) {
+                    if (++task < cr.num_tasks) {
                         task_first = task_end;
                         task_end += T.task[cr.task_base + task].num_kernels;
                         pc = PC_TASK_START;
@@ -569,6 +587,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         // per-mille of the running kernels (kept incrementally).
         int64_t t_prev = -1;
         uint32_t used = 0;
+        bool bar_prev = false;                  // R28: a barrier was pending at the previous step
         int64_t cal_next = 0;                   // CAL: next sampling time
         uint32_t cal_n = 0;                     // CAL: samples of this scenario
         for (;;) {
@@ -631,6 +650,25 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                 dirty |= __any_sync(FULL, nh);
             }
 
+
+            // cudaFree barriers (R28): while a request is queued or served nothing starts;
+            // the (request time, chain)-first request is served once no kernel runs
+            if (has_free) {
+                const uint32_t fw = __ballot_sync(FULL, pc == PC_FREE_WAIT);
+                const uint32_t fr = __ballot_sync(FULL, pc == PC_FREE_RET);
+                if (fw | fr) {
+                    bar_prev = true;
+                    if (!fr && !__any_sync(FULL, head_end != INF64)) {
+                        const bool w8 = (fw >> lane) & 1u;
+                        const int64_t rq = w8 ? free_req : INF64;
+                        const int64_t mrq = warp_min_nonneg(rq);
+                        const int head = __ffs(__ballot_sync(FULL, w8 && free_req == mrq)) - 1;
+                        if (lane == head) { pc = PC_FREE_RET; cpu_next = t + P.free_ns; }
+                    }
+                    continue;   // no dispatch during a barrier
+                }
+                if (bar_prev) { bar_prev = false; dirty = true; }   // released: waiting heads may start
+            }
 
             // Phase C: dispatch waiting stream heads by (level, ready, chain) under capacity (R20).
             // Runs only when a kernel retired or a stream got a new head: otherwise every
@@ -713,17 +751,22 @@ struct UrgRow {
     static constexpr int K = ROW == 0 ? K_FIFO : ROW == 1 ? K_STATIC : ROW < 34 ? K_URGENGO : K_EDF + (ROW - 34);
     static constexpr int F = ROW < 2 || ROW >= 34 ? 0 : ROW < 18 ? ROW - 2 : ROW - 18;
     static constexpr bool C = ROW >= 18 && ROW < 34;
+    // col: bit 0 per-kernel factor table, bit 1 throughput build, bit 2 extended model
     static const void *get(uint32_t col)
     {
-        if constexpr (C) {   // the calibration build exists in the latency variant only
-            return (col & 1u) ? (const void *)urg_sim_kernel<K, F, true, false, true>
-                              : (const void *)urg_sim_kernel<K, F, false, false, true>;
+        if constexpr (C) {   // the calibration build: latency variant, extended model
+            return (col & 1u) ? (const void *)urg_sim_kernel<K, F, true, false, true, true>
+                              : (const void *)urg_sim_kernel<K, F, false, false, true, true>;
         } else {
-            switch (col) {
-            case 0: return (const void *)urg_sim_kernel<K, F, false, false>;
-            case 1: return (const void *)urg_sim_kernel<K, F, true, false>;
-            case 2: return (const void *)urg_sim_kernel<K, F, false, true>;
-            default: return (const void *)urg_sim_kernel<K, F, true, true>;
+            switch (col & 7u) {
+            case 0: return (const void *)urg_sim_kernel<K, F, false, false, false, false>;
+            case 1: return (const void *)urg_sim_kernel<K, F, true, false, false, false>;
+            case 2: return (const void *)urg_sim_kernel<K, F, false, true, false, false>;
+            case 3: return (const void *)urg_sim_kernel<K, F, true, true, false, false>;
+            case 4: return (const void *)urg_sim_kernel<K, F, false, false, false, true>;
+            case 5: return (const void *)urg_sim_kernel<K, F, true, false, false, true>;
+            case 6: return (const void *)urg_sim_kernel<K, F, false, true, false, true>;
+            default: return (const void *)urg_sim_kernel<K, F, true, true, false, true>;
             }
         }
     }

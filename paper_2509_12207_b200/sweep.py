@@ -12,6 +12,8 @@ run through the same C-ABI call (``urg_simulate_batch``) on the current CUDA dev
                       launching, by number of colliding tasks (PAPER.md:790-791, fig:8_collision);
 * ``policies``     -- UrgenGo against the vanilla (FIFO), PAAM-like static, EDF, SJF, HRRN
                       and lowest-chain-utilisation-first policies (PAPER.md:782-784, fig:6_policy);
+* ``cudafree``     -- 0..4 tasks ending with cudaFree, a device-wide barrier (PAPER.md:907-911,
+                      fig:15_vector_free; DESIGN.md R28);
 * ``utilisation``  -- UrgenGo vs FIFO vs static priorities over an arrival-rate sweep
                       (BASELINE.json configs[2]; PAPER.md:679-683 fig:0_overall analogue).
 
@@ -40,6 +42,7 @@ class Point:
     policy: Policy
     batch: Batch
     num_prio: Optional[int] = None          # workload override (binding streams)
+    frees: Optional[int] = None             # workload override: the first n tasks end with cudaFree (R28)
 
 
 @dataclass
@@ -90,6 +93,26 @@ def policies(base: Policy, b: Batch) -> List[Point]:
     return out
 
 
+def cudafree(base: Policy, b: Batch, counts=(0, 1, 2, 3, 4)) -> List[Point]:
+    """PAPER.md:907-911 (fig:15_vector_free): 0..4 tasks ending with cudaFree, under UrgenGo,
+    static priorities and plain asynchronous launching."""
+    pols = [("UrgenGo", base), ("static (PAAM-like)", Policy(kind=STATIC, flags=0, sync_mode=SYNC_ASYNC)),
+            ("async (FIFO)", Policy(kind=FIFO, flags=0, sync_mode=SYNC_ASYNC))]
+    return [Point(f"{n} cudaFree tasks, {name}", p, b, frees=n) for n in counts for name, p in pols]
+
+
+def with_frees(w: Workload, n: int) -> Workload:
+    """A copy of w whose first n tasks (chain-major) end with cudaFree."""
+    import copy
+    w2 = copy.deepcopy(w)
+    k = 0
+    for ch in w2.chains:
+        for t in ch.tasks:
+            t.frees = k < n
+            k += 1
+    return w2
+
+
 def utilisation(base: Policy, batches: List[Batch]) -> List[Point]:
     pols = [("UrgenGo", base), ("FIFO", Policy(kind=FIFO, flags=0, sync_mode=SYNC_ASYNC)),
             ("static", Policy(kind=STATIC, flags=0, sync_mode=SYNC_ASYNC))]
@@ -101,20 +124,22 @@ def utilisation(base: Policy, batches: List[Batch]) -> List[Point]:
     return out
 
 
-STUDIES = ("sync_modes", "delta_eval", "num_prio", "ablation", "collisions", "policies")
+STUDIES = ("sync_modes", "delta_eval", "num_prio", "ablation", "collisions", "policies", "cudafree")
 
 
 def run(w: Workload, points: List[Point], stream=None) -> List[Result]:
     """Run every point on the current CUDA device (one urg_simulate_batch per point)."""
     import torch
     out = []
-    cache: Dict[int, DeviceWorkload] = {}
+    cache: Dict[tuple, DeviceWorkload] = {}
     try:
         for pt in points:
             npri = pt.num_prio if pt.num_prio is not None else w.num_prio
-            if npri not in cache:
-                cache[npri] = DeviceWorkload(replace(w, num_prio=npri))
-            dw = cache[npri]
+            key = (npri, pt.frees)
+            if key not in cache:
+                ww = replace(w, num_prio=npri)
+                cache[key] = DeviceWorkload(with_frees(ww, pt.frees) if pt.frees is not None else ww)
+            dw = cache[key]
             agg = torch.zeros(dw.agg_words, dtype=torch.int64, device="cuda")
             s = stream if stream is not None else torch.cuda.current_stream()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

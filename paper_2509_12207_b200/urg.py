@@ -31,7 +31,7 @@ class KernelDesc(ct.Structure):
 
 class TaskDesc(ct.Structure):
     _fields_ = [("cpu_nominal_ns", ct.c_uint32), ("cpu_estimate_ns", ct.c_uint32),
-                ("num_kernels", ct.c_uint32), ("kernels", ct.POINTER(KernelDesc))]
+                ("num_kernels", ct.c_uint32), ("kernels", ct.POINTER(KernelDesc)), ("flags", ct.c_uint32)]
 
 
 class ChainDesc(ct.Structure):
@@ -45,7 +45,7 @@ class WorkloadDesc(ct.Structure):
                 ("launch_ns", ct.c_int64), ("launch_akb_ns", ct.c_int64),
                 ("sync_lo_ns", ct.c_int64), ("sync_hi_ns", ct.c_int64), ("jitter_ns", ct.c_int64),
                 ("inst_quantiles_q16", ct.c_void_p), ("kern_quantiles_q16", ct.c_void_p),
-                ("rt_bin_ns", ct.c_int64), ("rt_bins", ct.c_uint32)]
+                ("rt_bin_ns", ct.c_int64), ("rt_bins", ct.c_uint32), ("free_ns", ct.c_int64)]
 
 
 class PolicyS(ct.Structure):
@@ -148,7 +148,7 @@ class DeviceWorkload:
                 ks = (KernelDesc * len(t.kernels))(*[KernelDesc(k.nominal_ns, k.estimate_ns, k.util_permille, k.flags)
                                                      for k in t.kernels])
                 keep.append(ks)
-                tasks[ti] = TaskDesc(t.cpu_nominal_ns, t.cpu_estimate_ns, len(t.kernels), ks)
+                tasks[ti] = TaskDesc(t.cpu_nominal_ns, t.cpu_estimate_ns, len(t.kernels), ks, 1 if t.frees else 0)
             keep.append(tasks)
             chains[ci] = ChainDesc(ch.period_ns, ch.deadline_ns, ch.offset_ns, len(ch.tasks), tasks,
                                    ch.cpu_sigma_ppm, ch.gpu_sigma_ppm)
@@ -156,7 +156,7 @@ class DeviceWorkload:
         kern = None if w.kern_quantiles_q16 is None else np.ascontiguousarray(w.kern_quantiles_q16, np.uint32)
         self.desc = WorkloadDesc(w.num_chains, chains, w.num_prio, w.launch_ns, w.launch_akb_ns, w.sync_lo_ns,
                                  w.sync_hi_ns, w.jitter_ns, None if inst is None else inst.ctypes.data,
-                                 None if kern is None else kern.ctypes.data, w.rt_bin_ns, w.rt_bins)
+                                 None if kern is None else kern.ctypes.data, w.rt_bin_ns, w.rt_bins, w.free_ns)
         self._keep = (keep, chains, inst, kern)
         h = ct.c_void_p()
         _check(lib().urg_create_workload(ct.byref(self.desc), ct.byref(h)))

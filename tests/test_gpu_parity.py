@@ -389,3 +389,64 @@ def test_classical_policies_wide(wide_build):
     b = Batch(seed=cfg.batch.seed, scenario_begin=100, scenario_count=8, horizon_ns=2_000 * MS, ftight_permille=400)
     for kind in (3, 4, 5, 6):
         both(cfg.workload(), Policy(kind=kind, flags=0, sync_mode=SYNC_ASYNC), b, f"wide kind {kind}")
+
+
+def _with_frees(w, n):
+    """The first n tasks (chain-major) end with cudaFree (the PAPER.md:909 experiment knob)."""
+    k = 0
+    for ch in w.chains:
+        for t in ch.tasks:
+            t.frees = k < n
+            k += 1
+    return w
+
+
+def test_cudafree_fixtures():
+    from workloads import w6
+    for two in (False, True):
+        for kind in (FIFO, STATIC, URGENGO, 3, 5):
+            both(w6(two), Policy(kind=kind, flags=7 if kind == URGENGO else 0, sync_mode=SYNC_ASYNC,
+                                 lax_threshold_ns=-1), Batch(horizon_ns=1 * MS), f"w6 {two} {kind}")
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_cudafree_random(seed):
+    rng = random.Random(12000 + seed)
+    w = random_workload(rng, C=rng.choice([2, 4, 11, 32]))
+    for ch in w.chains:
+        for t in ch.tasks:
+            t.frees = rng.random() < 0.3
+    w.free_ns = rng.choice([1, 50 * US, 188 * US, 2 * MS])
+    p = random_policy(rng)
+    p.kind = rng.choice([FIFO, STATIC, URGENGO, 3, 4, 5, 6])
+    both(w, p, Batch(seed=seed, scenario_count=rng.randint(1, 16), horizon_ns=300 * MS), f"free seed {seed}")
+
+
+@pytest.mark.parametrize("n", [1, 4])
+def test_cudafree_paper11(n, wide_build):
+    cfg = get_config("paper11")
+    w = _with_frees(cfg.workload(), n)
+    b = Batch(seed=cfg.batch.seed, scenario_count=8, horizon_ns=2_000 * MS, ftight_permille=400)
+    for name in ("urgengo", "fifo", "static"):
+        both(w, cfg.policies[name], b, f"paper11 frees={n} {name}")
+
+
+@pytest.fixture
+def ext_build(monkeypatch):
+    """Force the extended-model instantiations (R25/R26/R28 resolved at run time)."""
+    monkeypatch.setenv("URG_EXT", "1")
+    yield
+
+
+def test_extended_build_equals_core(ext_build):
+    """With noise, predictor and cudaFree off, the extended build reproduces the oracle exactly
+    like the core build (W1, toy2, paper11, a classical policy)."""
+    both(w1(), Policy(kind=URGENGO, flags=3, sync_mode=SYNC_ASYNC, lax_threshold_ns=5 * MS), Batch(horizon_ns=1 * MS), "ext w1")
+    for mode in (SYNC_ASYNC, SYNC_OVERLAP):
+        both(toy2(), Policy(kind=URGENGO, flags=7, sync_mode=mode, lax_threshold_ns=10 * MS), get_config("toy2").batch,
+             "ext toy2")
+    cfg = get_config("paper11")
+    b = Batch(seed=cfg.batch.seed, scenario_count=8, horizon_ns=2_000 * MS, ftight_permille=400)
+    for name in ("urgengo", "fifo", "static"):
+        both(cfg.workload(), cfg.policies[name], b, f"ext paper11 {name}")
+    both(cfg.workload(), Policy(kind=5, flags=0, sync_mode=SYNC_OVERLAP), b, "ext paper11 hrrn")

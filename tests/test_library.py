@@ -71,3 +71,11 @@ def test_validation_loci(L):
     assert e.status == -2 and "exceeds 32" in str(e)
     w = Workload(chains=[])
     assert "num_chains" in str(_create(w))
+
+
+def test_cudafree_needs_positive_cost(L):
+    from workloads import w6
+    w = w6(False)
+    w.free_ns = 0
+    e = _create(w)
+    assert e.status == -1 and "free_ns must be > 0" in str(e)

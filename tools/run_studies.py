@@ -31,6 +31,7 @@ studies = {
     "ablation (PAPER.md:774-776)": SW.ablation(base, b),
     "collisions (PAPER.md:790-791)": SW.collisions(base, b),
     "policies (PAPER.md:782-784)": SW.policies(base, b),
+    "cudaFree (PAPER.md:907-911)": SW.cudafree(base, b),
 }
 cfg3 = get_config("usweep")
 studies["utilisation sweep (configs[2])"] = SW.utilisation(base, [replace(x, scenario_count=SU) for x in cfg3.sweep])
