@@ -200,6 +200,11 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
     // static per-chain template data
     UrgChainRec cr = {};
     if (valid) cr = chs[c];
+    // the chain record: a register copy in the latency build; re-read from shared memory in
+    // the throughput build (64-register budget), except the two bases the per-launch path uses
+    const volatile UrgChainRec *crv = &chs[valid ? c : 0];
+    const uint32_t kbase = cr.kern_base, tbase = cr.task_base;
+#define CRF(f) (WIDE ? crv->f : cr.f)
 
     for (;;) {
         unsigned long long jw = 0;
@@ -211,8 +216,8 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         // ---- A1: scenario init (R3, R15 STATIC) ----
         int64_t Pp = 0, Dp = 0;
         if (valid) {
-            Pp = cr.period_ns * (int64_t)P.fa_den / (int64_t)P.fa_num;
-            Dp = cr.deadline_ns * (int64_t)P.fd_num / (int64_t)P.fd_den;
+            Pp = CRF(period_ns) * (int64_t)P.fa_den / (int64_t)P.fa_num;
+            Dp = CRF(deadline_ns) * (int64_t)P.fd_num / (int64_t)P.fd_den;
         }
         bool tight = false;
         if (P.tight_explicit) tight = valid && ((P.tight_mask >> c) & 1u);
@@ -273,7 +278,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             int64_t jit = 0;
             if (P.jitter_ns > 0)
                 jit = (int64_t)(rng_word(P.seed, s, URG_TAG_ARR, c, i, 0) % (uint32_t)(P.jitter_ns + 1));
-            return cr.offset_ns + (int64_t)i * Pp + jit;
+            return CRF(offset_ns) + (int64_t)i * Pp + jit;
         };
         auto inst_factor = [&](uint32_t w, uint32_t sigma) -> uint32_t {
             if (!T.inst_q) return 65536u;
@@ -293,7 +298,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         auto cls_key_a = [&]() -> int64_t {
             return KIND == K_EDF ? t_arr + Dp : KIND == K_HRRN ? t_arr : KIND == K_LCUF ? Pp : 0;
         };
-        auto cls_key_b = [&]() -> int64_t { return KIND == K_LCUF ? cr.gpu_est_total : rem_g + rem_c; };
+        auto cls_key_b = [&]() -> int64_t { return KIND == K_LCUF ? CRF(gpu_est_total) : rem_g + rem_c; };
         // "chain o ranks before chain s" (ties by smaller chain id; exact 128-bit ratios)
         auto cls_before = [&](int64_t oA, int64_t oB, int o, int64_t sA, int64_t sB, int sl, int64_t t) -> bool {
             if (KIND == K_EDF || KIND == K_SJF) {
@@ -325,14 +330,14 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         auto retire = [&](int64_t t) {
             ++done;
             head_end = INF64;
-            if (launched > done) { head_ready = t; head_u = T.kern[cr.kern_base + done].util_permille; }
+            if (launched > done) { head_ready = t; head_u = T.kern[kbase + done].util_permille; }
             if (pc == PC_SYNC_WAIT && done >= sync_target) { pc = PC_SYNC_RET; cpu_next = t + sync_cost; }
         };
         // Phase C start of this lane's waiting head: non-preemptive, exact duration (R4, R19, R20)
         auto start_head = [&](int64_t t) {
             uint64_t G = 65536u;
             if (KQ) G = T.kern_q[rng_word(P.seed, s, URG_TAG_KERN, c, inst, done) >> 20];
-            uint64_t d = ((((uint64_t)T.kern[cr.kern_base + done].nominal_ns * Fg) >> 16) * G) >> 16;
+            uint64_t d = ((((uint64_t)T.kern[kbase + done].nominal_ns * Fg) >> 16) * G) >> 16;
             d = d < 1 ? 1 : (d > 0xFFFFFFFFull ? 0xFFFFFFFFull : d);
             head_util = head_u;
             head_end = t + (int64_t)d;
@@ -354,7 +359,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                 if (pc == PC_SYNC_RET) {   // sync returned: covered kernels leave the AKB
                     if (akb_on) akb = launched - sync_target;
                     if (launched < task_end) pc = PC_ATTEMPT;
-                    else if (has_free && (T.task[cr.task_base + task].flags & 1u)) {
+                    else if (has_free && (T.task[tbase + task].flags & 1u)) {
                         // R28: the task ends with cudaFree -- request the device barrier and block
                         pc = PC_FREE_WAIT;
                         free_req = t;
@@ -364,9 +369,9 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                 }
                 if (pc == PC_FREE_RET) task_done = true;   // R28: the barrier was served
                 if (task_done) {
-                    if (++task < cr.num_tasks) {
+                    if (++task < CRF(num_tasks)) {
                         task_first = task_end;
-                        task_end += T.task[cr.task_base + task].num_kernels;
+                        task_end += T.task[tbase + task].num_kernels;
                         pc = PC_TASK_START;
                     } else {   // instance complete (R18, R22)
                         const int64_t rt = t - t_arr;
@@ -382,15 +387,15 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                 }
                 if (pc == PC_ARRIVE) {   // frame arrival / instance start (R6)
                     ++n_total;
-                    Fg = inst_factor(rng_word(P.seed, s, URG_TAG_INST, c, inst, 0), cr.gpu_sigma_ppm);
-                    Fc = inst_factor(rng_word(P.seed, s, URG_TAG_INST, c, inst, 1), cr.cpu_sigma_ppm);
+                    Fg = inst_factor(rng_word(P.seed, s, URG_TAG_INST, c, inst, 0), CRF(gpu_sigma_ppm));
+                    Fc = inst_factor(rng_word(P.seed, s, URG_TAG_INST, c, inst, 1), CRF(cpu_sigma_ppm));
                     task = 0; launched = 0; done = 0; sync_ord = 0;
-                    rem_g = cr.gpu_est_total; rem_c = cr.cpu_est_total;
+                    rem_g = CRF(gpu_est_total); rem_c = CRF(cpu_est_total);
                     if (ma) {   // R26: this instance's ~E^cpu_j, floor mean of the last min(W, h_j) measurements
                         rem_c = 0;
-                        for (uint32_t j = 0; j < cr.num_tasks; ++j) {
+                        for (uint32_t j = 0; j < CRF(num_tasks); ++j) {
                             const uint32_t h = ma_cnt[j];
-                            uint32_t pred = T.task[cr.task_base + j].cpu_estimate_ns;
+                            uint32_t pred = T.task[tbase + j].cpu_estimate_ns;
                             if (h) {
                                 const uint32_t k = h < P.ma_w ? h : P.ma_w;
                                 uint64_t sum = 0;
@@ -401,7 +406,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                             rem_c += pred;
                         }
                     }
-                    task_first = 0; task_end = T.task[cr.task_base].num_kernels;
+                    task_first = 0; task_end = T.task[tbase].num_kernels;
                     pc = PC_TASK_START;
                 }
                 if (pc == PC_TASK_START) {   // new CPU segment: evaluate, early exit
@@ -422,7 +427,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                         }
                     }
                     if (!exited) {
-                        const int64_t e = (int64_t)(((uint64_t)T.task[cr.task_base + task].cpu_nominal_ns * Fc) >> 16);
+                        const int64_t e = (int64_t)(((uint64_t)T.task[tbase + task].cpu_nominal_ns * Fc) >> 16);
                         if (ma) { ma_ring[task * P.ma_w + ma_cnt[task] % P.ma_w] = (uint32_t)e; ++ma_cnt[task]; }
                         pc = PC_CPU_DONE;
                         cpu_next = t + e;
@@ -441,7 +446,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                 }
                 if (pc == PC_ENQUEUE) {   // the kernel reaches its stream (R16) + sync decision (R17)
                     const uint32_t n = launched;
-                    const UrgKernRec kr = T.kern[cr.kern_base + n];
+                    const UrgKernRec kr = T.kern[kbase + n];
                     const int64_t est = kr.estimate_ns;
                     if (launched == done) { head_ready = t; head_u = kr.util_permille; newhead = true; }   // stream was empty
                     ++launched; ++n_launch;
@@ -459,7 +464,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                         if (k && !CAL) atomicAdd(&agg[(uint64_t)C * stride + (k + 1 > 32 ? 32 : k + 1)], 1ull);
                     }
                     const bool last = launched == task_end;
-                    if (last) rem_c -= ma ? ma_pred[task] : T.task[cr.task_base + task].cpu_estimate_ns;
+                    if (last) rem_c -= ma ? ma_pred[task] : T.task[tbase + task].cpu_estimate_ns;
                     if (n == task_first) { acc = 0; batch_start = task_first; }
                     int32_t target = -1;
                     if (P.sync_mode == S_ASYNC) {
@@ -504,7 +509,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     if (urg) { lax = laxity(t); L_last = lax; }
                     const bool own_urgent = lax >= 0 && lax <= P.lax_threshold_ns;
                     if (f_delay && !own_urgent && (urgent_m & ~(1u << lane)) &&
-                        T.kern[cr.kern_base + launched].util_permille >= P.util_exempt) {
+                        T.kern[kbase + launched].util_permille >= P.util_exempt) {
                         pc = PC_ATTEMPT;
                         cpu_next = t + P.sleep_ns;
                         break;
