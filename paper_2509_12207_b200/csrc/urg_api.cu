@@ -19,7 +19,8 @@
 
 typedef void (*urg_sim_fn)(const uint8_t *blob, const UrgSimParams P, uint32_t *records, unsigned long long *agg,
                            unsigned long long *work, long long *err);
-const void *urg_sim_kernel_for(uint32_t kind, uint32_t flags, bool kern_q, bool wide, bool cal, bool ext);   // urg_sim.cu
+const void *urg_sim_kernel_for(uint32_t kind, uint32_t flags, bool kern_q, bool wide, bool cal, bool ext,
+                               bool pk);   // urg_sim.cu
 extern "C" __global__ void urg_cal_hist_kernel(const int64_t *buf, uint64_t count, uint64_t cap, long long *ws,
                                                int pass);
 extern "C" __global__ void urg_cal_pick_kernel(long long *ws, int pass, int pct, long long *result);
@@ -296,8 +297,11 @@ static urg_status prepare_launch(const urg_workload *w, const urg_policy *p, con
     bool ext = (p->kind == URG_URGENGO && p->noise_permille) || (p->kind >= URG_URGENGO && p->cpu_ma_window) ||
                w->has_free;
     if (const char *ee = getenv("URG_EXT")) ext = ext || atoi(ee) != 0;   // test hook: force the extended build
+    // two scenarios per warp in the throughput core build when the chains fit a half warp
+    bool pk = wide && !cal && !ext && w->num_chains <= 16;
+    if (const char *ep = getenv("URG_PACK")) pk = pk && atoi(ep) != 0;          // test hook: disable packing
     fn = (urg_sim_fn)urg_sim_kernel_for(p->kind, p->kind == URG_URGENGO ? p->flags : 0, w->has_kern_q, wide && !cal,
-                                        cal, ext);
+                                        cal, ext, pk);
     if (!fn) return fail(URG_EINTERNAL, "no kernel instantiation for kind %u flags %u", p->kind, p->flags);
     P.blob_bytes = (uint32_t)w->blob.size();
     P.mbar_offset = align16(P.blob_bytes);
@@ -308,8 +312,8 @@ static urg_status prepare_launch(const urg_workload *w, const urg_policy *p, con
         P.ma_slot = w->max_tasks * (P.ma_w + 2);
         per_lane += P.ma_slot * 4u;
     }
-    urg_status st = geometry(w, (const void *)fn, b->scenario_count, P.snap_offset, per_lane, warps, ctas,
-                             P.smem_bytes);
+    urg_status st = geometry(w, (const void *)fn, pk ? (b->scenario_count + 1) / 2 : b->scenario_count,
+                             P.snap_offset, per_lane, warps, ctas, P.smem_bytes);
     if (st != URG_OK) return st;
     P.ma_offset = P.snap_offset + (uint32_t)warps * 32u * URG_SNAP_BYTES_PER_LANE;
     return URG_OK;

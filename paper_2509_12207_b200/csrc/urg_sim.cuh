@@ -135,7 +135,11 @@ struct Tmpl {   // shared-memory views of the staged template
 // EXT: the extended-model build (estimation noise R25, CPU predictor R26, cudaFree
 // barriers R28 resolved at run time); the core build has none of their branches (the
 // policies of the benchmarks use none of them and run ~9 % faster without).
-template <int KIND, int FLAGS, bool KQ, bool WIDE, bool CAL = false, bool EXT = true>
+//
+// PK: two scenarios per warp (lanes 0-15 and 16-31, at most 16 chains), throughput core
+// build only: the halves step in lockstep, every warp collective is segmented per half,
+// so the step's overhead is shared by two scenarios.
+template <int KIND, int FLAGS, bool KQ, bool WIDE, bool CAL = false, bool EXT = true, bool PK = false>
 __global__ void __launch_bounds__(WIDE ? 1024 : 512, 1)
 urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t *__restrict__ records,
                unsigned long long *__restrict__ agg, unsigned long long *__restrict__ work,
@@ -190,8 +194,32 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
     uint32_t *ma_pred = ma_cnt + P.ma_max_tasks;
     const int64_t busy_launch = P.launch_ns + (urg ? P.launch_akb_ns : 0);
     const uint32_t stride = P.agg_stride;
-    const bool valid = (uint32_t)lane < C;
-    const uint32_t c = lane;
+    // lane -> (half, chain); masks and snapshot slots stay indexed by lane
+    const int half = PK ? (lane >> 4) : 0;
+    const uint32_t hmask = PK ? (0xFFFFu << (16 * half)) : FULL;
+    const int hbase = PK ? (lane & 16) : 0;
+    const uint32_t c = PK ? (uint32_t)(lane & 15) : (uint32_t)lane;
+    const bool valid_c = c < C;
+    // per-half warp collectives (the whole warp when !PK)
+    auto hmin = [&](uint32_t v) -> uint32_t {
+        if (!PK) return __reduce_min_sync(FULL, v);
+        const uint32_t a = __reduce_min_sync(FULL, half ? 0xFFFFFFFFu : v);
+        const uint32_t b = __reduce_min_sync(FULL, half ? v : 0xFFFFFFFFu);
+        return half ? b : a;
+    };
+    auto hsum = [&](uint32_t v) -> uint32_t {
+        if (!PK) return __reduce_add_sync(FULL, v);
+        const uint32_t a = __reduce_add_sync(FULL, half ? 0u : v);
+        const uint32_t b = __reduce_add_sync(FULL, half ? v : 0u);
+        return half ? b : a;
+    };
+    auto hany = [&](bool pred) -> bool { return (__ballot_sync(FULL, pred) & hmask) != 0u; };
+    auto hmin64 = [&](int64_t v) -> int64_t {   // v >= 0 in every lane
+        const uint32_t hi = (uint32_t)((uint64_t)v >> 32), lo = (uint32_t)v;
+        const uint32_t mh = hmin(hi);
+        const uint32_t ml = hmin(hi == mh ? lo : 0xFFFFFFFFu);
+        return (int64_t)(((uint64_t)mh << 32) | ml);
+    };
     unsigned long long my_launches = 0, my_steps = 0;
 #ifdef URG_STATS
     unsigned long long st_single = 0, st_multi = 0, st_dispatch = 0, st_rebase = 0;   // profiling build only
@@ -199,18 +227,20 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
 
     // static per-chain template data
     UrgChainRec cr = {};
-    if (valid) cr = chs[c];
+    if (valid_c) cr = chs[c];
     // the chain record: a register copy in the latency build; re-read from shared memory in
     // the throughput build (64-register budget), except the two bases the per-launch path uses
-    const volatile UrgChainRec *crv = &chs[valid ? c : 0];
+    const volatile UrgChainRec *crv = &chs[valid_c ? c : 0];
     const uint32_t kbase = cr.kern_base, tbase = cr.task_base;
 #define CRF(f) (WIDE ? crv->f : cr.f)
 
     for (;;) {
         unsigned long long jw = 0;
-        if (lane == 0) jw = atomicAdd(work, 1ull);
+        if (lane == 0) jw = atomicAdd(work, PK ? 2ull : 1ull);
         jw = __shfl_sync(FULL, jw, 0);
         if (jw >= P.scenario_count) break;
+        jw += (unsigned long long)half;                        // PK: the upper half takes the next one
+        const bool valid = valid_c && jw < P.scenario_count;
         const uint32_t s = (uint32_t)(P.scenario_begin + jw);
 
         // ---- A1: scenario init (R3, R15 STATIC) ----
@@ -226,7 +256,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             const uint32_t w = valid ? rng_word(P.seed, s, URG_TAG_TIGHT, c, 0, 0) : 0xFFFFFFFFu;
             uint32_t rank = 0;
             for (uint32_t o = 0; o < C; ++o) {
-                const uint32_t wo = __shfl_sync(FULL, w, o);
+                const uint32_t wo = __shfl_sync(FULL, w, hbase + (int)o);
                 rank += (wo < w || (wo == w && o < c)) ? 1u : 0u;
             }
             tight = valid && rank < n_tight;
@@ -234,7 +264,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         if (tight) Dp /= 2;
         int64_t maxD = Dp;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
+        for (int o = PK ? 8 : 16; o > 0; o >>= 1) {
             const int64_t x = (int64_t)__shfl_xor_sync(FULL, (unsigned long long)maxD, o);
             maxD = x > maxD ? x : maxD;
         }
@@ -243,7 +273,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         {
             uint32_t r = 1;
             for (uint32_t o = 0; o < C; ++o) {
-                const int64_t Do = shfl64(Dp, o);
+                const int64_t Do = shfl64(Dp, hbase + (int)o);
                 r += (Do < Dp || (Do == Dp && o < c)) ? 1u : 0u;
             }
             if (C > 1 && P.num_prio > 1) static_level = (uint32_t)(((uint64_t)(r - 1) * (P.num_prio - 1)) / (C - 1));
@@ -562,19 +592,19 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         // binding snapshot is not needed).
         auto snapshot = [&](bool may_bind, uint32_t &urgent_m, uint32_t &active_m, uint32_t &busy_m) {
             urgent_m = 0; active_m = 0; busy_m = 0;
-            if (f_delay) urgent_m = __ballot_sync(FULL, akb > 0 && L_last >= 0 && L_last <= P.lax_threshold_ns);
+            if (f_delay) urgent_m = __ballot_sync(FULL, akb > 0 && L_last >= 0 && L_last <= P.lax_threshold_ns) & hmask;
             if (coll) {
-                busy_m = __ballot_sync(FULL, launched > done);
-                active_m = __ballot_sync(FULL, akb > 0);
+                busy_m = __ballot_sync(FULL, launched > done) & hmask;
+                active_m = __ballot_sync(FULL, akb > 0) & hmask;
                 snapL[lane] = L_last;
                 snapLev[lane] = level;
                 __syncwarp();
             } else if (f_bind && __any_sync(FULL, may_bind)) {
-                active_m = __ballot_sync(FULL, akb > 0);
+                active_m = __ballot_sync(FULL, akb > 0) & hmask;
                 snapL[lane] = L_last;
                 __syncwarp();
             } else if (cls && __any_sync(FULL, may_bind)) {
-                active_m = __ballot_sync(FULL, akb > 0);
+                active_m = __ballot_sync(FULL, akb > 0) & hmask;
                 snapA[lane] = cls_key_a();
                 snapB[lane] = cls_key_b();
                 __syncwarp();
@@ -595,17 +625,20 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         bool bar_prev = false;                  // R28: a barrier was pending at the previous step
         int64_t cal_next = 0;                   // CAL: next sampling time
         uint32_t cal_n = 0;                     // CAL: samples of this scenario
+        bool fin = false;                       // PK: this half's scenario has ended
         for (;;) {
             // A2: next event time.  Every lane's next event is strictly after t_prev, so
             // the warp minimum is taken on the 32-bit distance (one REDUX); distances that
             // do not fit 32 bits saturate and fall back to the exact 64-bit minimum.
-            const int64_t mine = head_end < cpu_next ? head_end : cpu_next;
+            const int64_t mine = fin ? INF64 : (head_end < cpu_next ? head_end : cpu_next);
             const uint64_t dl = (uint64_t)mine - (uint64_t)t_prev;   // exact when mine > t_prev
             const uint32_t d32 = mine <= t_prev ? 0u : (dl >= 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)dl);
-            const uint32_t m = __reduce_min_sync(FULL, d32);
+            const uint32_t m = hmin(d32);
             int64_t t;
-            if (m == 0xFFFFFFFFu) t = warp_min_nonneg(mine);
-            else t = t_prev + m;
+            if (PK ? __any_sync(FULL, m == 0xFFFFFFFFu && !fin) : m == 0xFFFFFFFFu) {
+                const int64_t tt = hmin64(mine);
+                t = m == 0xFFFFFFFFu ? tt : t_prev + m;
+            } else t = t_prev + m;
             if (CAL && cal_next < P.cal_end && cal_next < t) {
                 // the state between two steps is constant: one warp max of the AKB urgency
                 // keys (order-preserving unsigned), then one sample per elapsed 1 ms tick
@@ -625,25 +658,35 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                 }
             }
             if (CAL && cal_next >= P.cal_end) break;   // no sample left to take
-            if (t > H_stop) break;
-            if (m == 0u) {   // time must advance (invariant); report and stop this scenario
-                if (lane == 0 && atomicCAS((unsigned long long *)err, 0ull, (unsigned long long)ERR_TIME) == 0ull)
+            if (PK) {   // each half ends on its own; the warp goes on while one half runs
+                if (!fin && m == 0u && lane == hbase &&
+                    atomicCAS((unsigned long long *)err, 0ull, (unsigned long long)ERR_TIME) == 0ull)
                     err[1] = s;
-                break;
+                fin = fin || t > H_stop || m == 0u;
+                if (__all_sync(FULL, fin)) break;
+            } else {
+                if (t > H_stop) break;
+                if (m == 0u) {   // time must advance (invariant); report and stop this scenario
+                    if (lane == 0 && atomicCAS((unsigned long long *)err, 0ull, (unsigned long long)ERR_TIME) == 0ull)
+                        err[1] = s;
+                    break;
+                }
             }
-            t_prev = t;
-            ++my_steps;
+            if (!fin) {
+                t_prev = t;
+                if (lane == hbase) ++my_steps;   // one loop step of this half's scenario
+            }
 
             // Phase A: retire (R21, R19)
-            const bool ret = head_end == t;
-            bool dirty = __any_sync(FULL, ret);   // GPU state changed: Phase C must run
-            if (dirty) {
-                used -= __reduce_add_sync(FULL, ret ? head_util : 0u);
+            const bool ret = !fin && head_end == t;
+            bool dirty = PK ? hany(ret) : __any_sync(FULL, ret);   // GPU state changed: Phase C must run
+            if (PK ? __any_sync(FULL, ret) : dirty) {
+                used -= hsum(ret ? head_util : 0u);
                 if (ret) retire(t);
             }
 
             // Phase B: CPU steps of every chain due at t, against the round snapshot (R21)
-            const bool due = cpu_next == t;
+            const bool due = !fin && cpu_next == t;
             if (__any_sync(FULL, due)) {
 #ifdef URG_STATS
                 ++st_multi;
@@ -652,7 +695,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                 if (urg || cls) snapshot(due && can_bind(), urgent_m, active_m, busy_m);
                 bool nh = false;
                 if (due) nh = phase_b(t, urgent_m, active_m, busy_m);
-                dirty |= __any_sync(FULL, nh);
+                dirty |= PK ? hany(nh) : __any_sync(FULL, nh);
             }
 
 
@@ -680,7 +723,30 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             // waiting head was already found not to fit and `used` has not decreased.
             // The greedy scan in key order starts, each time, the smallest-key head that
             // fits the capacity left (heads that do not fit stay unfit as `used` grows).
-            if (dirty) {
+            if (PK && __any_sync(FULL, dirty)) {
+                // both halves: a half that is not dirty has no head that fits (fit = 0)
+                bool waiting = !fin && launched > done && head_end == INF64;
+                for (;;) {
+                    const uint32_t fitw = __ballot_sync(FULL, waiting && used + head_u <= 1000u);
+                    if (!fitw) break;
+                    const uint32_t fit = fitw & hmask;
+                    const bool multi = (fit & (fit - 1)) != 0u;
+                    const bool any_multi = __any_sync(FULL, multi);
+                    int wl = fit ? __ffs(fit) - 1 : -1;
+                    if (any_multi) {
+                        const bool in = (fit >> lane) & 1u;
+                        const uint64_t key = ((uint64_t)level << 56) | ((uint64_t)head_ready << 5) | (uint64_t)lane;
+                        const uint32_t hi = in ? (uint32_t)(key >> 32) : 0xFFFFFFFFu;
+                        const uint32_t mh = hmin(hi);
+                        const uint32_t ml = hmin((in && hi == mh) ? (uint32_t)key : 0xFFFFFFFFu);
+                        if (fit) wl = (int)(ml & 31u);
+                    }
+                    const uint32_t uw = __shfl_sync(FULL, head_u, wl >= 0 ? wl : lane);
+                    if (wl >= 0) used += uw;
+                    if (lane == wl) { start_head(t); waiting = false; }
+                    if (!any_multi) break;   // each half started its only fitting head (others did not fit)
+                }
+            } else if (!PK && dirty) {
 #ifdef URG_STATS
                 ++st_dispatch;
 #endif
@@ -732,6 +798,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         }
         my_launches += __reduce_add_sync(FULL, n_launch);
     }
+    if (PK) my_steps += __shfl_sync(FULL, my_steps, 16);   // the upper half's steps
     if (lane == 0) {
         if (CAL) return;
         atomicAdd(&agg[(uint64_t)C * stride + URG_COLL_BINS + 0], my_launches);
@@ -756,9 +823,15 @@ struct UrgRow {
     static constexpr int K = ROW == 0 ? K_FIFO : ROW == 1 ? K_STATIC : ROW < 34 ? K_URGENGO : K_EDF + (ROW - 34);
     static constexpr int F = ROW < 2 || ROW >= 34 ? 0 : ROW < 18 ? ROW - 2 : ROW - 18;
     static constexpr bool C = ROW >= 18 && ROW < 34;
-    // col: bit 0 per-kernel factor table, bit 1 throughput build, bit 2 extended model
+    // col: bit 0 per-kernel factor table, bit 1 throughput build, bit 2 extended model,
+    // bit 3 two scenarios per warp (throughput core build only)
     static const void *get(uint32_t col)
     {
+        if constexpr (!C) {
+            if ((col & 14u) == 10u)
+                return (col & 1u) ? (const void *)urg_sim_kernel<K, F, true, true, false, false, true>
+                                  : (const void *)urg_sim_kernel<K, F, false, true, false, false, true>;
+        }
         if constexpr (C) {   // the calibration build: latency variant, extended model
             return (col & 1u) ? (const void *)urg_sim_kernel<K, F, true, false, true, true>
                               : (const void *)urg_sim_kernel<K, F, false, false, true, true>;

@@ -450,3 +450,39 @@ def test_extended_build_equals_core(ext_build):
     for name in ("urgengo", "fifo", "static"):
         both(cfg.workload(), cfg.policies[name], b, f"ext paper11 {name}")
     both(cfg.workload(), Policy(kind=5, flags=0, sync_mode=SYNC_OVERLAP), b, "ext paper11 hrrn")
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_packed_two_scenarios_per_warp(seed, wide_build):
+    """PK build (two scenarios per warp, throughput core build, C <= 16): random workloads and
+    policies, odd scenario counts (the last warp's upper half has no scenario)."""
+    rng = random.Random(13000 + seed)
+    w = random_workload(rng, C=rng.choice([1, 2, 5, 11, 16]), jitter=rng.choice([0, 2 * MS]))
+    if rng.random() < 0.5:
+        from workloads.quantiles import inst_z_table, pareto_table
+        w.inst_quantiles_q16 = inst_z_table()
+        for ch in w.chains:
+            ch.cpu_sigma_ppm, ch.gpu_sigma_ppm = rng.randint(0, 500_000), rng.randint(0, 500_000)
+        if rng.random() < 0.5:
+            w.kern_quantiles_q16 = pareto_table()
+    p = random_policy(rng)
+    p.kind = rng.choice([FIFO, STATIC, URGENGO, URGENGO, 3, 4, 5, 6])
+    p.flags = rng.randint(0, 15) if p.kind == URGENGO else 0
+    b = Batch(seed=seed, scenario_begin=rng.randint(0, 50), scenario_count=rng.choice([1, 3, 7, 33, 64]),
+              horizon_ns=rng.choice([150, 400]) * MS, ftight_permille=rng.choice([0, 400]))
+    both(w, p, b, f"pk seed {seed}")
+
+
+def test_packed_equals_unpacked_large_batch(monkeypatch):
+    """configs[4]'s workload, 5001 scenarios (throughput build): the packed and the one-scenario-
+    per-warp kernels give identical records and aggregates."""
+    cfg = get_config("scaleout")
+    w, p = cfg.workload(), cfg.policies["urgengo"]
+    b = Batch(seed=cfg.batch.seed, scenario_count=5001, horizon_ns=150 * MS, ftight_permille=400)
+    r1, a1 = gpu_run(w, p, b)
+    monkeypatch.setenv("URG_PACK", "0")
+    r2, a2 = gpu_run(w, p, b)
+    assert np.array_equal(r1, r2) and np.array_equal(a1, a2)
+    o = O.run(w, p, Batch(seed=b.seed, scenario_begin=5000, scenario_count=1, horizon_ns=b.horizon_ns,
+                          ftight_permille=400))
+    assert np.array_equal(o.records[0], r1[5000])
