@@ -140,7 +140,10 @@ struct Tmpl {   // shared-memory views of the staged template
 // build only: the halves step in lockstep, every warp collective is segmented per half,
 // so the step's overhead is shared by two scenarios.
 template <int KIND, int FLAGS, bool KQ, bool WIDE, bool CAL = false, bool EXT = true, bool PK = false>
-__global__ void __launch_bounds__(WIDE ? 1024 : 512, 1)
+#ifndef URG_PK_THREADS
+#define URG_PK_THREADS 768   // measured: 80 registers beat 64 with spills (configs[2]/[4] +3-4 %)
+#endif
+__global__ void __launch_bounds__(WIDE ? (PK ? URG_PK_THREADS : 1024) : 512, 1)
 urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t *__restrict__ records,
                unsigned long long *__restrict__ agg, unsigned long long *__restrict__ work,
                long long *__restrict__ err)
