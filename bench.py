@@ -169,6 +169,7 @@ def parse():
     ap.add_argument("--scenarios", type=int, default=0, help="override scenarios per GPU (default: the config's)")
     ap.add_argument("--horizon-ms", type=int, default=0, help="override the horizon")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-throughput", action="store_true", help="skip the configs[4] throughput-regime line item")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU work of the cpu_baseline sample")
     return ap.parse_args()
 
@@ -239,6 +240,7 @@ def main():
     from paper_2509_12207_b200.dist import allreduce_agg
     from paper_2509_12207_b200.urg import DeviceWorkload, OutputsS, batch_struct, lib, policy_struct
     from dataclasses import replace
+    from workloads import get_config
     from workloads.spec import RECORD_WORDS
 
     world = _env_int("WORLD_SIZE", 1)
@@ -384,6 +386,37 @@ def main():
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": a.steps,
             "clocks": clocks}
+
+    # ---- throughput regime beside the headline (not the metric's workload): configs[4]'s
+    #      workload at a size that fills the GPU, the throughput build, device-timed ----
+    if not a.no_throughput and a.config == "paper11":
+        tcfg = get_config("scaleout")
+        tw = tcfg.workload()
+        tS = 300_000
+        tb = replace(tcfg.batch, scenario_begin=rank * tS, scenario_count=tS)
+        tdw = DeviceWorkload(tw)
+        tagg = torch.zeros(tdw.agg_words, dtype=torch.int64, device="cuda")
+        tdw.simulate(tcfg.policies["urgengo"], tb, tagg, stream=stream)          # warm-up
+        tt_ms = []
+        for _ in range(2):
+            tagg.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            tdw.simulate(tcfg.policies["urgengo"], tb, tagg, stream=stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            tt_ms.append(e0.elapsed_time(e1))
+        tdw.check(stream)
+        tl = int(tagg[-2].item())
+        tdw.close()
+        x = torch.tensor([max(tt_ms)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(x, op=dist.ReduceOp.MAX)
+        line["throughput_regime"] = {
+            "workload": f"scaleout (BASELINE.json configs[4]) workload, {tS} scenarios x 1 s per GPU, UrgenGo; "
+                        "throughput build (two scenarios per warp); reported beside the headline, not the metric",
+            "value": tl * n / (x.item() / 1e3), "unit": UNIT, "ms_per_launch": x.item(),
+            "launch_events_per_gpu": tl}
 
     # ---- cpu_baseline: the oracle, unchanged, on a bounded sample (rank 0, N = 1 only) ----
     if pool is not None:
