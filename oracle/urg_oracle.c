@@ -53,6 +53,7 @@ typedef struct {
     int64_t rt_bin_ns;
     uint32_t rt_bins;
     int64_t free_ns;            /* cudaFree cost once the device is idle (Table 5) */
+    uint32_t cpu_cores;         /* CPU cores shared by the chains' threads, 0 = one per thread (R29) */
     /* policy */
     uint32_t kind, flags, sync_mode;
     int64_t delta_eval_ns, lax_threshold_ns, sleep_ns;
@@ -73,7 +74,7 @@ enum { TAG_ARR = 1, TAG_TIGHT = 2, TAG_INST = 3, TAG_KERN = 4, TAG_SYNC = 5, TAG
 /* trace kinds */
 enum { TR_STEP = 1, TR_INST_START, TR_TASK_START, TR_EVAL, TR_DELAY, TR_BIND, TR_ENQUEUE,
        TR_DISPATCH, TR_RETIRE, TR_SYNC_CALL, TR_SYNC_RET, TR_FREE_CLOSE, TR_INST_DONE,
-       TR_EARLY_EXIT, TR_COLLISION, TR_FREE_CALL, TR_FREE_START, TR_FREE_RET };
+       TR_EARLY_EXIT, TR_COLLISION, TR_FREE_CALL, TR_FREE_START, TR_FREE_RET, TR_CPU_RUN, TR_CPU_STOP };
 
 #define REC_WORDS 8
 #define AGG_COUNTERS 5
@@ -255,6 +256,10 @@ typedef struct {
     int head_running;
     int64_t head_ready, head_end;
     int64_t free_req;               /* time of this chain's pending cudaFree request (R28) */
+    /* CPU job of the chain's thread under a limited core count (R29) */
+    int job, job_run;               /* a job exists / it holds a core */
+    int64_t job_rem, job_ready, run_start;
+    int64_t cpu_prio;               /* SCHED_FIFO priority key: higher runs first */
     /* results */
     uint32_t total, miss, early, unfin, launches, hash;
     uint64_t sum_rt;
@@ -277,6 +282,7 @@ typedef struct {
     int64_t *trace; int64_t trace_cap; int64_t trace_len;
     int64_t *agg;
     int64_t steps, launches, t_prev;
+    int cpu_dirty, rerank;          /* R29: the runnable set / the priorities changed in this step */
     /* calibration sampling */
     int64_t cal_next, cal_end;
     int64_t *cal_L; int64_t cal_n, cal_cap;
@@ -548,13 +554,15 @@ static int next_instance(orc_sim *S, uint32_t c, int64_t t)
     return 1;
 }
 
+static void cpu_busy(orc_sim *S, uint32_t c, int64_t t, int64_t d);
+
 static void issue_sync(orc_sim *S, uint32_t c, int64_t t, uint32_t target)
 {
     orc_lane *L = &S->lane[c];
     L->sync_target = target;
     L->sync_cost = sync_cost(S, c, L->inst, L->sync_ord++);
     tr(S, t, TR_SYNC_CALL, c, L->inst, target, L->sync_cost);
-    if (L->done >= target) { L->pc = PC_SYNC_RET; L->cpu_next = t + L->sync_cost; }
+    if (L->done >= target) { L->pc = PC_SYNC_RET; cpu_busy(S, c, t, L->sync_cost); }
     else { L->pc = PC_SYNC_WAIT; L->cpu_next = ORC_INF; }
 }
 
@@ -591,6 +599,26 @@ static void count_collision(orc_sim *S, uint32_t c, int64_t t)
     tr(S, t, TR_COLLISION, c, L->inst, card, L->level);
 }
 
+/* The chain's thread is busy for d ns from t -- a CPU segment, a launch call or a sync
+ * call's cost.  With one core per thread (cpu_cores = 0) it simply runs; with cpu_cores
+ * cores it becomes a CPU job that runs when the scheduler gives it a core (R29). */
+static void cpu_busy(orc_sim *S, uint32_t c, int64_t t, int64_t d)
+{
+    orc_lane *L = &S->lane[c];
+    if (S->in->cpu_cores == 0 || d == 0) { L->cpu_next = t + d; return; }
+    L->job = 1; L->job_run = 0; L->job_rem = d; L->job_ready = t; L->cpu_next = ORC_INF;
+    S->cpu_dirty = 1;
+}
+
+/* Chain c's urgency laxity at t without refreshing its AKB (the CPU re-rank of R29). */
+static int64_t current_laxity(const orc_sim *S, uint32_t c, int64_t t)
+{
+    const orc_lane *L = &S->lane[c];
+    int64_t lax = orc_eq2_laxity(L->t_arr, L->Dp, S->in->k_est + L->kbase, L->N, L->launched,
+                                 L->cpu_pred, L->M, L->cpu_idx, t);
+    return noisy_laxity(S, c, L->t_arr, L->Dp, t, lax);
+}
+
 /* One CPU step of chain c at time t (R21 Phase B): the thread runs
  * its program until it must wait for time to pass or for the GPU. */
 static void lane_step(orc_sim *S, uint32_t c, int64_t t)
@@ -621,7 +649,8 @@ static void lane_step(orc_sim *S, uint32_t c, int64_t t)
                 L->cpu_hist[L->task * W + L->cpu_hist_n[L->task] % W] = (uint32_t)e;
                 L->cpu_hist_n[L->task]++;
             }
-            L->pc = PC_CPU_DONE; L->cpu_next = t + e;
+            if (urgengo(S)) S->rerank = 1;                  /* a CPU segment starts: re-rank */
+            L->pc = PC_CPU_DONE; cpu_busy(S, c, t, e);
             if (e > 0) return;
             continue;
         }
@@ -641,7 +670,7 @@ static void lane_step(orc_sim *S, uint32_t c, int64_t t)
                 tr(S, t, TR_BIND, c, L->inst, L->level, n);
             }
             int64_t busy = in->launch_ns + (urgengo(S) ? in->launch_akb_ns : 0);
-            L->pc = PC_ENQUEUE; L->cpu_next = t + busy;
+            L->pc = PC_ENQUEUE; cpu_busy(S, c, t, busy);
             if (busy > 0) return;
             continue;
         }
@@ -810,7 +839,61 @@ static void retire(orc_sim *S, int64_t t)
         if (L->q_head < L->q_tail) L->head_ready = t;    /* next kernel becomes head */
         tr(S, t, TR_RETIRE, c, L->inst, K, 0);
         if (L->pc == PC_SYNC_WAIT && L->done >= L->sync_target) {
-            L->pc = PC_SYNC_RET; L->cpu_next = t + L->sync_cost;
+            L->pc = PC_SYNC_RET; cpu_busy(S, c, t, L->sync_cost);
+        }
+    }
+}
+
+/* CPU scheduling of the chains' threads on cpu_cores cores ("we
+ * calculate UL_C(t0) and then map the urgency level to the corresponding CPU priority
+ * PRI_C for all active chains ... sched_setscheduler(SCHED_FIFO)"; SPEC.md:130-134;
+ * DESIGN.md R29).  UrgenGo re-ranks every active chain by its urgency at t whenever a
+ * chain starts a CPU segment; STATIC uses its static levels; the other policies give every
+ * thread the same priority.  The runnable jobs are ordered by (priority descending, time
+ * they became runnable, chain id) and the first cpu_cores of them hold a core; a job that
+ * loses its core keeps its remaining work. */
+typedef struct { int64_t prio, ready; uint32_t chain; } orc_job;
+
+static int orc_job_cmp(const void *a, const void *b)
+{
+    const orc_job *x = a, *y = b;
+    if (x->prio != y->prio) return x->prio > y->prio ? -1 : 1;
+    if (x->ready != y->ready) return x->ready < y->ready ? -1 : 1;
+    return x->chain < y->chain ? -1 : (x->chain > y->chain);
+}
+
+static void cpu_schedule(orc_sim *S, int64_t t)
+{
+    const orc_input *in = S->in;
+    if (in->cpu_cores == 0) return;
+    if (S->rerank) {
+        S->rerank = 0;
+        for (uint32_t c = 0; c < S->C; ++c) {
+            orc_lane *L = &S->lane[c];
+            if (L->pc == PC_ARRIVE || L->pc == PC_DONE) continue;   /* not active */
+            L->cpu_prio = orc_urgency_key(current_laxity(S, c, t));
+        }
+        S->cpu_dirty = 1;
+    }
+    if (!S->cpu_dirty) return;
+    S->cpu_dirty = 0;
+    orc_job jobs[64];
+    uint32_t n = 0;
+    for (uint32_t c = 0; c < S->C; ++c) {
+        const orc_lane *L = &S->lane[c];
+        if (!L->job) continue;
+        jobs[n].prio = in->kind == ORC_STATIC ? -(int64_t)L->static_level : in->kind == ORC_URGENGO ? L->cpu_prio : 0;
+        jobs[n].ready = L->job_ready; jobs[n].chain = c; ++n;
+    }
+    qsort(jobs, n, sizeof(orc_job), orc_job_cmp);
+    for (uint32_t i = 0; i < n; ++i) {
+        orc_lane *L = &S->lane[jobs[i].chain];
+        if (i < in->cpu_cores && !L->job_run) {
+            L->job_run = 1; L->run_start = t; L->cpu_next = t + L->job_rem;
+            tr(S, t, TR_CPU_RUN, jobs[i].chain, L->inst, L->job_rem, 0);
+        } else if (i >= in->cpu_cores && L->job_run) {
+            L->job_run = 0; L->job_rem -= t - L->run_start; L->cpu_next = ORC_INF;
+            tr(S, t, TR_CPU_STOP, jobs[i].chain, L->inst, L->job_rem, 0);
         }
     }
 }
@@ -925,7 +1008,11 @@ static int sim_scenario(const orc_input *in, uint64_t s, uint32_t *rec, int64_t 
             S.snap_tarr[c] = S.lane[c].t_arr; S.snap_R[c] = remaining_work(&S, c);
         }
         for (uint32_t c = 0; c < S.C; ++c)                               /* Phase B */
-            if (S.lane[c].cpu_next == t) lane_step(&S, c, t);
+            if (S.lane[c].cpu_next == t) {
+                if (S.lane[c].job) { S.lane[c].job = 0; S.lane[c].job_run = 0; S.cpu_dirty = 1; }   /* job done */
+                lane_step(&S, c, t);
+            }
+        cpu_schedule(&S, t);                                             /* CPU cores (R29) */
         dispatch(&S, t);                                                 /* Phase C */
     }
     /* end of horizon (R7): admitted, unfinished instances are misses */

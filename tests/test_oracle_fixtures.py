@@ -319,3 +319,12 @@ def test_cudafree_serialises_requests():
     r = O.run(w, Policy(kind=FIFO, flags=0, sync_mode=SYNC_ASYNC), Batch(horizon_ns=1 * MS))
     # both kernels run 1-2 ms (u 400 + 400); both frees requested at 2 ms: chain 0 served 2-2.3, chain 1 2.3-2.6
     assert [_sum_rt(r.records[0][c]) for c in range(2)] == [2_300_000, 2_600_000]
+
+
+@pytest.mark.parametrize("case", _gold("w7.json")["cases"], ids=lambda c: c["name"])
+def test_w7_cpu_cores(case):
+    """R29: chains' threads sharing CPU cores with policy priorities (hand-derived)."""
+    from workloads import w7
+    w = w7(case["cores"])
+    r = O.run(w, Policy(kind=case["kind"], flags=0, sync_mode=SYNC_ASYNC, lax_threshold_ns=-1), Batch(horizon_ns=2 * MS))
+    assert [_sum_rt(r.records[0][c]) for c in range(2)] == [int(round(x * MS)) for x in case["rt_ms"]]

@@ -506,3 +506,38 @@ def test_cudafree_barrier_invariants(seed):
         elif name == "RETIRE":
             running.discard((c, i, a))
     assert r.records[0][:, 0].sum() > 0
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_cpu_cores_invariants(seed):
+    """R29 on random workloads: never more than K jobs hold a core, a preempted job keeps exactly
+    its unfinished work, FIFO (equal priorities) never preempts, and K >= C cores reproduce the
+    one-core-per-thread model exactly."""
+    rng = random.Random(6000 + seed)
+    w = random_workload(rng, C=rng.randint(2, 6))
+    p = random_policy(rng)
+    b = Batch(seed=seed, scenario_count=1, horizon_ns=300 * MS)
+    base = O.run(w, p, b)
+    w.cpu_cores = w.num_chains
+    assert np.array_equal(O.run(w, p, b).records, base.records)
+    K = rng.choice([1, 2])
+    w.cpu_cores = K
+    r = O.run(w, p, b, trace_cap=400_000)
+    running, last_t = {}, None
+    for t, k, c, i, a, bb in r.trace:
+        t, k, c, a = int(t), int(k), int(c), int(a)
+        if t != last_t:                                  # the core count holds between instants
+            assert len(running) <= K
+            last_t = t
+        for x in [x for x, (st, rem) in running.items() if st + rem <= t]:
+            del running[x]                               # completed jobs release their core
+        name = O.TRACE_KINDS[k]
+        if name == "CPU_RUN":
+            assert c not in running
+            running[c] = (t, a)
+        elif name == "CPU_STOP":
+            assert p.kind != FIFO, "equal priorities never preempt"
+            st, rem = running.pop(c)
+            assert a == rem - (t - st) and a > 0
+    assert len(running) <= K
+    assert r.records[:, :, 0].sum() > 0

@@ -74,6 +74,7 @@ class Workload:
     rt_bin_ns: int = 1 * MS
     rt_bins: int = 1024
     free_ns: int = 188 * US            # cudaFree cost on an idle device (Table 5; R28)
+    cpu_cores: int = 0                 # cores shared by the chains' threads, 0 = one each (8; R29)
 
     @property
     def num_chains(self) -> int:

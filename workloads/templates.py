@@ -160,3 +160,11 @@ def w6(two_chains: bool = True) -> Workload:
     b = Chain(1000 * MS, 100 * MS, 0, [Task(500 * US, 500 * US, [Kernel(5 * MS, 5 * MS, 500), Kernel(1 * MS, 1 * MS, 500)])])
     return Workload(chains=[a, b] if two_chains else [a], num_prio=2, launch_ns=0, launch_akb_ns=0, sync_lo_ns=0,
                     sync_hi_ns=0, jitter_ns=0, free_ns=188 * US)
+
+
+def w7(cores: int = 1) -> Workload:
+    """Fixture W7 (tests/golden/w7.json): two chains sharing CPU cores (R29)."""
+    a = Chain(1000 * MS, 20 * MS, 0, [Task(4 * MS, 4 * MS, [Kernel(1 * MS, 1 * MS, 1000)])])
+    b = Chain(1000 * MS, 6 * MS, 1 * MS, [Task(2 * MS, 2 * MS, [Kernel(1 * MS, 1 * MS, 1000)])])
+    return Workload(chains=[a, b], num_prio=2, launch_ns=0, launch_akb_ns=0, sync_lo_ns=0, sync_hi_ns=0,
+                    jitter_ns=0, cpu_cores=cores)
