@@ -80,6 +80,9 @@ typedef struct {
     uint32_t rt_bins;                     /* number of bins B (>= 1; last bin is open-ended) */
     int64_t free_ns;                      /* cudaFree cost on an idle device (Table 5: 188 us);
                                              must be > 0 when any task ends with cudaFree */
+    uint32_t cpu_cores;                   /* CPU cores shared by the chains' threads with the policy's
+                                             SCHED_FIFO priorities (8; DESIGN.md
+                                             R29); 0 = one core per thread, <= 32 */
 } urg_workload_desc;
 
 typedef struct urg_workload urg_workload; /* opaque; immutable after create; owns its device copy */

@@ -40,6 +40,7 @@ struct urg_workload {
     uint32_t max_tasks = 0;           // most tasks of any chain (CPU predictor state size, R26)
     bool has_free = false;            // some task ends with cudaFree (R28)
     int64_t free_ns = 0;
+    uint32_t cpu_cores = 0;           // cores shared by the chains' threads, 0 = one each (R29)
 };
 
 static thread_local std::string g_err;
@@ -89,6 +90,7 @@ extern "C" urg_status urg_create_workload(const urg_workload_desc *d, urg_worklo
     if (d->rt_bin_ns <= 0) return fail(URG_EINVAL, "rt_bin_ns must be > 0");
     if (d->rt_bins < 1 || d->rt_bins > (1u << 20)) return fail(URG_EINVAL, "rt_bins must be in 1..2^20");
     if (d->free_ns < 0 || d->free_ns >= (1LL << 40)) return fail(URG_EINVAL, "free_ns must be in [0, 2^40)");
+    if (d->cpu_cores > 32) return fail(URG_EINVAL, "cpu_cores must be <= 32 (0 = one core per chain thread)");
 
     uint32_t n_tasks = 0, n_kern = 0;
     for (uint32_t c = 0; c < d->num_chains && d->chains; ++c)
@@ -147,6 +149,7 @@ extern "C" urg_status urg_create_workload(const urg_workload_desc *d, urg_worklo
     w->jitter_ns = d->jitter_ns; w->rt_bin_ns = d->rt_bin_ns;
     w->has_kern_q = d->kern_quantiles_q16 != nullptr;
     w->free_ns = d->free_ns;
+    w->cpu_cores = d->cpu_cores;
     w->blob.assign(off, 0);
     memcpy(w->blob.data(), &h, sizeof h);
     UrgChainRec *chs = (UrgChainRec *)(w->blob.data() + h.off_chains);
@@ -249,7 +252,7 @@ static void fill_params(const urg_workload *w, const urg_policy *p, const urg_ba
     P.kind = p->kind; P.flags = p->flags; P.sync_mode = p->sync_mode; P.util_exempt = p->util_exempt_permille;
     P.delta_eval_ns = p->delta_eval_ns; P.lax_threshold_ns = p->lax_threshold_ns; P.sleep_ns = p->sleep_ns;
     P.noise_pm = p->noise_permille; P.ma_w = p->cpu_ma_window;
-    P.has_free = w->has_free ? 1u : 0u; P.free_ns = w->free_ns;
+    P.has_free = w->has_free ? 1u : 0u; P.free_ns = w->free_ns; P.cpu_cores = w->cpu_cores;
     P.seed = b->seed; P.scenario_begin = b->scenario_begin; P.scenario_count = b->scenario_count;
     P.horizon_ns = b->horizon_ns;
     P.fa_num = b->fa_num; P.fa_den = b->fa_den; P.fd_num = b->fd_num; P.fd_den = b->fd_den;
@@ -295,7 +298,7 @@ static urg_status prepare_launch(const urg_workload *w, const urg_policy *p, con
     fill_params(w, p, b, P);
     // the extended-model build only when the batch uses noise, the CPU predictor or cudaFree
     bool ext = (p->kind == URG_URGENGO && p->noise_permille) || (p->kind >= URG_URGENGO && p->cpu_ma_window) ||
-               w->has_free;
+               w->has_free || w->cpu_cores > 0;
     if (const char *ee = getenv("URG_EXT")) ext = ext || atoi(ee) != 0;   // test hook: force the extended build
     // two scenarios per warp in the throughput core build when the chains fit a half warp
     bool pk = wide && !cal && !ext && w->num_chains <= 16;

@@ -190,6 +190,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
     const bool noise = EXT && urg && P.noise_pm > 0;       // R25
     const bool ma = EXT && akb_on && P.ma_w > 0;           // R26 (every policy that estimates remaining work)
     const bool has_free = EXT && P.has_free != 0;          // R28: some task ends with cudaFree
+    const bool cores_on = EXT && P.cpu_cores > 0;          // R29: the chains' threads share P.cpu_cores cores
     // R26 predictor state of this lane's chain in shared memory: [max_tasks][W] ring of
     // measured CPU durations, [max_tasks] counts, [max_tasks] this instance's estimates
     uint32_t *ma_ring = (uint32_t *)(sm + P.ma_offset) + (size_t)threadIdx.x * P.ma_slot;
@@ -295,6 +296,9 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         int64_t rem_g = 0, rem_c = 0;          // sum of estimates of kernels / CPU segments not yet passed
         int32_t nz = 0;                        // R25: estimation noise of the current task instance, per-mille
         int64_t free_req = 0;                  // R28: time of this chain's pending cudaFree request
+        bool job = false, job_run = false;     // R29: a CPU job exists / it holds a core
+        bool cpu_chg = false, rerank_req = false;
+        int64_t job_rem = 0, job_ready = 0, run_start = 0, cpu_prio = 0;
         int64_t acc = 0;
         uint32_t batch_start = 0, sync_target = 0, sync_ord = 0;
         int64_t sync_cost = 0;
@@ -325,6 +329,11 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             int64_t rem = rem_g + rem_c;
             if (noise) rem = rem * (1000 + nz) / 1000;
             return t_arr + Dp - rem - t;
+        };
+        // R29: the thread is busy for d ns from t; with shared cores that is a CPU job
+        auto cpu_busy = [&](int64_t t, int64_t d) {
+            if (!cores_on || d == 0) { cpu_next = t + d; return; }
+            job = true; job_run = false; job_rem = d; job_ready = t; cpu_next = INF64; cpu_chg = true;
         };
         // R27 policy keys of this chain: EDF (t_arr + D', -), SJF (-, R), HRRN (t_arr, R),
         // LCUF (P', sum of kernel estimates); R = the remaining estimated work of Eq. 2
@@ -364,7 +373,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             ++done;
             head_end = INF64;
             if (launched > done) { head_ready = t; head_u = T.kern[kbase + done].util_permille; }
-            if (pc == PC_SYNC_WAIT && done >= sync_target) { pc = PC_SYNC_RET; cpu_next = t + sync_cost; }
+            if (pc == PC_SYNC_WAIT && done >= sync_target) { pc = PC_SYNC_RET; cpu_busy(t, sync_cost); }
         };
         // Phase C start of this lane's waiting head: non-preemptive, exact duration (R4, R19, R20)
         auto start_head = [&](int64_t t) {
@@ -380,6 +389,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         // Returns true if the lane's stream got a new head (Phase C must run).
         auto phase_b = [&](int64_t t, uint32_t urgent_m, uint32_t active_m, uint32_t busy_m) -> bool {
             bool newhead = false;
+            if (cores_on && job) { job = false; job_run = false; cpu_chg = true; }   // R29: the job completed
             for (uint32_t guard = 0;; ++guard) {
                 if (guard > (1u << 24)) {
                     if (atomicCAS((unsigned long long *)err, 0ull, (unsigned long long)ERR_GUARD) == 0ull) err[1] = s;
@@ -462,8 +472,9 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     if (!exited) {
                         const int64_t e = (int64_t)(((uint64_t)T.task[tbase + task].cpu_nominal_ns * Fc) >> 16);
                         if (ma) { ma_ring[task * P.ma_w + ma_cnt[task] % P.ma_w] = (uint32_t)e; ++ma_cnt[task]; }
+                        if (cores_on && urg) rerank_req = true;   // R29: a CPU segment starts
                         pc = PC_CPU_DONE;
-                        cpu_next = t + e;
+                        cpu_busy(t, e);
                         if (e > 0) break;
                     }
                 }
@@ -527,7 +538,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                         ++sync_ord;
                         if (done >= sync_target) {
                             pc = PC_SYNC_RET;
-                            cpu_next = t + sync_cost;
+                            cpu_busy(t, sync_cost);
                             if (sync_cost > 0) break;
                             continue;
                         }
@@ -582,7 +593,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                         }
                     }
                     pc = PC_ENQUEUE;
-                    cpu_next = t + busy_launch;
+                    cpu_busy(t, busy_launch);
                     if (busy_launch > 0) break;
                     continue;
                 }
@@ -701,6 +712,37 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                 dirty |= PK ? hany(nh) : __any_sync(FULL, nh);
             }
 
+
+            // R29: CPU cores -- re-rank UrgenGo's priorities when a CPU segment started, then
+            // give the cores to the first K runnable jobs by (priority, runnable since, chain)
+            if (cores_on) {
+                const bool rr = __any_sync(FULL, rerank_req);
+                rerank_req = false;
+                if (rr && urg && valid && pc != PC_ARRIVE && pc != PC_DONE) cpu_prio = urgency_key(laxity(t));
+                if (rr || __any_sync(FULL, cpu_chg)) {
+                    cpu_chg = false;
+                    const uint32_t jm = __ballot_sync(FULL, job);
+                    bool want = job;
+                    if ((uint32_t)__popc(jm) > P.cpu_cores) {
+                        const int64_t prio = KIND == K_STATIC ? -(int64_t)static_level : urg ? cpu_prio : 0;
+                        __syncwarp();   // Phase B's reads of the snapshot slots are done
+                        snapA[lane] = prio;
+                        snapB[lane] = job_ready;
+                        __syncwarp();
+                        uint32_t better = 0, mm = jm & ~(1u << lane);
+                        while (mm) {
+                            const int o = __ffs(mm) - 1;
+                            mm &= mm - 1;
+                            const int64_t po = snapA[o], ro = snapB[o];
+                            better += (po > prio || (po == prio && (ro < job_ready || (ro == job_ready && o < lane)))) ? 1u : 0u;
+                        }
+                        want = job && better < P.cpu_cores;
+                        __syncwarp();
+                    }
+                    if (want && !job_run) { job_run = true; run_start = t; cpu_next = t + job_rem; }
+                    else if (job && !want && job_run) { job_run = false; job_rem -= t - run_start; cpu_next = INF64; }
+                }
+            }
 
             // cudaFree barriers (R28): while a request is queued or served nothing starts;
             // the (request time, chain)-first request is served once no kernel runs

@@ -14,6 +14,8 @@ run through the same C-ABI call (``urg_simulate_batch``) on the current CUDA dev
                       and lowest-chain-utilisation-first policies (PAPER.md:782-784, fig:6_policy);
 * ``cudafree``     -- 0..4 tasks ending with cudaFree, a device-wide barrier (PAPER.md:907-911,
                       fig:15_vector_free; DESIGN.md R28);
+* ``cpu_cores``    -- the chains' threads on 1..8 shared CPU cores with the policy's SCHED_FIFO
+                      priorities (PAPER.md:386-399; DESIGN.md R29);
 * ``utilisation``  -- UrgenGo vs FIFO vs static priorities over an arrival-rate sweep
                       (BASELINE.json configs[2]; PAPER.md:679-683 fig:0_overall analogue).
 
@@ -43,6 +45,7 @@ class Point:
     batch: Batch
     num_prio: Optional[int] = None          # workload override (binding streams)
     frees: Optional[int] = None             # workload override: the first n tasks end with cudaFree (R28)
+    cores: Optional[int] = None             # workload override: CPU cores shared by the threads (R29)
 
 
 @dataclass
@@ -101,6 +104,14 @@ def cudafree(base: Policy, b: Batch, counts=(0, 1, 2, 3, 4)) -> List[Point]:
     return [Point(f"{n} cudaFree tasks, {name}", p, b, frees=n) for n in counts for name, p in pols]
 
 
+def cpu_cores(base: Policy, b: Batch, counts=(1, 2, 4, 8, 0)) -> List[Point]:
+    """PAPER.md:386-399 urgency-centric CPU scheduling: the chains' threads on 1..8 shared cores
+    (0 = one core per thread) under UrgenGo, static priorities and FIFO (R29)."""
+    pols = [("UrgenGo", base), ("static (PAAM-like)", Policy(kind=STATIC, flags=0, sync_mode=SYNC_ASYNC)),
+            ("FIFO", Policy(kind=FIFO, flags=0, sync_mode=SYNC_ASYNC))]
+    return [Point(f"{'unlimited' if n == 0 else n} cores, {name}", p, b, cores=n) for n in counts for name, p in pols]
+
+
 def with_frees(w: Workload, n: int) -> Workload:
     """A copy of w whose first n tasks (chain-major) end with cudaFree."""
     import copy
@@ -124,7 +135,7 @@ def utilisation(base: Policy, batches: List[Batch]) -> List[Point]:
     return out
 
 
-STUDIES = ("sync_modes", "delta_eval", "num_prio", "ablation", "collisions", "policies", "cudafree")
+STUDIES = ("sync_modes", "delta_eval", "num_prio", "ablation", "collisions", "policies", "cudafree", "cpu_cores")
 
 
 def run(w: Workload, points: List[Point], stream=None) -> List[Result]:
@@ -135,9 +146,9 @@ def run(w: Workload, points: List[Point], stream=None) -> List[Result]:
     try:
         for pt in points:
             npri = pt.num_prio if pt.num_prio is not None else w.num_prio
-            key = (npri, pt.frees)
+            key = (npri, pt.frees, pt.cores)
             if key not in cache:
-                ww = replace(w, num_prio=npri)
+                ww = replace(w, num_prio=npri, cpu_cores=pt.cores if pt.cores is not None else w.cpu_cores)
                 cache[key] = DeviceWorkload(with_frees(ww, pt.frees) if pt.frees is not None else ww)
             dw = cache[key]
             agg = torch.zeros(dw.agg_words, dtype=torch.int64, device="cuda")

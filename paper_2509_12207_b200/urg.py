@@ -45,7 +45,8 @@ class WorkloadDesc(ct.Structure):
                 ("launch_ns", ct.c_int64), ("launch_akb_ns", ct.c_int64),
                 ("sync_lo_ns", ct.c_int64), ("sync_hi_ns", ct.c_int64), ("jitter_ns", ct.c_int64),
                 ("inst_quantiles_q16", ct.c_void_p), ("kern_quantiles_q16", ct.c_void_p),
-                ("rt_bin_ns", ct.c_int64), ("rt_bins", ct.c_uint32), ("free_ns", ct.c_int64)]
+                ("rt_bin_ns", ct.c_int64), ("rt_bins", ct.c_uint32), ("free_ns", ct.c_int64),
+                ("cpu_cores", ct.c_uint32)]
 
 
 class PolicyS(ct.Structure):
@@ -156,7 +157,8 @@ class DeviceWorkload:
         kern = None if w.kern_quantiles_q16 is None else np.ascontiguousarray(w.kern_quantiles_q16, np.uint32)
         self.desc = WorkloadDesc(w.num_chains, chains, w.num_prio, w.launch_ns, w.launch_akb_ns, w.sync_lo_ns,
                                  w.sync_hi_ns, w.jitter_ns, None if inst is None else inst.ctypes.data,
-                                 None if kern is None else kern.ctypes.data, w.rt_bin_ns, w.rt_bins, w.free_ns)
+                                 None if kern is None else kern.ctypes.data, w.rt_bin_ns, w.rt_bins, w.free_ns,
+                                 w.cpu_cores)
         self._keep = (keep, chains, inst, kern)
         h = ct.c_void_p()
         _check(lib().urg_create_workload(ct.byref(self.desc), ct.byref(h)))

@@ -486,3 +486,34 @@ def test_packed_equals_unpacked_large_batch(monkeypatch):
     o = O.run(w, p, Batch(seed=b.seed, scenario_begin=5000, scenario_count=1, horizon_ns=b.horizon_ns,
                           ftight_permille=400))
     assert np.array_equal(o.records[0], r1[5000])
+
+
+def test_cpu_cores_fixtures():
+    from workloads import w7
+    for cores in (0, 1, 2):
+        for kind in (FIFO, STATIC, URGENGO, 4):
+            both(w7(cores), Policy(kind=kind, flags=0, sync_mode=SYNC_ASYNC, lax_threshold_ns=-1),
+                 Batch(horizon_ns=2 * MS), f"w7 cores={cores} kind={kind}")
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_cpu_cores_random(seed):
+    rng = random.Random(14000 + seed)
+    w = random_workload(rng, C=rng.choice([2, 4, 7, 13, 32]))
+    w.cpu_cores = rng.choice([1, 2, 3, 8])
+    p = random_policy(rng)
+    p.kind = rng.choice([FIFO, STATIC, URGENGO, URGENGO, 3, 5])
+    p.flags = rng.randint(0, 15) if p.kind == URGENGO else 0
+    if rng.random() < 0.3:
+        p.cpu_ma_window = 4
+    both(w, p, Batch(seed=seed, scenario_count=rng.randint(1, 16), horizon_ns=300 * MS), f"cores seed {seed}")
+
+
+@pytest.mark.parametrize("cores", [1, 2, 8])
+def test_cpu_cores_paper11(cores):
+    cfg = get_config("paper11")
+    w = cfg.workload()
+    w.cpu_cores = cores
+    b = Batch(seed=cfg.batch.seed, scenario_count=6, horizon_ns=2_000 * MS, ftight_permille=400)
+    for name in ("urgengo", "fifo", "static"):
+        both(w, cfg.policies[name], b, f"paper11 cores={cores} {name}")
