@@ -83,6 +83,9 @@ typedef struct {
     uint32_t cpu_cores;                   /* CPU cores shared by the chains' threads with the policy's
                                              SCHED_FIFO priorities (8; DESIGN.md
                                              R29); 0 = one core per thread, <= 32 */
+    uint32_t contention_permille;         /* alpha: a kernel started while U per-mille of the GPU runs
+                                             takes d + floor(d * alpha * U / 10^6) (
+                                             DESIGN.md R30); 0 = no slow-down */
 } urg_workload_desc;
 
 typedef struct urg_workload urg_workload; /* opaque; immutable after create; owns its device copy */

@@ -23,8 +23,9 @@ def main():
     cfg = get_config("paper11")
     b = replace(cfg.batch, scenario_count=1)          # scenario 0 of configs[1] (Q5)
     lth, n = O.calibrate(cfg.workload(), cfg.policies["urgengo"], b, window_ns=30_000_000_000)
-    out = {"paper11": lth, "_samples": {"paper11": n},
-           "_how": "python -m oracle.calibrate (PAPER.md:464-465, DESIGN.md Q5)"}
+    out = json.load(open(OUT)) if os.path.exists(OUT) else {}
+    out.update({"paper11": lth, "_samples": {"paper11": n},
+                "_how": "python -m oracle.calibrate (PAPER.md:464-465, DESIGN.md Q5)"})
     with open(OUT, "w") as f:
         json.dump(out, f, indent=1)
         f.write("\n")

@@ -54,6 +54,7 @@ typedef struct {
     uint32_t rt_bins;
     int64_t free_ns;            /* cudaFree cost once the device is idle (Table 5) */
     uint32_t cpu_cores;         /* CPU cores shared by the chains' threads, 0 = one per thread (R29) */
+    uint32_t contention_permille; /* alpha: kernel slow-down per unit of co-running utilisation (R30) */
     /* policy */
     uint32_t kind, flags, sync_mode;
     int64_t delta_eval_ns, lax_threshold_ns, sleep_ns;
@@ -820,9 +821,13 @@ static void dispatch(orc_sim *S, int64_t t)
         uint32_t K = L->q[L->q_head].K;
         uint32_t u = S->in->k_util[L->kbase + K];
         if (S->gpu_used + u > 1000) continue;            /* does not fit: skip (greedy) */
+        /* contention (R30): a kernel started while
+         * U_run per-mille of the GPU is busy runs d + floor(d * alpha * U_run / 10^6) */
+        int64_t d = kernel_duration(S, cand[j].chain, L->inst, K);
+        d += d * (int64_t)S->in->contention_permille * (int64_t)S->gpu_used / 1000000;
         S->gpu_used += u;
         L->head_running = 1;
-        L->head_end = t + kernel_duration(S, cand[j].chain, L->inst, K);
+        L->head_end = t + d;
         tr(S, t, TR_DISPATCH, cand[j].chain, L->inst, K, L->head_end);
     }
 }

@@ -41,6 +41,7 @@ struct urg_workload {
     bool has_free = false;            // some task ends with cudaFree (R28)
     int64_t free_ns = 0;
     uint32_t cpu_cores = 0;           // cores shared by the chains' threads, 0 = one each (R29)
+    uint32_t alpha_pm = 0;            // contention slow-down (R30)
 };
 
 static thread_local std::string g_err;
@@ -91,6 +92,7 @@ extern "C" urg_status urg_create_workload(const urg_workload_desc *d, urg_worklo
     if (d->rt_bins < 1 || d->rt_bins > (1u << 20)) return fail(URG_EINVAL, "rt_bins must be in 1..2^20");
     if (d->free_ns < 0 || d->free_ns >= (1LL << 40)) return fail(URG_EINVAL, "free_ns must be in [0, 2^40)");
     if (d->cpu_cores > 32) return fail(URG_EINVAL, "cpu_cores must be <= 32 (0 = one core per chain thread)");
+    if (d->contention_permille > 100000) return fail(URG_EINVAL, "contention_permille must be <= 100000");
 
     uint32_t n_tasks = 0, n_kern = 0;
     for (uint32_t c = 0; c < d->num_chains && d->chains; ++c)
@@ -150,6 +152,7 @@ extern "C" urg_status urg_create_workload(const urg_workload_desc *d, urg_worklo
     w->has_kern_q = d->kern_quantiles_q16 != nullptr;
     w->free_ns = d->free_ns;
     w->cpu_cores = d->cpu_cores;
+    w->alpha_pm = d->contention_permille;
     w->blob.assign(off, 0);
     memcpy(w->blob.data(), &h, sizeof h);
     UrgChainRec *chs = (UrgChainRec *)(w->blob.data() + h.off_chains);
@@ -252,7 +255,7 @@ static void fill_params(const urg_workload *w, const urg_policy *p, const urg_ba
     P.kind = p->kind; P.flags = p->flags; P.sync_mode = p->sync_mode; P.util_exempt = p->util_exempt_permille;
     P.delta_eval_ns = p->delta_eval_ns; P.lax_threshold_ns = p->lax_threshold_ns; P.sleep_ns = p->sleep_ns;
     P.noise_pm = p->noise_permille; P.ma_w = p->cpu_ma_window;
-    P.has_free = w->has_free ? 1u : 0u; P.free_ns = w->free_ns; P.cpu_cores = w->cpu_cores;
+    P.has_free = w->has_free ? 1u : 0u; P.free_ns = w->free_ns; P.cpu_cores = w->cpu_cores; P.alpha_pm = w->alpha_pm;
     P.seed = b->seed; P.scenario_begin = b->scenario_begin; P.scenario_count = b->scenario_count;
     P.horizon_ns = b->horizon_ns;
     P.fa_num = b->fa_num; P.fa_den = b->fa_den; P.fd_num = b->fd_num; P.fd_den = b->fd_den;
@@ -298,7 +301,7 @@ static urg_status prepare_launch(const urg_workload *w, const urg_policy *p, con
     fill_params(w, p, b, P);
     // the extended-model build only when the batch uses noise, the CPU predictor or cudaFree
     bool ext = (p->kind == URG_URGENGO && p->noise_permille) || (p->kind >= URG_URGENGO && p->cpu_ma_window) ||
-               w->has_free || w->cpu_cores > 0;
+               w->has_free || w->cpu_cores > 0 || w->alpha_pm > 0;
     if (const char *ee = getenv("URG_EXT")) ext = ext || atoi(ee) != 0;   // test hook: force the extended build
     // two scenarios per warp in the throughput core build when the chains fit a half warp
     bool pk = wide && !cal && !ext && w->num_chains <= 16;

@@ -54,7 +54,7 @@ struct UrgSimParams {
     // estimation noise (R25) and CPU moving-average predictor (R26)
     uint32_t noise_pm, ma_w, ma_max_tasks, ma_slot, ma_offset;
     // cudaFree barriers (R28), CPU cores (R29)
-    uint32_t has_free, cpu_cores;
+    uint32_t has_free, cpu_cores, alpha_pm;   // + R30 contention alpha (per-mille)
     int64_t free_ns;
     // TH_urgent calibration build only: sampling end, sample rows ([count] counts, then
     // [count][cal_cap] laxities)

@@ -191,6 +191,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
     const bool ma = EXT && akb_on && P.ma_w > 0;           // R26 (every policy that estimates remaining work)
     const bool has_free = EXT && P.has_free != 0;          // R28: some task ends with cudaFree
     const bool cores_on = EXT && P.cpu_cores > 0;          // R29: the chains' threads share P.cpu_cores cores
+    const bool contend = EXT && P.alpha_pm > 0;            // R30: co-running kernels slow a starting one down
     // R26 predictor state of this lane's chain in shared memory: [max_tasks][W] ring of
     // measured CPU durations, [max_tasks] counts, [max_tasks] this instance's estimates
     uint32_t *ma_ring = (uint32_t *)(sm + P.ma_offset) + (size_t)threadIdx.x * P.ma_slot;
@@ -376,11 +377,12 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             if (pc == PC_SYNC_WAIT && done >= sync_target) { pc = PC_SYNC_RET; cpu_busy(t, sync_cost); }
         };
         // Phase C start of this lane's waiting head: non-preemptive, exact duration (R4, R19, R20)
-        auto start_head = [&](int64_t t) {
+        auto start_head = [&](int64_t t, uint32_t u_run) {
             uint64_t G = 65536u;
             if (KQ) G = T.kern_q[rng_word(P.seed, s, URG_TAG_KERN, c, inst, done) >> 20];
             uint64_t d = ((((uint64_t)T.kern[kbase + done].nominal_ns * Fg) >> 16) * G) >> 16;
             d = d < 1 ? 1 : (d > 0xFFFFFFFFull ? 0xFFFFFFFFull : d);
+            if (contend) d += d * (uint64_t)P.alpha_pm * u_run / 1000000ull;   // R30
             head_util = head_u;
             head_end = t + (int64_t)d;
         };
@@ -787,8 +789,8 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                         if (fit) wl = (int)(ml & 31u);
                     }
                     const uint32_t uw = __shfl_sync(FULL, head_u, wl >= 0 ? wl : lane);
+                    if (lane == wl) { start_head(t, used); waiting = false; }
                     if (wl >= 0) used += uw;
-                    if (lane == wl) { start_head(t); waiting = false; }
                     if (!any_multi) break;   // each half started its only fitting head (others did not fit)
                 }
             } else if (!PK && dirty) {
@@ -809,8 +811,9 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                         const uint32_t ml = __reduce_min_sync(FULL, (in && hi == mh) ? (uint32_t)key : 0xFFFFFFFFu);
                         wl = (int)(ml & 31u);
                     }
+                    const uint32_t u_run = used;
                     used += __shfl_sync(FULL, head_u, wl);
-                    if (lane == wl) { start_head(t); waiting = false; }
+                    if (lane == wl) { start_head(t, u_run); waiting = false; }
                     if ((fit & (fit - 1)) == 0) break;   // the others did not fit before; `used` only grew
                 }
             }

@@ -16,6 +16,7 @@ run through the same C-ABI call (``urg_simulate_batch``) on the current CUDA dev
                       fig:15_vector_free; DESIGN.md R28);
 * ``cpu_cores``    -- the chains' threads on 1..8 shared CPU cores with the policy's SCHED_FIFO
                       priorities (PAPER.md:386-399; DESIGN.md R29);
+* ``contention``   -- kernel slow-down from co-running kernels (PAPER.md:209-212; DESIGN.md R30);
 * ``utilisation``  -- UrgenGo vs FIFO vs static priorities over an arrival-rate sweep
                       (BASELINE.json configs[2]; PAPER.md:679-683 fig:0_overall analogue).
 
@@ -46,6 +47,7 @@ class Point:
     num_prio: Optional[int] = None          # workload override (binding streams)
     frees: Optional[int] = None             # workload override: the first n tasks end with cudaFree (R28)
     cores: Optional[int] = None             # workload override: CPU cores shared by the threads (R29)
+    alpha: Optional[int] = None             # workload override: contention slow-down per-mille (R30)
 
 
 @dataclass
@@ -112,6 +114,14 @@ def cpu_cores(base: Policy, b: Batch, counts=(1, 2, 4, 8, 0)) -> List[Point]:
     return [Point(f"{'unlimited' if n == 0 else n} cores, {name}", p, b, cores=n) for n in counts for name, p in pols]
 
 
+def contention(base: Policy, b: Batch, alphas=(0, 250, 500, 1000, 2000)) -> List[Point]:
+    """PAPER.md:209-212 (fig:13_cdf): co-running kernels slow each other down; miss ratios of
+    UrgenGo, static priorities and FIFO as the slow-down alpha grows (R30)."""
+    pols = [("UrgenGo", base), ("static (PAAM-like)", Policy(kind=STATIC, flags=0, sync_mode=SYNC_ASYNC)),
+            ("FIFO", Policy(kind=FIFO, flags=0, sync_mode=SYNC_ASYNC))]
+    return [Point(f"alpha {a} permille, {name}", p, b, alpha=a) for a in alphas for name, p in pols]
+
+
 def with_frees(w: Workload, n: int) -> Workload:
     """A copy of w whose first n tasks (chain-major) end with cudaFree."""
     import copy
@@ -135,7 +145,8 @@ def utilisation(base: Policy, batches: List[Batch]) -> List[Point]:
     return out
 
 
-STUDIES = ("sync_modes", "delta_eval", "num_prio", "ablation", "collisions", "policies", "cudafree", "cpu_cores")
+STUDIES = ("sync_modes", "delta_eval", "num_prio", "ablation", "collisions", "policies", "cudafree", "cpu_cores",
+           "contention")
 
 
 def run(w: Workload, points: List[Point], stream=None) -> List[Result]:
@@ -146,9 +157,10 @@ def run(w: Workload, points: List[Point], stream=None) -> List[Result]:
     try:
         for pt in points:
             npri = pt.num_prio if pt.num_prio is not None else w.num_prio
-            key = (npri, pt.frees, pt.cores)
+            key = (npri, pt.frees, pt.cores, pt.alpha)
             if key not in cache:
-                ww = replace(w, num_prio=npri, cpu_cores=pt.cores if pt.cores is not None else w.cpu_cores)
+                ww = replace(w, num_prio=npri, cpu_cores=pt.cores if pt.cores is not None else w.cpu_cores,
+                             contention_permille=pt.alpha if pt.alpha is not None else w.contention_permille)
                 cache[key] = DeviceWorkload(with_frees(ww, pt.frees) if pt.frees is not None else ww)
             dw = cache[key]
             agg = torch.zeros(dw.agg_words, dtype=torch.int64, device="cuda")

@@ -517,3 +517,23 @@ def test_cpu_cores_paper11(cores):
     b = Batch(seed=cfg.batch.seed, scenario_count=6, horizon_ns=2_000 * MS, ftight_permille=400)
     for name in ("urgengo", "fifo", "static"):
         both(w, cfg.policies[name], b, f"paper11 cores={cores} {name}")
+
+
+def test_contention_fixtures_and_random():
+    """R30 contention slow-down: W8 hand-worked cases, random workloads, configs[1]."""
+    from workloads import w8
+    for alpha in (0, 600, 2000):
+        for kind in (FIFO, URGENGO):
+            both(w8(alpha), Policy(kind=kind, flags=0, sync_mode=SYNC_ASYNC, lax_threshold_ns=-1),
+                 Batch(horizon_ns=1 * MS), f"w8 alpha={alpha}")
+    rng = random.Random(15000)
+    for i in range(6):
+        w = random_workload(rng, C=rng.choice([2, 5, 11, 32]))
+        w.contention_permille = rng.choice([100, 600, 3000])
+        p = random_policy(rng)
+        both(w, p, Batch(seed=i, scenario_count=rng.randint(1, 12), horizon_ns=300 * MS), f"contention {i}")
+    cfg = get_config("paper11")
+    w = cfg.workload()
+    w.contention_permille = 500
+    both(w, cfg.policies["urgengo"], Batch(seed=cfg.batch.seed, scenario_count=6, horizon_ns=2_000 * MS,
+                                           ftight_permille=400), "paper11 contention")

@@ -328,3 +328,12 @@ def test_w7_cpu_cores(case):
     w = w7(case["cores"])
     r = O.run(w, Policy(kind=case["kind"], flags=0, sync_mode=SYNC_ASYNC, lax_threshold_ns=-1), Batch(horizon_ns=2 * MS))
     assert [_sum_rt(r.records[0][c]) for c in range(2)] == [int(round(x * MS)) for x in case["rt_ms"]]
+
+
+@pytest.mark.parametrize("case", _gold("w8.json")["cases"], ids=lambda c: str(c["alpha_permille"]))
+def test_w8_contention(case):
+    from workloads import w8
+    w = w8(case["alpha_permille"])
+    for kind in (FIFO, URGENGO):
+        r = O.run(w, Policy(kind=kind, flags=0, sync_mode=SYNC_ASYNC, lax_threshold_ns=-1), Batch(horizon_ns=1 * MS))
+        assert [_sum_rt(r.records[0][c]) for c in range(2)] == [int(round(x * MS)) for x in case["rt_ms"]]

@@ -541,3 +541,33 @@ def test_cpu_cores_invariants(seed):
             assert a == rem - (t - st) and a > 0
     assert len(running) <= K
     assert r.records[:, :, 0].sum() > 0
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_contention_durations_replayed(seed):
+    """R30: every kernel's run time is its contention-free duration d plus
+    floor(d * alpha * U_run / 10^6), U_run the utilisation already running at its start
+    (d taken from the alpha = 0 run of the same scenario: durations are keyed by chain,
+    instance and kernel, not by the schedule)."""
+    rng = random.Random(8000 + seed)
+    w = random_workload(rng, C=rng.randint(2, 6))
+    p = random_policy(rng)
+    b = Batch(seed=seed, scenario_count=1, horizon_ns=300 * MS)
+    base = O.run(w, p, b, trace_cap=400_000)
+    d0 = {(int(c), int(i), int(a)): int(bb) - int(t) for t, k, c, i, a, bb in base.trace if k == K["DISPATCH"]}
+    w.contention_permille = rng.choice([100, 600, 3000])
+    r = O.run(w, p, b, trace_cap=400_000)
+    util = {c: [k.util_permille for tk in ch.tasks for k in tk.kernels] for c, ch in enumerate(w.chains)}
+    running, checked = {}, 0
+    for t, k, c, i, a, bb in r.trace:
+        t, k, c, i, a, bb = int(t), int(k), int(c), int(i), int(a), int(bb)
+        if k == K["RETIRE"]:
+            running.pop((c, i, a))
+        elif k == K["DISPATCH"]:
+            u_run = sum(running.values())
+            if (c, i, a) in d0:
+                d = d0[(c, i, a)]
+                assert bb - t == d + d * w.contention_permille * u_run // 1_000_000
+                checked += 1
+            running[(c, i, a)] = util[c][a]
+    assert checked > 0

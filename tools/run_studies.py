@@ -33,6 +33,7 @@ studies = {
     "policies (PAPER.md:782-784)": SW.policies(base, b),
     "cudaFree (PAPER.md:907-911)": SW.cudafree(base, b),
     "CPU cores (PAPER.md:386-399)": SW.cpu_cores(base, b),
+    "contention (PAPER.md:209-212)": SW.contention(base, b),
 }
 cfg3 = get_config("usweep")
 studies["utilisation sweep (configs[2])"] = SW.utilisation(base, [replace(x, scenario_count=SU) for x in cfg3.sweep])

@@ -75,6 +75,7 @@ class Workload:
     rt_bins: int = 1024
     free_ns: int = 188 * US            # cudaFree cost on an idle device (Table 5; R28)
     cpu_cores: int = 0                 # cores shared by the chains' threads, 0 = one each (8; R29)
+    contention_permille: int = 0       # kernel slow-down per co-running utilisation (R30)
 
     @property
     def num_chains(self) -> int:

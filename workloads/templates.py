@@ -168,3 +168,30 @@ def w7(cores: int = 1) -> Workload:
     b = Chain(1000 * MS, 6 * MS, 1 * MS, [Task(2 * MS, 2 * MS, [Kernel(1 * MS, 1 * MS, 1000)])])
     return Workload(chains=[a, b], num_prio=2, launch_ns=0, launch_akb_ns=0, sync_lo_ns=0, sync_hi_ns=0,
                     jitter_ns=0, cpu_cores=cores)
+
+
+def w8(alpha_permille: int = 600) -> Workload:
+    """Fixture W8 (tests/golden/w8.json): kernel contention slow-down (R30)."""
+    a = Chain(1000 * MS, 100 * MS, 0, [Task(500 * US, 500 * US, [Kernel(4 * MS, 4 * MS, 500)])])
+    b = Chain(1000 * MS, 100 * MS, 0, [Task(1 * MS, 1 * MS, [Kernel(2 * MS, 2 * MS, 500)])])
+    return Workload(chains=[a, b], num_prio=2, launch_ns=0, launch_akb_ns=0, sync_lo_ns=0, sync_hi_ns=0,
+                    jitter_ns=0, contention_permille=alpha_permille)
+
+
+def contention_pair(co_run: bool = True, alpha_permille: int = 0, template_seed: int = 0x5EED0007) -> Workload:
+    """Fig. fig:13_cdf set-up: 2D detection (YOLOX, Table 4: 323 kernels,
+    19.8 ms) alone or sharing the GPU with 3D detection (PointPillars: 41 kernels, 13.4 ms).
+    Chain 0 = 2D detection with the tighter deadline (the higher static priority), 2 ms CPU
+    segment; chain 1 = 3D detection, 2 ms CPU segment; both every 50 ms with 15 ms jitter."""
+    rng = np.random.default_rng(template_seed)
+    util_vals = np.array([u for u, _ in UTIL_TABLE])
+    util_p = np.array([p for _, p in UTIL_TABLE])
+    chains = []
+    for name, dl in (("det2d", 60), ("det3d", 120)):
+        nk, egpu = TABLE4[name]
+        durs = synth_kernel_times(nk, _ns(egpu), rng)
+        utils = rng.choice(util_vals, size=nk, p=util_p)
+        ks = [Kernel(d, d, int(u)) for d, u in zip(durs, utils)]
+        chains.append(Chain(50 * MS, dl * MS, 0, [Task(2 * MS, 2 * MS, ks)]))
+    return Workload(chains=chains if co_run else chains[:1], num_prio=6, jitter_ns=15 * MS,
+                    contention_permille=alpha_permille)
