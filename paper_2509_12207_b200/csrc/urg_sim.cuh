@@ -612,15 +612,18 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             if (coll) {
                 busy_m = __ballot_sync(FULL, launched > done) & hmask;
                 active_m = __ballot_sync(FULL, akb > 0) & hmask;
+                __syncwarp();   // the previous phase's reads of the snapshot are done
                 snapL[lane] = L_last;
                 snapLev[lane] = level;
                 __syncwarp();
             } else if (f_bind && __any_sync(FULL, may_bind)) {
                 active_m = __ballot_sync(FULL, akb > 0) & hmask;
+                __syncwarp();
                 snapL[lane] = L_last;
                 __syncwarp();
             } else if (cls && __any_sync(FULL, may_bind)) {
                 active_m = __ballot_sync(FULL, akb > 0) & hmask;
+                __syncwarp();
                 snapA[lane] = cls_key_a();
                 snapB[lane] = cls_key_b();
                 __syncwarp();
