@@ -537,3 +537,34 @@ def test_contention_fixtures_and_random():
     w.contention_permille = 500
     both(w, cfg.policies["urgengo"], Batch(seed=cfg.batch.seed, scenario_count=6, horizon_ns=2_000 * MS,
                                            ftight_permille=400), "paper11 contention")
+
+
+@pytest.mark.parametrize("wpc", ["1", "3", "16"])
+def test_results_independent_of_geometry(wpc, monkeypatch):
+    """Dynamic scenario fetch: the warps-per-CTA geometry changes which warp simulates which
+    scenario, never the results (records keyed by global scenario index)."""
+    cfg = get_config("paper11")
+    w, p = cfg.workload(), cfg.policies["urgengo"]
+    b = Batch(seed=cfg.batch.seed, scenario_count=50, horizon_ns=1_000 * MS, ftight_permille=400)
+    ref_r, ref_a = gpu_run(w, p, b)
+    monkeypatch.setenv("URG_WARPS_PER_CTA", wpc)
+    r, a = gpu_run(w, p, b)
+    assert np.array_equal(r, ref_r) and np.array_equal(a, ref_a)
+
+
+def test_largest_template_that_fits():
+    """A template near the shared-memory budget (9000 kernel records, ~150 KB) in both builds."""
+    rng = random.Random(77)
+    tasks = [Task(rng.randint(0, 2 * MS), rng.randint(0, 2 * MS),
+                  [Kernel(rng.randint(1000, 300_000), rng.randint(1000, 300_000), rng.choice([100, 500, 1000]))
+                   for _ in range(900)]) for _ in range(10)]
+    w = Workload(chains=[Chain(400 * MS, 300 * MS, 0, tasks[:5]), Chain(500 * MS, 350 * MS, 0, tasks[5:])],
+                 num_prio=6, jitter_ns=0, rt_bins=2048)
+    p = Policy(kind=URGENGO, flags=7, sync_mode=SYNC_OVERLAP, lax_threshold_ns=5 * MS)
+    both(w, p, Batch(seed=3, scenario_count=5, horizon_ns=900 * MS), "big template")
+    import os as _os
+    _os.environ["URG_WIDE"] = "1"
+    try:
+        both(w, p, Batch(seed=3, scenario_count=5, horizon_ns=900 * MS), "big template wide")
+    finally:
+        del _os.environ["URG_WIDE"]

@@ -79,3 +79,23 @@ def test_cudafree_needs_positive_cost(L):
     w.free_ns = 0
     e = _create(w)
     assert e.status == -1 and "free_ns must be > 0" in str(e)
+
+
+def test_template_over_shared_memory_budget(L):
+    """A template larger than the shared-memory budget is refused with URG_ERANGE before any
+    device work (SURVEY.md §8(b) 'template larger than the smem budget -> URG_ERANGE')."""
+    ks = [Kernel(1000, 1000, 500)] * 10_500          # 10.5k kernel records x 16 B > 160 KB
+    w = Workload(chains=[Chain(100_000_000, 50_000_000, 0, [Task(1000, 1000, ks)])])
+    e = _create(w)
+    assert e.status == -2 and "shared memory" in str(e)
+
+
+def test_header_documents_every_entry_point():
+    """Each entry point declared in include/urg.h has a comment block citing the paper or the
+    design document (argument meaning, layout, ownership and errors live there)."""
+    src = open(os.path.join(ROOT, "include", "urg.h")).read()
+    for sym in declared_symbols():
+        i = src.index(sym + "(")
+        block = src[max(0, i - 1500):i]
+        assert "/*" in block, sym
+    assert src.count("PAPER.md") >= 10
