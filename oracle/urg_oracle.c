@@ -1010,7 +1010,7 @@ static int sim_scenario(const orc_input *in, uint64_t s, uint32_t *rec, int64_t 
         for (uint32_t c = 0; c < S.C; ++c) {
             S.snap_L[c] = S.lane[c].L_last; S.snap_n[c] = S.lane[c].akb_n;
             S.snap_level[c] = S.lane[c].level; S.snap_busy[c] = S.lane[c].q_head < S.lane[c].q_tail;
-            S.snap_tarr[c] = S.lane[c].t_arr; S.snap_R[c] = remaining_work(&S, c);
+            if (classical(&S)) { S.snap_tarr[c] = S.lane[c].t_arr; S.snap_R[c] = remaining_work(&S, c); }
         }
         for (uint32_t c = 0; c < S.C; ++c)                               /* Phase B */
             if (S.lane[c].cpu_next == t) {

@@ -16,3 +16,8 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:urg_
     -o gpurun_out/prof_$TAG python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-throughput > gpurun_out/ncu_full_$TAG.log 2>&1
 timeout 600 python tools/measure_next.py $TAG > gpurun_out/next_$TAG.log 2>&1; cp profiles/${TAG}_next.json gpurun_out/ 2>/dev/null
 tail -2 gpurun_out/pytest_$TAG.log; cat gpurun_out/smoke_$TAG.log; cut -c1-300 gpurun_out/bench_$TAG.json
+# throughput regime: one --set full capture of the packed (two scenarios per warp) kernel
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:urg_sim_kernel -s 1 -c 1 \
+    -o gpurun_out/prof_pk_$TAG python bench.py --config scaleout --scenarios 40000 --steps 1 --warmup 1 \
+    --no-cpu-baseline --no-throughput > gpurun_out/ncu_pk_$TAG.log 2>&1
+timeout 600 bash scripts/sanitize.sh > gpurun_out/sanitize_$TAG.log 2>&1
