@@ -43,7 +43,7 @@ class OrcInput(ct.Structure):
         ("ch_period", ct.c_void_p), ("ch_deadline", ct.c_void_p), ("ch_offset", ct.c_void_p),
         ("ch_ntasks", ct.c_void_p), ("ch_cpu_sigma", ct.c_void_p), ("ch_gpu_sigma", ct.c_void_p),
         ("t_cpu_nom", ct.c_void_p), ("t_cpu_est", ct.c_void_p), ("t_nk", ct.c_void_p), ("t_flags", ct.c_void_p),
-        ("k_nom", ct.c_void_p), ("k_est", ct.c_void_p), ("k_util", ct.c_void_p),
+        ("k_nom", ct.c_void_p), ("k_est", ct.c_void_p), ("k_util", ct.c_void_p), ("k_flags", ct.c_void_p),
         ("num_prio", ct.c_uint32),
         ("launch_ns", ct.c_int64), ("launch_akb_ns", ct.c_int64), ("sync_lo_ns", ct.c_int64),
         ("sync_hi_ns", ct.c_int64), ("jitter_ns", ct.c_int64),
@@ -108,7 +108,7 @@ def _make_input(w: Workload, p: Policy, b: Batch):
         ch_period=_ptr(f["ch_period"]), ch_deadline=_ptr(f["ch_deadline"]), ch_offset=_ptr(f["ch_offset"]),
         ch_ntasks=_ptr(f["ch_ntasks"]), ch_cpu_sigma=_ptr(f["ch_cpu_sigma"]), ch_gpu_sigma=_ptr(f["ch_gpu_sigma"]),
         t_cpu_nom=_ptr(f["t_cpu_nom"]), t_cpu_est=_ptr(f["t_cpu_est"]), t_nk=_ptr(f["t_nk"]), t_flags=_ptr(f["t_flags"]),
-        k_nom=_ptr(f["k_nom"]), k_est=_ptr(f["k_est"]), k_util=_ptr(f["k_util"]),
+        k_nom=_ptr(f["k_nom"]), k_est=_ptr(f["k_est"]), k_util=_ptr(f["k_util"]), k_flags=_ptr(f["k_flags"]),
         num_prio=w.num_prio, launch_ns=w.launch_ns, launch_akb_ns=w.launch_akb_ns,
         sync_lo_ns=w.sync_lo_ns, sync_hi_ns=w.sync_hi_ns, jitter_ns=w.jitter_ns,
         inst_q16=_ptr(inst), kern_q16=_ptr(kern), rt_bin_ns=w.rt_bin_ns, rt_bins=w.rt_bins, free_ns=w.free_ns,

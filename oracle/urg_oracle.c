@@ -46,6 +46,7 @@ typedef struct {
     const uint32_t *t_flags;                        /* bit 0: the task ends with cudaFree (R28) */
     const uint32_t *k_nom, *k_est;                  /* all kernels, chain-major */
     const uint16_t *k_util;
+    const uint16_t *k_flags;        /* bit 0: the operation is a memcpy on the copy engine (R31) */
     uint32_t num_prio;
     int64_t launch_ns, launch_akb_ns, sync_lo_ns, sync_hi_ns, jitter_ns;
     const int32_t *inst_q16;    /* 4096 z quantiles or NULL */
@@ -284,6 +285,7 @@ typedef struct {
     int64_t *agg;
     int64_t steps, launches, t_prev;
     int cpu_dirty, rerank;          /* R29: the runnable set / the priorities changed in this step */
+    int copy_busy;                  /* R31: the copy engine runs a memcpy */
     /* calibration sampling */
     int64_t cal_next, cal_end;
     int64_t *cal_L; int64_t cal_n, cal_cap;
@@ -804,14 +806,38 @@ static int barrier(orc_sim *S, int64_t t)
     return 1;
 }
 
+static int is_copy(const orc_sim *S, uint32_t c, uint32_t K)
+{
+    return S->in->k_flags && (S->in->k_flags[S->lane[c].kbase + K] & 1u);
+}
+
 static void dispatch(orc_sim *S, int64_t t)
 {
     orc_cand cand[64];
     uint32_t n = 0;
     if (barrier(S, t)) return;
+    /* the copy engine (Table 3 "cuMemCpy: no stream priority"; SPEC.md:271;
+     * DESIGN.md R31): one memcpy at a time, the waiting memcpy heads in (ready time, chain)
+     * order, independent of the compute capacity */
+    if (!S->copy_busy) {
+        int32_t best = -1;
+        for (uint32_t c = 0; c < S->C; ++c) {
+            const orc_lane *L = &S->lane[c];
+            if (!(L->q_head < L->q_tail && !L->head_running && is_copy(S, c, L->q[L->q_head].K))) continue;
+            if (best < 0 || L->head_ready < S->lane[best].head_ready) best = (int32_t)c;
+        }
+        if (best >= 0) {
+            orc_lane *L = &S->lane[best];
+            uint32_t K = L->q[L->q_head].K;
+            S->copy_busy = 1;
+            L->head_running = 1;
+            L->head_end = t + kernel_duration(S, (uint32_t)best, L->inst, K);
+            tr(S, t, TR_DISPATCH, best, L->inst, K, L->head_end);
+        }
+    }
     for (uint32_t c = 0; c < S->C; ++c) {
         orc_lane *L = &S->lane[c];
-        if (L->q_head < L->q_tail && !L->head_running) {
+        if (L->q_head < L->q_tail && !L->head_running && !is_copy(S, c, L->q[L->q_head].K)) {
             cand[n].level = L->level; cand[n].ready = L->head_ready; cand[n].chain = c; ++n;
         }
     }
@@ -839,7 +865,8 @@ static void retire(orc_sim *S, int64_t t)
         orc_lane *L = &S->lane[c];
         if (!(L->q_head < L->q_tail && L->head_running && L->head_end == t)) continue;
         uint32_t K = L->q[L->q_head].K;
-        S->gpu_used -= S->in->k_util[L->kbase + K];
+        if (is_copy(S, c, K)) S->copy_busy = 0;          /* R31 */
+        else S->gpu_used -= S->in->k_util[L->kbase + K];
         L->q_head++; L->done++; L->head_running = 0;
         if (L->q_head < L->q_tail) L->head_ready = t;    /* next kernel becomes head */
         tr(S, t, TR_RETIRE, c, L->inst, K, 0);

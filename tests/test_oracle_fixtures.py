@@ -337,3 +337,12 @@ def test_w8_contention(case):
     for kind in (FIFO, URGENGO):
         r = O.run(w, Policy(kind=kind, flags=0, sync_mode=SYNC_ASYNC, lax_threshold_ns=-1), Batch(horizon_ns=1 * MS))
         assert [_sum_rt(r.records[0][c]) for c in range(2)] == [int(round(x * MS)) for x in case["rt_ms"]]
+
+
+@pytest.mark.parametrize("case", _gold("w9.json")["cases"], ids=lambda c: str(c["copies"]))
+def test_w9_copy_engine(case):
+    from workloads import w9
+    w = w9(case["copies"])
+    for kind in (FIFO, URGENGO):
+        r = O.run(w, Policy(kind=kind, flags=0, sync_mode=SYNC_ASYNC, lax_threshold_ns=-1), Batch(horizon_ns=1 * MS))
+        assert [_sum_rt(r.records[0][c]) for c in range(2)] == [int(round(x * MS)) for x in case["rt_ms"]]

