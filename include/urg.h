@@ -32,15 +32,19 @@ typedef enum {
     URG_EINTERNAL = -5   /* the kernel tripped an internal invariant (see urg_check) */
 } urg_status;
 
-/* One GPU kernel of a task: its lookup-table record (Table 1).
+/* One GPU operation of a task: a kernel's lookup-table record (Table 1)
+ * or a memcpy (flags bit 0).
  * nominal_ns: execution time before per-scenario factors (> 0);
  * estimate_ns: ~E^gpu_k used in Eq. 2; util_permille: U_k in [0, 1000]. */
 typedef struct {
     uint32_t nominal_ns;
     uint32_t estimate_ns;
     uint16_t util_permille;
-    uint16_t flags;            /* reserved, must be 0 */
+    uint16_t flags;            /* bit 0 (URG_OP_MEMCPY): runs on the copy engine, one at a time, no
+                                  stream priority, no compute capacity (Table 3, PAPER.md:374;
+                                  DESIGN.md R31); other bits must be 0 */
 } urg_kernel_desc;
+enum { URG_OP_MEMCPY = 1 };
 
 /* One task: a CPU segment, then num_kernels (>= 1) kernels launched in order on
  * one stream, then a final stream synchronisation. */

@@ -42,6 +42,7 @@ struct urg_workload {
     int64_t free_ns = 0;
     uint32_t cpu_cores = 0;           // cores shared by the chains' threads, 0 = one each (R29)
     uint32_t alpha_pm = 0;            // contention slow-down (R30)
+    bool has_copy = false;            // some operation is a memcpy (R31)
 };
 
 static thread_local std::string g_err;
@@ -119,8 +120,8 @@ extern "C" urg_status urg_create_workload(const urg_workload_desc *d, urg_worklo
                     return fail(URG_EINVAL, "chains[%u].tasks[%u].kernels[%u].nominal_ns must be > 0", c, j, k);
                 if (kd.util_permille > 1000)
                     return fail(URG_EINVAL, "chains[%u].tasks[%u].kernels[%u].util_permille must be <= 1000", c, j, k);
-                if (kd.flags != 0)
-                    return fail(URG_EINVAL, "chains[%u].tasks[%u].kernels[%u].flags must be 0", c, j, k);
+                if (kd.flags > 1)
+                    return fail(URG_EINVAL, "chains[%u].tasks[%u].kernels[%u].flags has unknown bits", c, j, k);
             }
             n_kern += t.num_kernels;
         }
@@ -171,8 +172,11 @@ extern "C" urg_status urg_create_workload(const urg_workload_desc *d, urg_worklo
             tks[tb + j] = UrgTaskRec{t.cpu_nominal_ns, t.cpu_estimate_ns, t.num_kernels, t.flags};
             if (t.flags & 1u) w->has_free = true;
             for (uint32_t k = 0; k < t.num_kernels; ++k)
+            {
                 krs[kb + local + k] = UrgKernRec{t.kernels[k].nominal_ns, t.kernels[k].estimate_ns,
-                                                 t.kernels[k].util_permille, 0};
+                                                 t.kernels[k].util_permille, t.kernels[k].flags};
+                if (t.kernels[k].flags & 1u) w->has_copy = true;
+            }
             local += t.num_kernels;
         }
         r.num_kernels = local;
@@ -256,6 +260,7 @@ static void fill_params(const urg_workload *w, const urg_policy *p, const urg_ba
     P.delta_eval_ns = p->delta_eval_ns; P.lax_threshold_ns = p->lax_threshold_ns; P.sleep_ns = p->sleep_ns;
     P.noise_pm = p->noise_permille; P.ma_w = p->cpu_ma_window;
     P.has_free = w->has_free ? 1u : 0u; P.free_ns = w->free_ns; P.cpu_cores = w->cpu_cores; P.alpha_pm = w->alpha_pm;
+    P.has_copy = w->has_copy ? 1u : 0u;
     P.seed = b->seed; P.scenario_begin = b->scenario_begin; P.scenario_count = b->scenario_count;
     P.horizon_ns = b->horizon_ns;
     P.fa_num = b->fa_num; P.fa_den = b->fa_den; P.fd_num = b->fd_num; P.fd_den = b->fd_den;
@@ -301,7 +306,7 @@ static urg_status prepare_launch(const urg_workload *w, const urg_policy *p, con
     fill_params(w, p, b, P);
     // the extended-model build only when the batch uses noise, the CPU predictor or cudaFree
     bool ext = (p->kind == URG_URGENGO && p->noise_permille) || (p->kind >= URG_URGENGO && p->cpu_ma_window) ||
-               w->has_free || w->cpu_cores > 0 || w->alpha_pm > 0;
+               w->has_free || w->cpu_cores > 0 || w->alpha_pm > 0 || w->has_copy;
     if (const char *ee = getenv("URG_EXT")) ext = ext || atoi(ee) != 0;   // test hook: force the extended build
     // two scenarios per warp in the throughput core build when the chains fit a half warp
     bool pk = wide && !cal && !ext && w->num_chains <= 16;

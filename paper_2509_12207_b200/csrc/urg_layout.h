@@ -28,7 +28,7 @@ struct __align__(16) UrgTaskRec {      // 16 B
 };
 
 struct __align__(16) UrgKernRec {      // 16 B: one LDS.128 per access
-    uint32_t nominal_ns, estimate_ns, util_permille, reserved;
+    uint32_t nominal_ns, estimate_ns, util_permille, flags;   // flags bit 0: memcpy (R31)
 };
 
 struct __align__(16) UrgBlobHeader {   // 64 B
@@ -55,6 +55,7 @@ struct UrgSimParams {
     uint32_t noise_pm, ma_w, ma_max_tasks, ma_slot, ma_offset;
     // cudaFree barriers (R28), CPU cores (R29)
     uint32_t has_free, cpu_cores, alpha_pm;   // + R30 contention alpha (per-mille)
+    uint32_t has_copy;                        // R31: some operation is a memcpy
     int64_t free_ns;
     // TH_urgent calibration build only: sampling end, sample rows ([count] counts, then
     // [count][cal_cap] laxities)

@@ -192,6 +192,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
     const bool has_free = EXT && P.has_free != 0;          // R28: some task ends with cudaFree
     const bool cores_on = EXT && P.cpu_cores > 0;          // R29: the chains' threads share P.cpu_cores cores
     const bool contend = EXT && P.alpha_pm > 0;            // R30: co-running kernels slow a starting one down
+    const bool has_copy = EXT && P.has_copy != 0;          // R31: memcpy operations on the copy engine
     // R26 predictor state of this lane's chain in shared memory: [max_tasks][W] ring of
     // measured CPU durations, [max_tasks] counts, [max_tasks] this instance's estimates
     uint32_t *ma_ring = (uint32_t *)(sm + P.ma_offset) + (size_t)threadIdx.x * P.ma_slot;
@@ -309,6 +310,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         int64_t head_ready = 0;                // time the waiting head became head (R20 key)
         uint32_t head_util = 0;                // util of the running kernel
         uint32_t head_u = 0xFFFFu;             // util of the waiting head (valid while one waits)
+        bool head_copy = false;                // R31: the head is a memcpy (copy engine)
         uint32_t n_total = 0, n_miss = 0, n_early = 0, n_unfin = 0, n_launch = 0, hash = 2166136261u;
         uint64_t sum_rt = 0;
 
@@ -373,7 +375,11 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         auto retire = [&](int64_t t) {
             ++done;
             head_end = INF64;
-            if (launched > done) { head_ready = t; head_u = T.kern[kbase + done].util_permille; }
+            if (launched > done) {
+                head_ready = t;
+                head_u = T.kern[kbase + done].util_permille;
+                if (has_copy) head_copy = T.kern[kbase + done].flags & 1u;
+            }
             if (pc == PC_SYNC_WAIT && done >= sync_target) { pc = PC_SYNC_RET; cpu_busy(t, sync_cost); }
         };
         // Phase C start of this lane's waiting head: non-preemptive, exact duration (R4, R19, R20)
@@ -382,8 +388,8 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             if (KQ) G = T.kern_q[rng_word(P.seed, s, URG_TAG_KERN, c, inst, done) >> 20];
             uint64_t d = ((((uint64_t)T.kern[kbase + done].nominal_ns * Fg) >> 16) * G) >> 16;
             d = d < 1 ? 1 : (d > 0xFFFFFFFFull ? 0xFFFFFFFFull : d);
-            if (contend) d += d * (uint64_t)P.alpha_pm * u_run / 1000000ull;   // R30
-            head_util = head_u;
+            if (contend && !head_copy) d += d * (uint64_t)P.alpha_pm * u_run / 1000000ull;   // R30
+            head_util = head_copy ? 0u : head_u;   // a memcpy uses the copy engine, not the SMs (R31)
             head_end = t + (int64_t)d;
         };
         // Phase B: this lane's CPU program at t, until it has to wait for time to pass.
@@ -494,7 +500,10 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     const uint32_t n = launched;
                     const UrgKernRec kr = T.kern[kbase + n];
                     const int64_t est = kr.estimate_ns;
-                    if (launched == done) { head_ready = t; head_u = kr.util_permille; newhead = true; }   // stream was empty
+                    if (launched == done) {   // stream was empty: head now
+                        head_ready = t; head_u = kr.util_permille; newhead = true;
+                        if (has_copy) head_copy = kr.flags & 1u;
+                    }
                     ++launched; ++n_launch;
                     rem_g -= est;
                     if (akb_on) ++akb;
@@ -801,6 +810,15 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                 ++st_dispatch;
 #endif
                 bool waiting = launched > done && head_end == INF64;
+                if (has_copy) {   // R31: the copy engine runs one memcpy at a time, (ready, chain) first
+                    const bool cw = waiting && head_copy;
+                    if (__any_sync(FULL, cw) && !__any_sync(FULL, head_end != INF64 && head_copy)) {
+                        const int64_t mr = warp_min_nonneg(cw ? head_ready : INF64);
+                        const int wl = __ffs(__ballot_sync(FULL, cw && head_ready == mr)) - 1;
+                        if (lane == wl) start_head(t, used);
+                    }
+                    waiting = waiting && !head_copy;   // memcpys never take compute capacity
+                }
                 for (;;) {
                     const uint32_t fit = __ballot_sync(FULL, waiting && used + head_u <= 1000u);
                     if (!fit) break;

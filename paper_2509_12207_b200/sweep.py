@@ -17,6 +17,7 @@ run through the same C-ABI call (``urg_simulate_batch``) on the current CUDA dev
 * ``cpu_cores``    -- the chains' threads on 1..8 shared CPU cores with the policy's SCHED_FIFO
                       priorities (PAPER.md:386-399; DESIGN.md R29);
 * ``contention``   -- kernel slow-down from co-running kernels (PAPER.md:209-212; DESIGN.md R30);
+* ``memcpy``       -- H2D/D2H memcpys around every task on the copy engine (Table 3; DESIGN.md R31);
 * ``utilisation``  -- UrgenGo vs FIFO vs static priorities over an arrival-rate sweep
                       (BASELINE.json configs[2]; PAPER.md:679-683 fig:0_overall analogue).
 
@@ -48,6 +49,7 @@ class Point:
     frees: Optional[int] = None             # workload override: the first n tasks end with cudaFree (R28)
     cores: Optional[int] = None             # workload override: CPU cores shared by the threads (R29)
     alpha: Optional[int] = None             # workload override: contention slow-down per-mille (R30)
+    copies: bool = False                    # workload override: H2D/D2H memcpys around every task (R31)
 
 
 @dataclass
@@ -122,6 +124,26 @@ def contention(base: Policy, b: Batch, alphas=(0, 250, 500, 1000, 2000)) -> List
     return [Point(f"alpha {a} permille, {name}", p, b, alpha=a) for a in alphas for name, p in pols]
 
 
+def memcpy(base: Policy, b: Batch) -> List[Point]:
+    """Table 3: every task starts with a 0.3 ms H2D memcpy and ends with a 0.1 ms
+    D2H memcpy on the copy engine (R31), against the same workload without copies."""
+    pols = [("UrgenGo", base), ("static (PAAM-like)", Policy(kind=STATIC, flags=0, sync_mode=SYNC_ASYNC)),
+            ("FIFO", Policy(kind=FIFO, flags=0, sync_mode=SYNC_ASYNC))]
+    return [Point(f"{'with' if cp else 'no'} memcpys, {name}", p, b, copies=cp) for cp in (False, True)
+            for name, p in pols]
+
+
+def with_copies(w: Workload, h2d_ns: int = 300_000, d2h_ns: int = 100_000) -> Workload:
+    """A copy of w whose tasks start with an H2D and end with a D2H memcpy (R31)."""
+    import copy
+    from workloads.spec import Kernel
+    w2 = copy.deepcopy(w)
+    for ch in w2.chains:
+        for t in ch.tasks:
+            t.kernels = [Kernel(h2d_ns, h2d_ns, 200, 1)] + t.kernels + [Kernel(d2h_ns, d2h_ns, 200, 1)]
+    return w2
+
+
 def with_frees(w: Workload, n: int) -> Workload:
     """A copy of w whose first n tasks (chain-major) end with cudaFree."""
     import copy
@@ -146,7 +168,7 @@ def utilisation(base: Policy, batches: List[Batch]) -> List[Point]:
 
 
 STUDIES = ("sync_modes", "delta_eval", "num_prio", "ablation", "collisions", "policies", "cudafree", "cpu_cores",
-           "contention")
+           "contention", "memcpy")
 
 
 def run(w: Workload, points: List[Point], stream=None) -> List[Result]:
@@ -157,10 +179,12 @@ def run(w: Workload, points: List[Point], stream=None) -> List[Result]:
     try:
         for pt in points:
             npri = pt.num_prio if pt.num_prio is not None else w.num_prio
-            key = (npri, pt.frees, pt.cores, pt.alpha)
+            key = (npri, pt.frees, pt.cores, pt.alpha, pt.copies)
             if key not in cache:
                 ww = replace(w, num_prio=npri, cpu_cores=pt.cores if pt.cores is not None else w.cpu_cores,
                              contention_permille=pt.alpha if pt.alpha is not None else w.contention_permille)
+                if pt.copies:
+                    ww = with_copies(ww)
                 cache[key] = DeviceWorkload(with_frees(ww, pt.frees) if pt.frees is not None else ww)
             dw = cache[key]
             agg = torch.zeros(dw.agg_words, dtype=torch.int64, device="cuda")

@@ -568,3 +568,40 @@ def test_largest_template_that_fits():
         both(w, p, Batch(seed=3, scenario_count=5, horizon_ns=900 * MS), "big template wide")
     finally:
         del _os.environ["URG_WIDE"]
+
+
+def _with_copies(w, h2d_ns=300 * US, d2h_ns=100 * US):
+    """Every task starts with an H2D memcpy and ends with a D2H memcpy (R31)."""
+    import copy as _copy
+    w2 = _copy.deepcopy(w)
+    for ch in w2.chains:
+        for t in ch.tasks:
+            t.kernels = [Kernel(h2d_ns, h2d_ns, 200, 1)] + t.kernels + [Kernel(d2h_ns, d2h_ns, 200, 1)]
+    return w2
+
+
+def test_copy_engine():
+    """R31 memcpy on the copy engine: W9, random workloads, configs[1] with H2D/D2H copies,
+    also together with cudaFree and shared CPU cores."""
+    from workloads import w9
+    for copies in (True, False):
+        for kind in (FIFO, STATIC, URGENGO, 5):
+            both(w9(copies), Policy(kind=kind, flags=0, sync_mode=SYNC_ASYNC, lax_threshold_ns=-1),
+                 Batch(horizon_ns=1 * MS), f"w9 {copies} {kind}")
+    rng = random.Random(16000)
+    for i in range(6):
+        w = random_workload(rng, C=rng.choice([2, 5, 11, 32]))
+        for ch in w.chains:
+            for t in ch.tasks:
+                for k in t.kernels:
+                    k.flags = 1 if rng.random() < 0.3 else 0
+        p = random_policy(rng)
+        both(w, p, Batch(seed=i, scenario_count=rng.randint(1, 12), horizon_ns=300 * MS), f"copies {i}")
+    cfg = get_config("paper11")
+    w = _with_copies(cfg.workload())
+    b = Batch(seed=cfg.batch.seed, scenario_count=6, horizon_ns=2_000 * MS, ftight_permille=400)
+    for name in ("urgengo", "fifo"):
+        both(w, cfg.policies[name], b, f"paper11 copies {name}")
+    w.cpu_cores = 2
+    w.chains[0].tasks[0].frees = True
+    both(w, cfg.policies["urgengo"], b, "paper11 copies + cores + free")
