@@ -319,8 +319,9 @@ def main():
     clocks = clk.summary()
 
     # ---- e2e: the public API with HOST buffers, template upload included, every step ----
-    host_agg = np.zeros(dw.agg_words, np.int64)
-    host_rec = np.zeros((S, w.num_chains, RECORD_WORDS), np.uint32)
+    # pinned host buffers: the step's device->host result copies are DMA from/to page-locked memory
+    host_agg = torch.zeros(dw.agg_words, dtype=torch.int64, pin_memory=True).numpy()
+    host_rec = torch.zeros((S, w.num_chains, RECORD_WORDS), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
     L = lib()
     ps, bs = policy_struct(p), batch_struct(b)
     o = OutputsS(host_rec.ctypes.data, host_agg.ctypes.data)
