@@ -346,3 +346,15 @@ def test_w9_copy_engine(case):
     for kind in (FIFO, URGENGO):
         r = O.run(w, Policy(kind=kind, flags=0, sync_mode=SYNC_ASYNC, lax_threshold_ns=-1), Batch(horizon_ns=1 * MS))
         assert [_sum_rt(r.records[0][c]) for c in range(2)] == [int(round(x * MS)) for x in case["rt_ms"]]
+
+
+def test_toy2_fifo_first_dispatches():
+    """configs[0] (toy2) under FIFO: the first eight dispatches match the hand derivation."""
+    from workloads import get_config, toy2
+    g = _gold("toy2_fifo_first_dispatches.json")
+    cfg = get_config("toy2")
+    r = O.run(toy2(), cfg.policies["fifo"], cfg.batch, trace_cap=100_000)
+    got = [[int(c), int(i), int(a), int(t), int(b)] for t, k, c, i, a, b in r.trace
+           if k == O.TRACE_CODES["DISPATCH"]][:8]
+    want = [[c, i, k, int(round(s * MS)), int(round(e * MS))] for c, i, k, s, e in g["dispatches"]]
+    assert got == want
