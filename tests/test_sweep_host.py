@@ -29,3 +29,23 @@ def test_policy_study_kinds():
     cfg = get_config("paper11")
     kinds = [p.policy.kind for p in SW.policies(cfg.policies["urgengo"], cfg.batch)]
     assert kinds == [2, 0, 1, 3, 4, 5, 6]
+
+
+def test_workload_transforms():
+    """sweep's workload transforms change exactly what their study varies."""
+    from paper_2509_12207_b200 import sweep as SW
+    w = get_config("paper11").workload()
+    f2 = SW.with_frees(w, 2)
+    flags = [t.frees for ch in f2.chains for t in ch.tasks]
+    assert flags[:2] == [True, True] and not any(flags[2:])
+    assert not any(t.frees for ch in w.chains for t in ch.tasks)          # the original is untouched
+    cp = SW.with_copies(w)
+    for ch0, ch1 in zip(w.chains, cp.chains):
+        for t0, t1 in zip(ch0.tasks, ch1.tasks):
+            assert len(t1.kernels) == len(t0.kernels) + 2
+            assert t1.kernels[0].flags == 1 and t1.kernels[-1].flags == 1
+            assert [k.nominal_ns for k in t1.kernels[1:-1]] == [k.nominal_ns for k in t0.kernels]
+    pts = SW.cpu_cores(get_config("paper11").policies["urgengo"], get_config("paper11").batch)
+    assert sorted({p.cores for p in pts}) == [0, 1, 2, 4, 8]
+    assert sorted({p.alpha for p in SW.contention(get_config("paper11").policies["urgengo"],
+                                                   get_config("paper11").batch)}) == [0, 250, 500, 1000, 2000]
