@@ -24,7 +24,8 @@ _LIB = os.path.join(_HERE, "liburg_oracle.so")
 TRACE_KINDS = {1: "STEP", 2: "INST_START", 3: "TASK_START", 4: "EVAL", 5: "DELAY", 6: "BIND", 7: "ENQUEUE",
                8: "DISPATCH", 9: "RETIRE", 10: "SYNC_CALL", 11: "SYNC_RET", 12: "FREE_CLOSE",
                13: "INST_DONE", 14: "EARLY_EXIT", 15: "COLLISION", 16: "FREE_CALL", 17: "FREE_START",
-               18: "FREE_RET", 19: "CPU_RUN", 20: "CPU_STOP"}
+               18: "FREE_RET", 19: "CPU_RUN", 20: "CPU_STOP",
+               21: "PUBLISH", 22: "TAKE"}
 TRACE_CODES = {v: k for k, v in TRACE_KINDS.items()}
 
 
@@ -49,7 +50,7 @@ class OrcInput(ct.Structure):
         ("sync_hi_ns", ct.c_int64), ("jitter_ns", ct.c_int64),
         ("inst_q16", ct.c_void_p), ("kern_q16", ct.c_void_p),
         ("rt_bin_ns", ct.c_int64), ("rt_bins", ct.c_uint32), ("free_ns", ct.c_int64), ("cpu_cores", ct.c_uint32),
-        ("contention_permille", ct.c_uint32),
+        ("contention_permille", ct.c_uint32), ("task_exec", ct.c_uint32),
         ("kind", ct.c_uint32), ("flags", ct.c_uint32), ("sync_mode", ct.c_uint32),
         ("delta_eval_ns", ct.c_int64), ("lax_threshold_ns", ct.c_int64), ("sleep_ns", ct.c_int64),
         ("util_exempt_permille", ct.c_uint32),
@@ -112,7 +113,7 @@ def _make_input(w: Workload, p: Policy, b: Batch):
         num_prio=w.num_prio, launch_ns=w.launch_ns, launch_akb_ns=w.launch_akb_ns,
         sync_lo_ns=w.sync_lo_ns, sync_hi_ns=w.sync_hi_ns, jitter_ns=w.jitter_ns,
         inst_q16=_ptr(inst), kern_q16=_ptr(kern), rt_bin_ns=w.rt_bin_ns, rt_bins=w.rt_bins, free_ns=w.free_ns,
-        cpu_cores=w.cpu_cores, contention_permille=w.contention_permille,
+        cpu_cores=w.cpu_cores, contention_permille=w.contention_permille, task_exec=w.executors,
         kind=p.kind, flags=p.flags, sync_mode=p.sync_mode, delta_eval_ns=p.delta_eval_ns,
         lax_threshold_ns=p.lax_threshold_ns, sleep_ns=p.sleep_ns, util_exempt_permille=p.util_exempt_permille,
         noise_permille=p.noise_permille, cpu_ma_window=p.cpu_ma_window,

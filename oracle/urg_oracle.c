@@ -56,6 +56,7 @@ typedef struct {
     int64_t free_ns;            /* cudaFree cost once the device is idle (Table 5) */
     uint32_t cpu_cores;         /* CPU cores shared by the chains' threads, 0 = one per thread (R29) */
     uint32_t contention_permille; /* alpha: kernel slow-down per unit of co-running utilisation (R30) */
+    uint32_t task_exec;         /* 1: one executor thread per task, hand-over by message (R32) */
     /* policy */
     uint32_t kind, flags, sync_mode;
     int64_t delta_eval_ns, lax_threshold_ns, sleep_ns;
@@ -76,7 +77,8 @@ enum { TAG_ARR = 1, TAG_TIGHT = 2, TAG_INST = 3, TAG_KERN = 4, TAG_SYNC = 5, TAG
 /* trace kinds */
 enum { TR_STEP = 1, TR_INST_START, TR_TASK_START, TR_EVAL, TR_DELAY, TR_BIND, TR_ENQUEUE,
        TR_DISPATCH, TR_RETIRE, TR_SYNC_CALL, TR_SYNC_RET, TR_FREE_CLOSE, TR_INST_DONE,
-       TR_EARLY_EXIT, TR_COLLISION, TR_FREE_CALL, TR_FREE_START, TR_FREE_RET, TR_CPU_RUN, TR_CPU_STOP };
+       TR_EARLY_EXIT, TR_COLLISION, TR_FREE_CALL, TR_FREE_START, TR_FREE_RET, TR_CPU_RUN, TR_CPU_STOP,
+       TR_PUBLISH, TR_TAKE };
 
 #define REC_WORDS 8
 #define AGG_COUNTERS 5
@@ -221,10 +223,14 @@ typedef struct {            /* one AKB entry */
 typedef struct { uint32_t K; int64_t t_enq; } orc_stream_entry;
 
 enum { PC_ARRIVE = 0, PC_CPU_DONE, PC_ATTEMPT, PC_ENQUEUE, PC_SYNC_WAIT, PC_SYNC_RET, PC_FREE_WAIT, PC_FREE_RET,
-       PC_DONE };
+       PC_WAIT_MSG, PC_DONE };
 
 typedef struct {
     /* static per scenario */
+    uint32_t chain;                 /* the chain this thread serves (randomness, records) */
+    uint32_t stage, stage_end;      /* tasks [stage, stage_end) of every instance it runs: the whole
+                                       chain (R6), or one task under per-task executors (R32) */
+    uint32_t k0;                    /* kernels of the chain's tasks before `stage` */
     int64_t Pp, Dp;                 /* P', D' (R3) */
     uint32_t static_level;
     uint32_t N, M;                  /* kernels and tasks (= CPU segments) per instance */
@@ -262,6 +268,10 @@ typedef struct {
     int job, job_run;               /* a job exists / it holds a core */
     int64_t job_rem, job_ready, run_start;
     int64_t cpu_prio;               /* SCHED_FIFO priority key: higher runs first */
+    /* per-task executors (R32): the subscription's latest undelivered / delivered message
+     * (instance index + 1, 0 = none) and, on the chain's last stage, the next instance to record */
+    uint32_t msg_pend, msg;
+    uint32_t expect;
     /* results */
     uint32_t total, miss, early, unfin, launches, hash;
     uint64_t sum_rt;
@@ -270,7 +280,8 @@ typedef struct {
 typedef struct {
     const orc_input *in;
     uint64_t s;
-    uint32_t C;
+    uint32_t C;                     /* chains (records, aggregates) */
+    uint32_t nL;                    /* threads: C, or one per task under per-task executors (R32) */
     orc_lane *lane;
     uint32_t gpu_used;              /* sum of running utilisations, <= 1000 */
     int64_t H, H_stop;
@@ -304,17 +315,18 @@ static uint32_t hash_fold(uint32_t h, uint32_t x) { return (h ^ x) * 16777619u; 
 static int64_t arrival(const orc_sim *S, uint32_t c, uint32_t i)
 {
     const orc_input *in = S->in;
+    const uint32_t ch = S->lane[c].chain;
     int64_t jit = 0;
     if (in->jitter_ns > 0)
-        jit = (int64_t)(orc_word(in->seed, S->s, TAG_ARR, c, i, 0) % (uint64_t)(in->jitter_ns + 1));
-    return in->ch_offset[c] + (int64_t)i * S->lane[c].Pp + jit;
+        jit = (int64_t)(orc_word(in->seed, S->s, TAG_ARR, ch, i, 0) % (uint64_t)(in->jitter_ns + 1));
+    return in->ch_offset[ch] + (int64_t)i * S->lane[c].Pp + jit;
 }
 
-static uint32_t inst_factor(const orc_sim *S, uint32_t c, uint32_t i, uint32_t which, uint32_t sigma_ppm)
+static uint32_t inst_factor(const orc_sim *S, uint32_t ch, uint32_t i, uint32_t which, uint32_t sigma_ppm)
 {
     const orc_input *in = S->in;
     if (!in->inst_q16) return 65536u;
-    int64_t z = in->inst_q16[orc_word(in->seed, S->s, TAG_INST, c, i, which) >> 20];
+    int64_t z = in->inst_q16[orc_word(in->seed, S->s, TAG_INST, ch, i, which) >> 20];
     int64_t F = 65536 + (z * (int64_t)sigma_ppm) / 1000000;   /* C division truncates toward 0 */
     if (F < 6554) F = 6554;                                    /* factor floor 0.1 (R4) */
     return (uint32_t)F;
@@ -325,7 +337,7 @@ static int64_t kernel_duration(const orc_sim *S, uint32_t c, uint32_t i, uint32_
     const orc_input *in = S->in;
     const orc_lane *L = &S->lane[c];
     uint64_t G = 65536u;
-    if (in->kern_q16) G = in->kern_q16[orc_word(in->seed, S->s, TAG_KERN, c, i, k) >> 20];
+    if (in->kern_q16) G = in->kern_q16[orc_word(in->seed, S->s, TAG_KERN, L->chain, i, k) >> 20];
     uint64_t d = (((uint64_t)in->k_nom[L->kbase + k] * L->Fg) >> 16) * G >> 16;
     if (d < 1) d = 1;
     if (d > 0xFFFFFFFFull) d = 0xFFFFFFFFull;
@@ -343,7 +355,7 @@ static int64_t sync_cost(const orc_sim *S, uint32_t c, uint32_t i, uint32_t ord)
     const orc_input *in = S->in;
     if (in->sync_hi_ns <= in->sync_lo_ns) return in->sync_lo_ns;
     uint64_t span = (uint64_t)(in->sync_hi_ns - in->sync_lo_ns + 1);
-    return in->sync_lo_ns + (int64_t)(orc_word(in->seed, S->s, TAG_SYNC, c, i, ord) % span);
+    return in->sync_lo_ns + (int64_t)(orc_word(in->seed, S->s, TAG_SYNC, S->lane[c].chain, i, ord) % span);
 }
 
 /* ---- urgency evaluation trigger (R8): Eq. 2 + AKB refresh ---- */
@@ -356,7 +368,7 @@ static int64_t noisy_laxity(const orc_sim *S, uint32_t c, int64_t t_arr, int64_t
     const orc_input *in = S->in;
     const orc_lane *L = &S->lane[c];
     if (in->noise_permille == 0) return lax;
-    uint32_t w = orc_word(in->seed, S->s, TAG_NOISE, c, L->inst, L->task);
+    uint32_t w = orc_word(in->seed, S->s, TAG_NOISE, L->chain, L->inst, L->task);
     int64_t n = (int64_t)(w % (2 * in->noise_permille + 1)) - (int64_t)in->noise_permille;
     int64_t remaining = t_arr + D - t - lax;           /* sum of the remaining estimates (>= 0) */
     return t_arr + D - (remaining * (1000 + n)) / 1000 - t;
@@ -432,7 +444,7 @@ static int should_delay(const orc_sim *S, uint32_t c, uint32_t util, int64_t own
     const orc_input *in = S->in;
     if (util < in->util_exempt_permille) return 0;
     if (orc_is_urgent(own_L, in->lax_threshold_ns)) return 0;
-    for (uint32_t o = 0; o < S->C; ++o) {
+    for (uint32_t o = 0; o < S->nL; ++o) {
         if (o == c) continue;
         for (uint32_t e = 0; e < S->snap_n[o]; ++e)   /* every active kernel of chain o */
             if (orc_is_urgent(S->snap_L[o], in->lax_threshold_ns)) return 1;
@@ -472,7 +484,7 @@ static uint32_t bind_level(orc_sim *S, uint32_t c, int64_t own_L, int64_t t)
          * normalised like UrgenGo's non-urgent ranks (R15) */
         orc_cl_item it[64];
         uint32_t n = 0;
-        for (uint32_t o = 0; o < S->C; ++o) {
+        for (uint32_t o = 0; o < S->nL; ++o) {
             if (o != c && S->snap_n[o] == 0) continue;
             orc_cl_item *x = &it[n++];
             const orc_lane *L = &S->lane[o];
@@ -493,7 +505,7 @@ static uint32_t bind_level(orc_sim *S, uint32_t c, int64_t own_L, int64_t t)
     if (orc_is_urgent(own_L, in->lax_threshold_ns)) return 0;
     int64_t keys[64]; uint32_t chains[64], ranks[64], n = 0;
     keys[n] = orc_urgency_key(own_L); chains[n] = c; ++n;
-    for (uint32_t o = 0; o < S->C; ++o)
+    for (uint32_t o = 0; o < S->nL; ++o)
         if (o != c && S->snap_n[o] > 0) { keys[n] = orc_urgency_key(S->snap_L[o]); chains[n] = o; ++n; }
     orc_rank(keys, chains, n, ranks);
     return orc_normalise_level(ranks[0], n, in->num_prio);
@@ -516,8 +528,29 @@ static void record_outcome(orc_sim *S, uint32_t c, int64_t t, int early)
     L->hash = hash_fold(hash_fold(L->hash, (uint32_t)rt), (uint32_t)((uint64_t)rt >> 32));
     int64_t bin = rt / in->rt_bin_ns;
     if (bin > (int64_t)in->rt_bins - 1) bin = in->rt_bins - 1;
-    S->agg[(int64_t)c * (AGG_COUNTERS + in->rt_bins + RATIO_BINS) + AGG_COUNTERS + bin] += 1;
+    S->agg[(int64_t)L->chain * (AGG_COUNTERS + in->rt_bins + RATIO_BINS) + AGG_COUNTERS + bin] += 1;
     tr(S, t, TR_INST_DONE, c, L->inst, rt, late);
+}
+
+/* Per-task executors (R32; "each task is executed by a dedicated
+ * thread"): the thread of stage j > 0 takes the message naming instance i.  On the chain's
+ * last stage, instances the message sequence skipped -- exited early at an earlier stage, or
+ * overwritten in a full subscription queue of depth 1 -- are recorded now, in order, as
+ * misses (the early-exit marker in the hash). */
+static void take_message(orc_sim *S, uint32_t c, int64_t t)
+{
+    orc_lane *L = &S->lane[c];
+    uint32_t i = L->msg - 1;
+    L->msg = 0;
+    if (L->stage_end == L->M)
+        for (; L->expect < i; ++L->expect) {
+            L->miss++;
+            L->hash = hash_fold(hash_fold(L->hash, 0xFFFFFFFFu), 0xFFFFFFFFu);
+        }
+    L->inst = i;
+    L->t_arr = arrival(S, c, i);
+    L->pc = PC_ARRIVE; L->cpu_next = t;
+    tr(S, t, TR_TAKE, c, i, 0, 0);
 }
 
 /* Start of the instance L->inst at time t (frame arrival, or the end of the
@@ -525,10 +558,12 @@ static void record_outcome(orc_sim *S, uint32_t c, int64_t t, int early)
 static void start_instance(orc_sim *S, uint32_t c, int64_t t)
 {
     orc_lane *L = &S->lane[c];
-    L->total++;
-    L->Fg = inst_factor(S, c, L->inst, 0, S->in->ch_gpu_sigma[c]);
-    L->Fc = inst_factor(S, c, L->inst, 1, S->in->ch_cpu_sigma[c]);
-    L->task = 0; L->launched = 0; L->cpu_idx = 0; L->done = 0; L->sync_ord = 0;
+    if (!S->in->task_exec) L->total++;
+    L->Fg = inst_factor(S, L->chain, L->inst, 0, S->in->ch_gpu_sigma[L->chain]);
+    L->Fc = inst_factor(S, L->chain, L->inst, 1, S->in->ch_cpu_sigma[L->chain]);
+    /* the thread's first task of the instance; I~gpu / I~cpu count over the whole instance */
+    L->task = L->stage; L->launched = L->k0; L->cpu_idx = L->stage; L->done = L->k0;
+    L->sync_ord = L->stage << 16;               /* per-task executors: sync draws keyed per task (R32) */
     L->q_head = L->q_tail = 0;
     /* ~E^cpu_j for this instance ("moving averages across recent instances";
      * DESIGN.md R26): mean of the last min(W, h_j) measured durations of task j, floor;
@@ -545,10 +580,16 @@ static void start_instance(orc_sim *S, uint32_t c, int64_t t)
     tr(S, t, TR_INST_START, c, L->inst, L->t_arr, 0);
 }
 
-/* the chain moves on to instance inst+1 at time t; returns 1 if it starts now */
+/* the chain moves on to instance inst+1 at time t; returns 1 if it starts now.  A per-task
+ * executor of stage j > 0 takes the delivered message instead, or waits for one (R32). */
 static int next_instance(orc_sim *S, uint32_t c, int64_t t)
 {
     orc_lane *L = &S->lane[c];
+    if (L->stage > 0) {
+        if (L->msg) { take_message(S, c, t); return 1; }
+        L->pc = PC_WAIT_MSG; L->cpu_next = ORC_INF;
+        return 0;
+    }
     L->inst++;
     L->t_arr = arrival(S, c, L->inst);
     if (L->t_arr >= S->H) { L->pc = PC_DONE; L->cpu_next = ORC_INF; return 0; }   /* not admitted (R7) */
@@ -591,7 +632,7 @@ static void count_collision(orc_sim *S, uint32_t c, int64_t t)
     if (!orc_is_urgent(L->L_last, in->lax_threshold_ns)) return;
     int64_t own = orc_urgency_key(L->L_last);
     uint32_t k = 0;
-    for (uint32_t o = 0; o < S->C; ++o) {
+    for (uint32_t o = 0; o < S->nL; ++o) {
         if (o == c || !S->snap_busy[o]) continue;
         if (S->snap_level[o] <= L->level && orc_urgency_key(S->snap_L[o]) < own) ++k;
     }
@@ -641,7 +682,8 @@ static void lane_step(orc_sim *S, uint32_t c, int64_t t)
                 int64_t lax = evaluate(S, c, t);
                 if (flag(S, ORC_EARLY_EXIT) && lax < 0) {
                     L->akb_n = 0;                          /* purge the chain's AKB entries */
-                    record_outcome(S, c, t, 1);
+                    if (L->stage_end == L->M) { record_outcome(S, c, t, 1); L->expect = L->inst + 1; }
+                    else { L->early++; tr(S, t, TR_EARLY_EXIT, c, L->inst, 0, 0); }   /* no message (R32) */
                     if (next_instance(S, c, t)) continue;
                     return;
                 }
@@ -755,10 +797,22 @@ static void lane_step(orc_sim *S, uint32_t c, int64_t t)
             tr(S, t, TR_FREE_RET, c, L->inst, L->task, 0);
             goto task_done;
         }
+        case PC_WAIT_MSG: {                              /* a message was delivered (R32) */
+            take_message(S, c, t);
+            continue;
+        }
         task_done: {
             L->task++;
-            if (L->task < L->M) goto task_start;
-            record_outcome(S, c, t, 0);                  /* instance complete (R18) */
+            if (L->task < L->stage_end) goto task_start;
+            if (L->stage_end < L->M) {
+                /* per-task executors: publish to the next task's subscription, depth 1 -- an
+                 * undelivered older message is replaced (R32) */
+                S->lane[c + 1].msg_pend = L->inst + 1;
+                tr(S, t, TR_PUBLISH, c, L->inst, 0, 0);
+            } else {
+                record_outcome(S, c, t, 0);              /* instance complete (R18) */
+                L->expect = L->inst + 1;
+            }
             if (next_instance(S, c, t)) continue;
             return;
         }
@@ -788,7 +842,7 @@ static int barrier(orc_sim *S, int64_t t)
 {
     int queued = 0, serving = 0, running = 0;
     int32_t head = -1;
-    for (uint32_t c = 0; c < S->C; ++c) {
+    for (uint32_t c = 0; c < S->nL; ++c) {
         const orc_lane *L = &S->lane[c];
         if (L->pc == PC_FREE_RET) serving = 1;
         if (L->pc == PC_FREE_WAIT) {
@@ -821,7 +875,7 @@ static void dispatch(orc_sim *S, int64_t t)
      * order, independent of the compute capacity */
     if (!S->copy_busy) {
         int32_t best = -1;
-        for (uint32_t c = 0; c < S->C; ++c) {
+        for (uint32_t c = 0; c < S->nL; ++c) {
             const orc_lane *L = &S->lane[c];
             if (!(L->q_head < L->q_tail && !L->head_running && is_copy(S, c, L->q[L->q_head].K))) continue;
             if (best < 0 || L->head_ready < S->lane[best].head_ready) best = (int32_t)c;
@@ -835,7 +889,7 @@ static void dispatch(orc_sim *S, int64_t t)
             tr(S, t, TR_DISPATCH, best, L->inst, K, L->head_end);
         }
     }
-    for (uint32_t c = 0; c < S->C; ++c) {
+    for (uint32_t c = 0; c < S->nL; ++c) {
         orc_lane *L = &S->lane[c];
         if (L->q_head < L->q_tail && !L->head_running && !is_copy(S, c, L->q[L->q_head].K)) {
             cand[n].level = L->level; cand[n].ready = L->head_ready; cand[n].chain = c; ++n;
@@ -861,7 +915,7 @@ static void dispatch(orc_sim *S, int64_t t)
 /* Phase A: retire every kernel ending at t (R21). */
 static void retire(orc_sim *S, int64_t t)
 {
-    for (uint32_t c = 0; c < S->C; ++c) {
+    for (uint32_t c = 0; c < S->nL; ++c) {
         orc_lane *L = &S->lane[c];
         if (!(L->q_head < L->q_tail && L->head_running && L->head_end == t)) continue;
         uint32_t K = L->q[L->q_head].K;
@@ -900,9 +954,9 @@ static void cpu_schedule(orc_sim *S, int64_t t)
     if (in->cpu_cores == 0) return;
     if (S->rerank) {
         S->rerank = 0;
-        for (uint32_t c = 0; c < S->C; ++c) {
+        for (uint32_t c = 0; c < S->nL; ++c) {
             orc_lane *L = &S->lane[c];
-            if (L->pc == PC_ARRIVE || L->pc == PC_DONE) continue;   /* not active */
+            if (L->pc == PC_ARRIVE || L->pc == PC_WAIT_MSG || L->pc == PC_DONE) continue;   /* not active */
             L->cpu_prio = orc_urgency_key(current_laxity(S, c, t));
         }
         S->cpu_dirty = 1;
@@ -911,7 +965,7 @@ static void cpu_schedule(orc_sim *S, int64_t t)
     S->cpu_dirty = 0;
     orc_job jobs[64];
     uint32_t n = 0;
-    for (uint32_t c = 0; c < S->C; ++c) {
+    for (uint32_t c = 0; c < S->nL; ++c) {
         const orc_lane *L = &S->lane[c];
         if (!L->job) continue;
         jobs[n].prio = in->kind == ORC_STATIC ? -(int64_t)L->static_level : in->kind == ORC_URGENGO ? L->cpu_prio : 0;
@@ -934,7 +988,7 @@ static void cal_sample(orc_sim *S)
 {
     /* highest urgency among all active kernels of the AKB */
     int have = 0; int64_t best = 0, bestL = 0;
-    for (uint32_t c = 0; c < S->C; ++c) {
+    for (uint32_t c = 0; c < S->nL; ++c) {
         orc_lane *L = &S->lane[c];
         for (uint32_t e = 0; e < L->akb_n; ++e) {
             int64_t k = orc_urgency_key(L->akb[e].L);
@@ -957,26 +1011,34 @@ static int sim_scenario(const orc_input *in, uint64_t s, uint32_t *rec, int64_t 
     S.cal_L = cal_L; S.cal_cap = cal_cap; S.cal_n = 0; S.cal_end = cal_end; S.cal_next = 0;
     S.t_prev = -1;
     int rc = 0;
-    S.lane = calloc(S.C, sizeof(orc_lane));
-    S.snap_L = calloc(S.C, sizeof(int64_t));
-    S.snap_n = calloc(S.C, sizeof(uint32_t));
-    S.snap_level = calloc(S.C, sizeof(uint32_t));
-    S.snap_busy = calloc(S.C, sizeof(uint8_t));
-    S.snap_tarr = calloc(S.C, sizeof(int64_t));
-    S.snap_R = calloc(S.C, sizeof(int64_t));
-    uint32_t kb = 0, tb = 0;
-    for (uint32_t c = 0; c < S.C; ++c) {
-        orc_lane *L = &S.lane[c];
-        L->tbase = tb; L->kbase = kb; L->M = in->ch_ntasks[c]; L->N = 0;
-        for (uint32_t j = 0; j < L->M; ++j) L->N += in->t_nk[tb + j];
-        tb += L->M; kb += L->N;
-        L->akb = calloc(L->N, sizeof(orc_akb_entry));
-        L->cpu_hist = calloc((size_t)L->M * (in->cpu_ma_window ? in->cpu_ma_window : 1), sizeof(uint32_t));
-        L->cpu_hist_n = calloc(L->M, sizeof(uint32_t));
-        L->cpu_pred = calloc(L->M, sizeof(uint32_t));
-        for (uint32_t j = 0; j < L->M; ++j) L->cpu_pred[j] = in->t_cpu_est[L->tbase + j];
-        L->q = calloc(L->N, sizeof(orc_stream_entry));
-        L->hash = 2166136261u;
+    /* threads: one per chain (R6), or one per task, chain-major (per-task executors, R32) */
+    S.nL = S.C;
+    if (in->task_exec) { S.nL = 0; for (uint32_t c = 0; c < S.C; ++c) S.nL += in->ch_ntasks[c]; }
+    S.lane = calloc(S.nL, sizeof(orc_lane));
+    S.snap_L = calloc(S.nL, sizeof(int64_t));
+    S.snap_n = calloc(S.nL, sizeof(uint32_t));
+    S.snap_level = calloc(S.nL, sizeof(uint32_t));
+    S.snap_busy = calloc(S.nL, sizeof(uint8_t));
+    S.snap_tarr = calloc(S.nL, sizeof(int64_t));
+    S.snap_R = calloc(S.nL, sizeof(int64_t));
+    uint32_t kb = 0, tb = 0, nl = 0;
+    for (uint32_t ch = 0; ch < S.C; ++ch) {
+        uint32_t M = in->ch_ntasks[ch], N = 0, k0 = 0;
+        for (uint32_t j = 0; j < M; ++j) N += in->t_nk[tb + j];
+        for (uint32_t j = 0; j < (in->task_exec ? M : 1); ++j) {
+            orc_lane *L = &S.lane[nl++];
+            L->chain = ch; L->tbase = tb; L->kbase = kb; L->M = M; L->N = N;
+            L->stage = in->task_exec ? j : 0; L->stage_end = in->task_exec ? j + 1 : M; L->k0 = k0;
+            k0 += in->t_nk[tb + j];
+            L->akb = calloc(L->N, sizeof(orc_akb_entry));
+            L->cpu_hist = calloc((size_t)L->M * (in->cpu_ma_window ? in->cpu_ma_window : 1), sizeof(uint32_t));
+            L->cpu_hist_n = calloc(L->M, sizeof(uint32_t));
+            L->cpu_pred = calloc(L->M, sizeof(uint32_t));
+            for (uint32_t q = 0; q < L->M; ++q) L->cpu_pred[q] = in->t_cpu_est[L->tbase + q];
+            L->q = calloc(L->N, sizeof(orc_stream_entry));
+            L->hash = 2166136261u;
+        }
+        tb += M; kb += N;
     }
     /* scenario factors (R3): P' = P / f_a, D' = D * f_d, tight set halved */
     uint32_t tight = 0;
@@ -993,34 +1055,38 @@ static int sim_scenario(const orc_input *in, uint64_t s, uint32_t *rec, int64_t 
         }
     }
     int64_t maxD = 0;
-    for (uint32_t c = 0; c < S.C; ++c) {
+    int64_t *chD = calloc(S.C, sizeof(int64_t));
+    for (uint32_t c = 0; c < S.nL; ++c) {
         orc_lane *L = &S.lane[c];
-        L->Pp = in->ch_period[c] * (int64_t)in->fa_den / (int64_t)in->fa_num;
-        L->Dp = in->ch_deadline[c] * (int64_t)in->fd_num / (int64_t)in->fd_den;
-        if (tight & (1u << c)) L->Dp /= 2;
+        L->Pp = in->ch_period[L->chain] * (int64_t)in->fa_den / (int64_t)in->fa_num;
+        L->Dp = in->ch_deadline[L->chain] * (int64_t)in->fd_num / (int64_t)in->fd_den;
+        if (tight & (1u << L->chain)) L->Dp /= 2;
         if (L->Dp > maxD) maxD = L->Dp;
+        chD[L->chain] = L->Dp;
     }
-    /* STATIC (PAAM-like) levels: rank by D' ascending, ties by chain id (R15) */
-    for (uint32_t c = 0; c < S.C; ++c) {
-        uint32_t r = 1;
+    /* STATIC (PAAM-like) levels: rank the chains by D' ascending, ties by chain id (R15) */
+    for (uint32_t c = 0; c < S.nL; ++c) {
+        uint32_t r = 1, ch = S.lane[c].chain;
         for (uint32_t o = 0; o < S.C; ++o)
-            if (S.lane[o].Dp < S.lane[c].Dp || (S.lane[o].Dp == S.lane[c].Dp && o < c)) ++r;
+            if (chD[o] < chD[ch] || (chD[o] == chD[ch] && o < ch)) ++r;
         S.lane[c].static_level = (S.C <= 1 || in->num_prio <= 1) ? 0
             : (uint32_t)(((uint64_t)(r - 1) * (in->num_prio - 1)) / (S.C - 1));
     }
+    free(chD);
     S.H = in->horizon_ns;
     S.H_stop = S.H + maxD;                               /* R7 */
-    for (uint32_t c = 0; c < S.C; ++c) {
+    for (uint32_t c = 0; c < S.nL; ++c) {
         orc_lane *L = &S.lane[c];
         L->inst = 0;
         L->t_arr = arrival(&S, c, 0);
-        if (L->t_arr < S.H) { L->pc = PC_ARRIVE; L->cpu_next = L->t_arr; }
+        if (L->stage > 0) { L->pc = PC_WAIT_MSG; L->cpu_next = ORC_INF; }   /* R32: waits for a message */
+        else if (L->t_arr < S.H) { L->pc = PC_ARRIVE; L->cpu_next = L->t_arr; }
         else { L->pc = PC_DONE; L->cpu_next = ORC_INF; }
     }
     /* main loop (R21) */
     for (;;) {
         int64_t t = ORC_INF;
-        for (uint32_t c = 0; c < S.C; ++c) {
+        for (uint32_t c = 0; c < S.nL; ++c) {
             orc_lane *L = &S.lane[c];
             if (L->cpu_next < t) t = L->cpu_next;
             if (L->q_head < L->q_tail && L->head_running && L->head_end < t) t = L->head_end;
@@ -1034,27 +1100,55 @@ static int sim_scenario(const orc_input *in, uint64_t s, uint32_t *rec, int64_t 
         S.steps++;
         tr(&S, t, TR_STEP, -1, -1, 0, 0);
         retire(&S, t);                                                   /* Phase A */
-        for (uint32_t c = 0; c < S.C; ++c) {
+        for (uint32_t c = 0; c < S.nL; ++c) {
             S.snap_L[c] = S.lane[c].L_last; S.snap_n[c] = S.lane[c].akb_n;
             S.snap_level[c] = S.lane[c].level; S.snap_busy[c] = S.lane[c].q_head < S.lane[c].q_tail;
             if (classical(&S)) { S.snap_tarr[c] = S.lane[c].t_arr; S.snap_R[c] = remaining_work(&S, c); }
         }
-        for (uint32_t c = 0; c < S.C; ++c)                               /* Phase B */
+        for (uint32_t c = 0; c < S.nL; ++c)                              /* Phase B */
             if (S.lane[c].cpu_next == t) {
                 if (S.lane[c].job) { S.lane[c].job = 0; S.lane[c].job_run = 0; S.cpu_dirty = 1; }   /* job done */
                 lane_step(&S, c, t);
             }
+        /* per-task executors (R32): messages published in a round are delivered at its end;
+         * a thread waiting for one runs in the next round, at the same t, against the same
+         * read view; a delivered message replaces an untaken one (queue depth 1) */
+        while (in->task_exec) {
+            int woke = 0;
+            for (uint32_t c = 0; c < S.nL; ++c) {
+                orc_lane *L = &S.lane[c];
+                if (L->msg_pend) { L->msg = L->msg_pend; L->msg_pend = 0; }
+                if (L->pc == PC_WAIT_MSG && L->msg) { L->cpu_next = t; woke = 1; }
+            }
+            if (!woke) break;
+            for (uint32_t c = 0; c < S.nL; ++c)
+                if (S.lane[c].pc == PC_WAIT_MSG && S.lane[c].cpu_next == t) lane_step(&S, c, t);
+        }
         cpu_schedule(&S, t);                                             /* CPU cores (R29) */
         dispatch(&S, t);                                                 /* Phase C */
     }
     /* end of horizon (R7): admitted, unfinished instances are misses */
     const uint32_t stride = AGG_COUNTERS + in->rt_bins + RATIO_BINS;
-    for (uint32_t c = 0; c < S.C; ++c) {
-        orc_lane *L = &S.lane[c];
-        uint32_t first_unstarted = L->inst;
-        if (L->pc != PC_ARRIVE && L->pc != PC_DONE) { L->unfin++; first_unstarted = L->inst + 1; }
-        if (L->pc != PC_DONE)
-            for (uint32_t i = first_unstarted; arrival(&S, c, i) < S.H; ++i) { L->unfin++; L->total++; }
+    for (uint32_t c = 0, l0 = 0; c < S.C; l0 += in->task_exec ? in->ch_ntasks[c] : 1, ++c) {
+        orc_lane *L;
+        if (!in->task_exec) {
+            L = &S.lane[c];
+            uint32_t first_unstarted = L->inst;
+            if (L->pc != PC_ARRIVE && L->pc != PC_DONE) { L->unfin++; first_unstarted = L->inst + 1; }
+            if (L->pc != PC_DONE)
+                for (uint32_t i = first_unstarted; arrival(&S, c, i) < S.H; ++i) { L->unfin++; L->total++; }
+        } else {
+            /* R32: the chain's last stage has recorded instances [0, expect); every later admitted
+             * instance is unfinished; early exits and launches are summed over the stages */
+            L = &S.lane[l0 + in->ch_ntasks[c] - 1];
+            for (uint32_t i = L->expect; arrival(&S, l0, i) < S.H; ++i) L->unfin++;
+            L->total = L->expect + L->unfin;
+            uint32_t early = 0, launches = 0;
+            for (uint32_t j = 0; j < in->ch_ntasks[c]; ++j) {
+                early += S.lane[l0 + j].early; launches += S.lane[l0 + j].launches;
+            }
+            L->early = early; L->launches = launches;
+        }
         L->miss += L->unfin;
         uint32_t *r = rec + (uint64_t)c * REC_WORDS;
         r[0] = L->total; r[1] = L->miss; r[2] = L->early; r[3] = L->unfin;
@@ -1063,6 +1157,9 @@ static int sim_scenario(const orc_input *in, uint64_t s, uint32_t *rec, int64_t 
         int64_t *a = agg + (int64_t)c * stride;
         a[0] += L->total; a[1] += L->miss; a[2] += L->early; a[3] += L->unfin; a[4] += (int64_t)L->sum_rt;
         if (L->total) a[AGG_COUNTERS + in->rt_bins + (uint64_t)100 * L->miss / L->total] += 1;
+    }
+    for (uint32_t c = 0; c < S.nL; ++c) {
+        orc_lane *L = &S.lane[c];
         free(L->akb); free(L->q); free(L->cpu_hist); free(L->cpu_hist_n); free(L->cpu_pred);
     }
     agg[(int64_t)S.C * stride + COLL_BINS + 0] += S.launches;
@@ -1089,6 +1186,12 @@ int orc_run(const orc_input *in, uint32_t *records, int64_t *agg,
     }
     for (uint32_t c = 0; c < in->num_chains; ++c)     /* arrivals strictly increasing: P' > J (R3) */
         if (in->ch_period[c] * (int64_t)in->fa_den / (int64_t)in->fa_num <= in->jitter_ns) return -2;
+    if (in->task_exec) {                              /* R32: at most 32 threads; no R26 predictor */
+        uint32_t nt = 0;
+        for (uint32_t c = 0; c < in->num_chains; ++c) nt += in->ch_ntasks[c];
+        if (nt > 32) return -2;
+        if (in->cpu_ma_window) return -1;
+    }
     if (trace_len) *trace_len = 0;
     for (uint64_t j = 0; j < in->scenario_count; ++j) {
         uint32_t *rec = records + j * (uint64_t)in->num_chains * REC_WORDS;

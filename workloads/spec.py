@@ -29,6 +29,7 @@ F_BIND, F_DELAY, F_EARLY_EXIT = 1, 2, 4
 F_COLLISIONS = 8           # count kernel collisions of urgent kernels (metric only; R24)
 F_ALL = F_BIND | F_DELAY | F_EARLY_EXIT
 SYNC_ASYNC, SYNC_EACH, SYNC_BATCHED, SYNC_OVERLAP = 0, 1, 2, 3
+EXEC_CHAIN, EXEC_TASK = 0, 1   # one thread per chain (R6) / one executor per task (R32)
 
 MS = 1_000_000
 US = 1_000
@@ -76,6 +77,7 @@ class Workload:
     free_ns: int = 188 * US            # cudaFree cost on an idle device (Table 5; R28)
     cpu_cores: int = 0                 # cores shared by the chains' threads, 0 = one each (8; R29)
     contention_permille: int = 0       # kernel slow-down per co-running utilisation (R30)
+    executors: int = EXEC_CHAIN        # EXEC_TASK: one thread per task, depth-1 hand-over (R32)
 
     @property
     def num_chains(self) -> int:
