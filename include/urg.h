@@ -90,7 +90,16 @@ typedef struct {
     uint32_t contention_permille;         /* alpha: a kernel started while U per-mille of the GPU runs
                                              takes d + floor(d * alpha * U / 10^6) (
                                              DESIGN.md R30); 0 = no slow-down */
+    uint32_t executors;                   /* URG_EXEC_CHAIN: one thread per chain runs its tasks in turn
+                                             (R6).  URG_EXEC_TASK: one executor thread per task
+                                             ("each task is executed by a dedicated thread"):
+                                             task j+1 of instance i starts when task j publishes it, tasks
+                                             of successive instances overlap, and each subscription keeps
+                                             the latest message only (depth 1; R32).  Needs
+                                             sum(num_tasks) <= 32 (URG_ERANGE) and no CPU predictor
+                                             (urg_policy.cpu_ma_window = 0, else URG_EINVAL at simulate) */
 } urg_workload_desc;
+enum { URG_EXEC_CHAIN = 0, URG_EXEC_TASK = 1 };
 
 typedef struct urg_workload urg_workload; /* opaque; immutable after create; owns its device copy */
 

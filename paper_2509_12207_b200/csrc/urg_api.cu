@@ -43,6 +43,8 @@ struct urg_workload {
     uint32_t cpu_cores = 0;           // cores shared by the chains' threads, 0 = one each (R29)
     uint32_t alpha_pm = 0;            // contention slow-down (R30)
     bool has_copy = false;            // some operation is a memcpy (R31)
+    uint32_t num_lanes = 0;           // simulated threads: chains, or tasks under per-task executors (R32)
+    bool task_exec = false;
 };
 
 static thread_local std::string g_err;
@@ -94,6 +96,7 @@ extern "C" urg_status urg_create_workload(const urg_workload_desc *d, urg_worklo
     if (d->free_ns < 0 || d->free_ns >= (1LL << 40)) return fail(URG_EINVAL, "free_ns must be in [0, 2^40)");
     if (d->cpu_cores > 32) return fail(URG_EINVAL, "cpu_cores must be <= 32 (0 = one core per chain thread)");
     if (d->contention_permille > 100000) return fail(URG_EINVAL, "contention_permille must be <= 100000");
+    if (d->executors > URG_EXEC_TASK) return fail(URG_EINVAL, "executors must be URG_EXEC_CHAIN or URG_EXEC_TASK");
 
     uint32_t n_tasks = 0, n_kern = 0;
     for (uint32_t c = 0; c < d->num_chains && d->chains; ++c)
@@ -127,15 +130,19 @@ extern "C" urg_status urg_create_workload(const urg_workload_desc *d, urg_worklo
         }
         n_tasks += ch.num_tasks;
     }
+    const bool te = d->executors == URG_EXEC_TASK;
+    const uint32_t n_lanes = te ? n_tasks : d->num_chains;
+    if (n_lanes > 32)
+        return fail(URG_ERANGE, "per-task executors: %u tasks exceed 32 (one warp lane per executor thread)", n_lanes);
 
     // ---- pack the blob ----
     UrgBlobHeader h = {};
     h.magic = URG_BLOB_MAGIC;
-    h.num_chains = d->num_chains;
+    h.num_chains = n_lanes;
     h.num_tasks = n_tasks;
     h.num_kernels = n_kern;
     uint32_t off = align16(sizeof(UrgBlobHeader));
-    h.off_chains = off; off = align16(off + d->num_chains * (uint32_t)sizeof(UrgChainRec));
+    h.off_chains = off; off = align16(off + n_lanes * (uint32_t)sizeof(UrgChainRec));
     h.off_tasks = off;  off = align16(off + n_tasks * (uint32_t)sizeof(UrgTaskRec));
     h.off_kerns = off;  off = align16(off + n_kern * (uint32_t)sizeof(UrgKernRec));
     if (d->inst_quantiles_q16) { h.off_inst_q = off; off = align16(off + URG_QTABLE * 4); }
@@ -154,18 +161,25 @@ extern "C" urg_status urg_create_workload(const urg_workload_desc *d, urg_worklo
     w->free_ns = d->free_ns;
     w->cpu_cores = d->cpu_cores;
     w->alpha_pm = d->contention_permille;
+    w->num_lanes = n_lanes; w->task_exec = te;
     w->blob.assign(off, 0);
     memcpy(w->blob.data(), &h, sizeof h);
     UrgChainRec *chs = (UrgChainRec *)(w->blob.data() + h.off_chains);
     UrgTaskRec *tks = (UrgTaskRec *)(w->blob.data() + h.off_tasks);
     UrgKernRec *krs = (UrgKernRec *)(w->blob.data() + h.off_kerns);
-    uint32_t tb = 0, kb = 0;
+    uint32_t tb = 0, kb = 0, lane = 0;
     for (uint32_t c = 0; c < d->num_chains; ++c) {
         const urg_chain_desc &ch = d->chains[c];
-        UrgChainRec &r = chs[c];
-        r.period_ns = ch.period_ns; r.deadline_ns = ch.deadline_ns; r.offset_ns = ch.offset_ns;
-        r.num_tasks = ch.num_tasks; r.task_base = tb;
-        r.kern_base = kb; r.cpu_sigma_ppm = ch.cpu_sigma_ppm; r.gpu_sigma_ppm = ch.gpu_sigma_ppm;
+        uint32_t n_local = 0;
+        for (uint32_t j = 0; j < ch.num_tasks; ++j) n_local += ch.tasks[j].num_kernels;
+        // one thread record per chain, or per task of the chain (R32), chain-major
+        for (uint32_t j = 0, k_first = 0; j < (te ? ch.num_tasks : 1u); k_first += ch.tasks[j].num_kernels, ++j) {
+            UrgChainRec &r = chs[lane++];
+            r.period_ns = ch.period_ns; r.deadline_ns = ch.deadline_ns; r.offset_ns = ch.offset_ns;
+            r.num_tasks = ch.num_tasks; r.task_base = tb; r.num_kernels = n_local;
+            r.kern_base = kb; r.cpu_sigma_ppm = ch.cpu_sigma_ppm; r.gpu_sigma_ppm = ch.gpu_sigma_ppm;
+            r.chain_id = c; r.stage = te ? j : 0; r.stage_end = te ? j + 1 : ch.num_tasks; r.k_first = k_first;
+        }
         uint32_t local = 0;
         for (uint32_t j = 0; j < ch.num_tasks; ++j) {
             const urg_task_desc &t = ch.tasks[j];
@@ -179,7 +193,6 @@ extern "C" urg_status urg_create_workload(const urg_workload_desc *d, urg_worklo
             }
             local += t.num_kernels;
         }
-        r.num_kernels = local;
         if (ch.num_tasks > w->max_tasks) w->max_tasks = ch.num_tasks;
         tb += ch.num_tasks; kb += local;
         w->period.push_back(ch.period_ns);
@@ -231,6 +244,8 @@ static urg_status validate_call(const urg_workload *w, const urg_policy *p, cons
     if (p->sleep_ns <= 0) return fail(URG_EINVAL, "policy.sleep_ns must be > 0");
     if (p->noise_permille > 1000) return fail(URG_EINVAL, "policy.noise_permille must be <= 1000");
     if (p->cpu_ma_window > 64) return fail(URG_EINVAL, "policy.cpu_ma_window must be <= 64");
+    if (w->task_exec && p->cpu_ma_window)
+        return fail(URG_EINVAL, "policy.cpu_ma_window must be 0 with per-task executors (DESIGN.md R32)");
     if (b->fa_num == 0 || b->fa_den == 0) return fail(URG_EINVAL, "batch.fa_num and batch.fa_den must be > 0");
     if (b->fd_num == 0 || b->fd_den == 0) return fail(URG_EINVAL, "batch.fd_num and batch.fd_den must be > 0");
     if (b->ftight_permille > 1000) return fail(URG_EINVAL, "batch.ftight_permille must be <= 1000");
@@ -251,7 +266,8 @@ static urg_status validate_call(const urg_workload *w, const urg_policy *p, cons
 static void fill_params(const urg_workload *w, const urg_policy *p, const urg_batch *b, UrgSimParams &P)
 {
     memset(&P, 0, sizeof P);
-    P.num_chains = w->num_chains; P.num_prio = w->num_prio; P.rt_bins = w->rt_bins;
+    P.num_chains = w->num_chains; P.num_lanes = w->num_lanes; P.task_exec = w->task_exec ? 1u : 0u;
+    P.num_prio = w->num_prio; P.rt_bins = w->rt_bins;
     P.agg_stride = 5 + w->rt_bins + 101;
     P.launch_ns = w->launch_ns; P.launch_akb_ns = w->launch_akb_ns;
     P.sync_lo_ns = w->sync_lo_ns; P.sync_hi_ns = w->sync_hi_ns;
@@ -306,7 +322,7 @@ static urg_status prepare_launch(const urg_workload *w, const urg_policy *p, con
     fill_params(w, p, b, P);
     // the extended-model build only when the batch uses noise, the CPU predictor or cudaFree
     bool ext = (p->kind == URG_URGENGO && p->noise_permille) || (p->kind >= URG_URGENGO && p->cpu_ma_window) ||
-               w->has_free || w->cpu_cores > 0 || w->alpha_pm > 0 || w->has_copy;
+               w->has_free || w->cpu_cores > 0 || w->alpha_pm > 0 || w->has_copy || w->task_exec;
     if (const char *ee = getenv("URG_EXT")) ext = ext || atoi(ee) != 0;   // test hook: force the extended build
     // two scenarios per warp in the throughput core build when the chains fit a half warp
     bool pk = wide && !cal && !ext && w->num_chains <= 16;

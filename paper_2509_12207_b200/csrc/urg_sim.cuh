@@ -24,7 +24,7 @@ enum { S_ASYNC = 0, S_EACH = 1, S_BATCHED = 2, S_OVERLAP = 3 };
 // lane program counter; the per-launch states come first so one range test skips the
 // per-task / per-instance states on the common path
 enum { PC_ENQUEUE = 0, PC_ATTEMPT, PC_CPU_DONE, PC_SYNC_RET, PC_FREE_RET, PC_ARRIVE, PC_TASK_START, PC_SYNC_WAIT,
-       PC_FREE_WAIT, PC_DONE };
+       PC_FREE_WAIT, PC_WAIT_MSG, PC_DONE };
 enum { ERR_TIME = 1, ERR_GUARD = 2 };
 
 // ---------------------------------------------------------------------------
@@ -161,18 +161,26 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
     T.kern = (const UrgKernRec *)(sm + hdr->off_kerns);
     T.inst_q = hdr->off_inst_q ? (const int32_t *)(sm + hdr->off_inst_q) : nullptr;
     T.kern_q = hdr->off_kern_q ? (const uint32_t *)(sm + hdr->off_kern_q) : nullptr;
-    const uint32_t C = P.num_chains;
-    // per-chain totals of the estimates (the remaining-work sums of Eq. 2 start from them)
+    const uint32_t C = P.num_lanes;    // threads: chains, or tasks under per-task executors (R32)
+    const uint32_t NC = P.num_chains;  // chains: records and aggregates
+    // per-thread totals of the estimates from its first task on (the remaining-work sums of Eq. 2
+    // start from them)
     for (uint32_t c = warp; c < C; c += nwarps) {
-        int64_t g = 0, cp = 0;
-        for (uint32_t k = lane; k < chs[c].num_kernels; k += 32) g += T.kern[chs[c].kern_base + k].estimate_ns;
-        for (uint32_t j = lane; j < chs[c].num_tasks; j += 32) cp += T.task[chs[c].task_base + j].cpu_estimate_ns;
+        int64_t g = 0, cp = 0, gc = 0;
+        for (uint32_t k = lane; k < chs[c].num_kernels; k += 32) {
+            const int64_t e = T.kern[chs[c].kern_base + k].estimate_ns;
+            gc += e;
+            if (k >= chs[c].k_first) g += e;
+        }
+        for (uint32_t j = chs[c].stage + lane; j < chs[c].num_tasks; j += 32)
+            cp += T.task[chs[c].task_base + j].cpu_estimate_ns;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             g += (int64_t)__shfl_xor_sync(FULL, (unsigned long long)g, o);
             cp += (int64_t)__shfl_xor_sync(FULL, (unsigned long long)cp, o);
+            gc += (int64_t)__shfl_xor_sync(FULL, (unsigned long long)gc, o);
         }
-        if (lane == 0) { chs[c].gpu_est_total = g; chs[c].cpu_est_total = cp; }
+        if (lane == 0) { chs[c].gpu_est_total = g; chs[c].cpu_est_total = cp; chs[c].gpu_est_chain = gc; }
     }
     __syncthreads();
 
@@ -181,6 +189,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
     int64_t *snapL = (int64_t *)(sm + P.snap_offset) + warp * 128;
     int64_t *snapA = snapL + 32, *snapB = snapL + 64;
     uint32_t *snapLev = (uint32_t *)(snapL + 96);
+    uint32_t *mbox = (uint32_t *)(snapL + 112);   // R32: message published to each lane this round
     constexpr bool urg = KIND == K_URGENGO;
     constexpr bool cls = KIND >= K_EDF;        // classical policies (R27): AKB-tracking, no urgency
     constexpr bool akb_on = urg || cls;
@@ -193,6 +202,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
     const bool cores_on = EXT && P.cpu_cores > 0;          // R29: the chains' threads share P.cpu_cores cores
     const bool contend = EXT && P.alpha_pm > 0;            // R30: co-running kernels slow a starting one down
     const bool has_copy = EXT && P.has_copy != 0;          // R31: memcpy operations on the copy engine
+    const bool te = EXT && P.task_exec != 0;               // R32: one executor thread per task
     // R26 predictor state of this lane's chain in shared memory: [max_tasks][W] ring of
     // measured CPU durations, [max_tasks] counts, [max_tasks] this instance's estimates
     uint32_t *ma_ring = (uint32_t *)(sm + P.ma_offset) + (size_t)threadIdx.x * P.ma_slot;
@@ -239,6 +249,10 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
     const volatile UrgChainRec *crv = &chs[valid_c ? c : 0];
     const uint32_t kbase = cr.kern_base, tbase = cr.task_base;
 #define CRF(f) (WIDE ? crv->f : cr.f)
+    // R32: the chain this thread serves (randomness keys, records) and the tasks it runs
+    const uint32_t cid = EXT ? cr.chain_id : c;
+    const uint32_t stage = EXT ? cr.stage : 0u, k_first = EXT ? cr.k_first : 0u;
+    const bool last_stage = !EXT || cr.stage_end == cr.num_tasks;
 
     for (;;) {
         unsigned long long jw = 0;
@@ -256,14 +270,18 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             Dp = CRF(deadline_ns) * (int64_t)P.fd_num / (int64_t)P.fd_den;
         }
         bool tight = false;
-        if (P.tight_explicit) tight = valid && ((P.tight_mask >> c) & 1u);
+        // chain-level draws: with per-task executors only each chain's first thread counts (R32)
+        const bool first_of_chain = stage == 0u;
+        if (P.tight_explicit) tight = valid && ((P.tight_mask >> cid) & 1u);
         else if (P.ftight_permille) {
-            const uint32_t n_tight = (P.ftight_permille * C + 999u) / 1000u;
-            const uint32_t w = valid ? rng_word(P.seed, s, URG_TAG_TIGHT, c, 0, 0) : 0xFFFFFFFFu;
+            const uint32_t n_tight = (P.ftight_permille * NC + 999u) / 1000u;
+            const uint32_t w = valid ? rng_word(P.seed, s, URG_TAG_TIGHT, cid, 0, 0) : 0xFFFFFFFFu;
             uint32_t rank = 0;
             for (uint32_t o = 0; o < C; ++o) {
                 const uint32_t wo = __shfl_sync(FULL, w, hbase + (int)o);
-                rank += (wo < w || (wo == w && o < c)) ? 1u : 0u;
+                const uint32_t co = EXT ? __shfl_sync(FULL, cid, hbase + (int)o) : o;
+                const bool fo = !EXT || __shfl_sync(FULL, first_of_chain, hbase + (int)o);
+                rank += (fo && (wo < w || (wo == w && co < cid))) ? 1u : 0u;
             }
             tight = valid && rank < n_tight;
         }
@@ -280,12 +298,15 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             uint32_t r = 1;
             for (uint32_t o = 0; o < C; ++o) {
                 const int64_t Do = shfl64(Dp, hbase + (int)o);
-                r += (Do < Dp || (Do == Dp && o < c)) ? 1u : 0u;
+                const uint32_t co = EXT ? __shfl_sync(FULL, cid, hbase + (int)o) : o;
+                const bool fo = !EXT || __shfl_sync(FULL, first_of_chain, hbase + (int)o);
+                r += (fo && (Do < Dp || (Do == Dp && co < cid))) ? 1u : 0u;
             }
-            if (C > 1 && P.num_prio > 1) static_level = (uint32_t)(((uint64_t)(r - 1) * (P.num_prio - 1)) / (C - 1));
+            if (NC > 1 && P.num_prio > 1) static_level = (uint32_t)(((uint64_t)(r - 1) * (P.num_prio - 1)) / (NC - 1));
         }
 
         // ---- per-lane dynamic state ----
+        if (te) { mbox[lane] = 0u; __syncwarp(); }   // R32: no message published yet
         if (ma)
             for (uint32_t j = 0; j < P.ma_max_tasks; ++j) ma_cnt[j] = 0;
         int pc = PC_DONE;
@@ -313,11 +334,13 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         bool head_copy = false;                // R31: the head is a memcpy (copy engine)
         uint32_t n_total = 0, n_miss = 0, n_early = 0, n_unfin = 0, n_launch = 0, hash = 2166136261u;
         uint64_t sum_rt = 0;
+        uint32_t msg = 0;                      // R32: delivered, untaken message (instance + 1), 0 = none
+        uint32_t expect = 0;                   // R32, last stage: next instance to record
 
         auto arrival = [&](uint32_t i) -> int64_t {
             int64_t jit = 0;
             if (P.jitter_ns > 0)
-                jit = (int64_t)(rng_word(P.seed, s, URG_TAG_ARR, c, i, 0) % (uint32_t)(P.jitter_ns + 1));
+                jit = (int64_t)(rng_word(P.seed, s, URG_TAG_ARR, cid, i, 0) % (uint32_t)(P.jitter_ns + 1));
             return CRF(offset_ns) + (int64_t)i * Pp + jit;
         };
         auto inst_factor = [&](uint32_t w, uint32_t sigma) -> uint32_t {
@@ -343,7 +366,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         auto cls_key_a = [&]() -> int64_t {
             return KIND == K_EDF ? t_arr + Dp : KIND == K_HRRN ? t_arr : KIND == K_LCUF ? Pp : 0;
         };
-        auto cls_key_b = [&]() -> int64_t { return KIND == K_LCUF ? CRF(gpu_est_total) : rem_g + rem_c; };
+        auto cls_key_b = [&]() -> int64_t { return KIND == K_LCUF ? CRF(gpu_est_chain) : rem_g + rem_c; };
         // "chain o ranks before chain s" (ties by smaller chain id; exact 128-bit ratios)
         auto cls_before = [&](int64_t oA, int64_t oB, int o, int64_t sA, int64_t sB, int sl, int64_t t) -> bool {
             if (KIND == K_EDF || KIND == K_SJF) {
@@ -366,8 +389,24 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
 
         if (valid) {
             t_arr = arrival(0);
-            if (t_arr < H) { pc = PC_ARRIVE; cpu_next = t_arr; }
+            if (te && stage > 0) pc = PC_WAIT_MSG;   // R32: waits for the previous task's message
+            else if (t_arr < H) { pc = PC_ARRIVE; cpu_next = t_arr; }
         }
+        // R32: take the delivered message (instance msg - 1); on the chain's last stage, record
+        // the instances the message sequence skipped as misses, in order
+        auto take_msg = [&]() {
+            const uint32_t i = msg - 1u;
+            msg = 0;
+            if (last_stage)
+                for (; expect < i; ++expect) {
+                    ++n_miss;
+                    hash = (hash ^ 0xFFFFFFFFu) * 16777619u;
+                    hash = (hash ^ 0xFFFFFFFFu) * 16777619u;
+                }
+            inst = i;
+            t_arr = arrival(i);
+            pc = PC_ARRIVE;
+        };
 
         // ---- lane-local pieces of a loop step (R21); used by the warp-wide
         //      step and by the single-lane ("solo") steps below ----
@@ -385,7 +424,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         // Phase C start of this lane's waiting head: non-preemptive, exact duration (R4, R19, R20)
         auto start_head = [&](int64_t t, uint32_t u_run) {
             uint64_t G = 65536u;
-            if (KQ) G = T.kern_q[rng_word(P.seed, s, URG_TAG_KERN, c, inst, done) >> 20];
+            if (KQ) G = T.kern_q[rng_word(P.seed, s, URG_TAG_KERN, cid, inst, done) >> 20];
             uint64_t d = ((((uint64_t)T.kern[kbase + done].nominal_ns * Fg) >> 16) * G) >> 16;
             d = d < 1 ? 1 : (d > 0xFFFFFFFFull ? 0xFFFFFFFFull : d);
             if (contend && !head_copy) d += d * (uint64_t)P.alpha_pm * u_run / 1000000ull;   // R30
@@ -398,6 +437,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         auto phase_b = [&](int64_t t, uint32_t urgent_m, uint32_t active_m, uint32_t busy_m) -> bool {
             bool newhead = false;
             if (cores_on && job) { job = false; job_run = false; cpu_chg = true; }   // R29: the job completed
+            if (te && pc == PC_WAIT_MSG) take_msg();   // woken by a delivered message (R32)
             for (uint32_t guard = 0;; ++guard) {
                 if (guard > (1u << 24)) {
                     if (atomicCAS((unsigned long long *)err, 0ull, (unsigned long long)ERR_GUARD) == 0ull) err[1] = s;
@@ -420,11 +460,15 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                 }
                 if (pc == PC_FREE_RET) task_done = true;   // R28: the barrier was served
                 if (task_done) {
-                    if (++task < CRF(num_tasks)) {
+                    if (++task < (EXT ? CRF(stage_end) : CRF(num_tasks))) {
                         task_first = task_end;
                         task_end += T.task[tbase + task].num_kernels;
                         pc = PC_TASK_START;
+                    } else if (!last_stage) {   // R32: publish instance inst to the next task's thread
+                        mbox[lane + 1] = inst + 1u;
+                        next_inst = true;
                     } else {   // instance complete (R18, R22)
+                        expect = inst + 1u;
                         const int64_t rt = t - t_arr;
                         if (rt > Dp) ++n_miss;
                         sum_rt += (uint64_t)rt;
@@ -432,15 +476,15 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                         hash = (hash ^ (uint32_t)((uint64_t)rt >> 32)) * 16777619u;
                         int64_t bin = rt / P.rt_bin_ns;
                         if (bin > (int64_t)P.rt_bins - 1) bin = P.rt_bins - 1;
-                        if (!CAL) atomicAdd(&agg[(uint64_t)c * stride + 5 + bin], 1ull);
+                        if (!CAL) atomicAdd(&agg[(uint64_t)cid * stride + 5 + bin], 1ull);
                         next_inst = true;
                     }
                 }
-                if (pc == PC_ARRIVE) {   // frame arrival / instance start (R6)
-                    ++n_total;
-                    Fg = inst_factor(rng_word(P.seed, s, URG_TAG_INST, c, inst, 0), CRF(gpu_sigma_ppm));
-                    Fc = inst_factor(rng_word(P.seed, s, URG_TAG_INST, c, inst, 1), CRF(cpu_sigma_ppm));
-                    task = 0; launched = 0; done = 0; sync_ord = 0;
+                if (pc == PC_ARRIVE) {   // frame arrival / instance start (R6; R32: the thread's task)
+                    if (!te) ++n_total;
+                    Fg = inst_factor(rng_word(P.seed, s, URG_TAG_INST, cid, inst, 0), CRF(gpu_sigma_ppm));
+                    Fc = inst_factor(rng_word(P.seed, s, URG_TAG_INST, cid, inst, 1), CRF(cpu_sigma_ppm));
+                    task = stage; launched = k_first; done = k_first; sync_ord = stage << 16;
                     rem_g = CRF(gpu_est_total); rem_c = CRF(cpu_est_total);
                     if (ma) {   // R26: this instance's ~E^cpu_j, floor mean of the last min(W, h_j) measurements
                         rem_c = 0;
@@ -457,22 +501,26 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                             rem_c += pred;
                         }
                     }
-                    task_first = 0; task_end = T.task[tbase].num_kernels;
+                    task_first = k_first; task_end = k_first + T.task[tbase + stage].num_kernels;
                     pc = PC_TASK_START;
                 }
                 if (pc == PC_TASK_START) {   // new CPU segment: evaluate, early exit
                     bool exited = false;
                     if (urg) {
                         if (noise)
-                            nz = (int32_t)(rng_word(P.seed, s, URG_TAG_NOISE, c, inst, task) %
+                            nz = (int32_t)(rng_word(P.seed, s, URG_TAG_NOISE, cid, inst, task) %
                                            (2u * P.noise_pm + 1u)) - (int32_t)P.noise_pm;
                         const int64_t lax = laxity(t);   // Eq. 2 (R9)
                         L_last = lax;
                         if (f_early && lax < 0) {
                             akb = 0;
-                            ++n_early; ++n_miss;
-                            hash = (hash ^ 0xFFFFFFFFu) * 16777619u;
-                            hash = (hash ^ 0xFFFFFFFFu) * 16777619u;
+                            ++n_early;
+                            if (last_stage) {   // R32: an earlier task's exit is a gap the last task records
+                                ++n_miss;
+                                hash = (hash ^ 0xFFFFFFFFu) * 16777619u;
+                                hash = (hash ^ 0xFFFFFFFFu) * 16777619u;
+                                expect = inst + 1u;
+                            }
                             pc = PC_DONE;
                             next_inst = exited = true;
                         }
@@ -487,6 +535,12 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     }
                 }
                 if (next_inst) {   // advance to the next instance of this chain (R6, R7)
+                    if (te && stage > 0) {   // R32: the next message, or wait for one
+                        if (msg) { take_msg(); continue; }
+                        pc = PC_WAIT_MSG;
+                        cpu_next = INF64;
+                        break;
+                    }
                     ++inst;
                     t_arr = arrival(inst);
                     if (t_arr >= H) { pc = PC_DONE; cpu_next = INF64; break; }   // not admitted
@@ -516,7 +570,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                             mm &= mm - 1;
                             k += (snapLev[o] <= level && urgency_key(snapL[o]) < own) ? 1u : 0u;
                         }
-                        if (k && !CAL) atomicAdd(&agg[(uint64_t)C * stride + (k + 1 > 32 ? 32 : k + 1)], 1ull);
+                        if (k && !CAL) atomicAdd(&agg[(uint64_t)NC * stride + (k + 1 > 32 ? 32 : k + 1)], 1ull);
                     }
                     const bool last = launched == task_end;
                     if (last) rem_c -= ma ? ma_pred[task] : T.task[tbase + task].cpu_estimate_ns;
@@ -544,7 +598,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                         sync_target = (uint32_t)target;
                         sync_cost = P.sync_lo_ns;
                         if (P.sync_hi_ns > P.sync_lo_ns)
-                            sync_cost += (int64_t)(rng_word(P.seed, s, URG_TAG_SYNC, c, inst, sync_ord) %
+                            sync_cost += (int64_t)(rng_word(P.seed, s, URG_TAG_SYNC, cid, inst, sync_ord) %
                                                    (uint32_t)(P.sync_hi_ns - P.sync_lo_ns + 1));
                         ++sync_ord;
                         if (done >= sync_target) {
@@ -720,10 +774,23 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                 ++st_multi;
 #endif
                 uint32_t urgent_m = 0, active_m = 0, busy_m = 0;
-                if (urg || cls) snapshot(due && can_bind(), urgent_m, active_m, busy_m);
+                if (urg || cls) snapshot(te || (due && can_bind()), urgent_m, active_m, busy_m);
                 bool nh = false;
                 if (due) nh = phase_b(t, urgent_m, active_m, busy_m);
                 dirty |= PK ? hany(nh) : __any_sync(FULL, nh);
+                // R32: messages published in a round are delivered at its end (a newer one replaces
+                // an untaken one); threads waiting for one run in the next round, same t and read view
+                while (te) {
+                    __syncwarp();
+                    const uint32_t pub = mbox[lane];
+                    if (pub) { msg = pub; mbox[lane] = 0u; }
+                    __syncwarp();
+                    const bool wake = !fin && pc == PC_WAIT_MSG && msg != 0u;
+                    if (!__any_sync(FULL, wake)) break;
+                    bool nh2 = false;
+                    if (wake) nh2 = phase_b(t, urgent_m, active_m, busy_m);
+                    dirty |= __any_sync(FULL, nh2);
+                }
             }
 
 
@@ -732,7 +799,8 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             if (cores_on) {
                 const bool rr = __any_sync(FULL, rerank_req);
                 rerank_req = false;
-                if (rr && urg && valid && pc != PC_ARRIVE && pc != PC_DONE) cpu_prio = urgency_key(laxity(t));
+                if (rr && urg && valid && pc != PC_ARRIVE && pc != PC_WAIT_MSG && pc != PC_DONE)
+                    cpu_prio = urgency_key(laxity(t));
                 if (rr || __any_sync(FULL, cpu_chg)) {
                     cpu_chg = false;
                     const uint32_t jm = __ballot_sync(FULL, job);
@@ -845,19 +913,34 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             continue;
         }
         // ---- A11: end of horizon accounting (R7) and per-scenario records ----
-        if (valid) {
-            uint32_t first_unstarted = inst;
-            if (pc != PC_ARRIVE && pc != PC_DONE) { ++n_unfin; first_unstarted = inst + 1; }
-            if (pc != PC_DONE)
-                for (uint32_t i = first_unstarted; arrival(i) < H; ++i) { ++n_unfin; ++n_total; }
+        if (te) {   // R32: the chain's early exits and launches, summed over its threads
+            uint32_t e_sum = 0, l_sum = 0;
+            for (uint32_t o = 0; o < C; ++o) {
+                const uint32_t co = __shfl_sync(FULL, cid, (int)o);
+                const uint32_t eo = __shfl_sync(FULL, n_early, (int)o), lo = __shfl_sync(FULL, n_launch, (int)o);
+                if (co == cid) { e_sum += eo; l_sum += lo; }
+            }
+            if (valid && last_stage) { n_early = e_sum; n_launch = l_sum; }
+            else n_launch = 0;   // counted once, on the chain's last stage (the warp's launch total)
+        }
+        if (valid && last_stage) {
+            if (te) {   // R32: instances [0, expect) are recorded; later admitted ones are unfinished
+                for (uint32_t i = expect; arrival(i) < H; ++i) ++n_unfin;
+                n_total = expect + n_unfin;
+            } else {
+                uint32_t first_unstarted = inst;
+                if (pc != PC_ARRIVE && pc != PC_DONE) { ++n_unfin; first_unstarted = inst + 1; }
+                if (pc != PC_DONE)
+                    for (uint32_t i = first_unstarted; arrival(i) < H; ++i) { ++n_unfin; ++n_total; }
+            }
             n_miss += n_unfin;
             if (records) {
-                uint4 *r = (uint4 *)(records + ((uint64_t)jw * C + c) * 8);
+                uint4 *r = (uint4 *)(records + ((uint64_t)jw * NC + cid) * 8);
                 r[0] = make_uint4(n_total, n_miss, n_early, n_unfin);
                 r[1] = make_uint4(n_launch, hash, (uint32_t)sum_rt, (uint32_t)(sum_rt >> 32));
             }
             // A12: aggregates (integer sums: order-independent, R23)
-            unsigned long long *a = agg + (uint64_t)c * stride;
+            unsigned long long *a = agg + (uint64_t)cid * stride;
             atomicAdd(&a[0], (unsigned long long)n_total);
             atomicAdd(&a[1], (unsigned long long)n_miss);
             atomicAdd(&a[2], (unsigned long long)n_early);
@@ -870,8 +953,8 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
     if (PK) my_steps += __shfl_sync(FULL, my_steps, 16);   // the upper half's steps
     if (lane == 0) {
         if (CAL) return;
-        atomicAdd(&agg[(uint64_t)C * stride + URG_COLL_BINS + 0], my_launches);
-        atomicAdd(&agg[(uint64_t)C * stride + URG_COLL_BINS + 1], my_steps);
+        atomicAdd(&agg[(uint64_t)NC * stride + URG_COLL_BINS + 0], my_launches);
+        atomicAdd(&agg[(uint64_t)NC * stride + URG_COLL_BINS + 1], my_steps);
 #ifdef URG_STATS
         atomicAdd(&work[4], st_single); atomicAdd(&work[5], st_multi);
         atomicAdd(&work[6], st_dispatch); atomicAdd(&work[7], st_rebase);

@@ -46,7 +46,7 @@ class WorkloadDesc(ct.Structure):
                 ("sync_lo_ns", ct.c_int64), ("sync_hi_ns", ct.c_int64), ("jitter_ns", ct.c_int64),
                 ("inst_quantiles_q16", ct.c_void_p), ("kern_quantiles_q16", ct.c_void_p),
                 ("rt_bin_ns", ct.c_int64), ("rt_bins", ct.c_uint32), ("free_ns", ct.c_int64),
-                ("cpu_cores", ct.c_uint32), ("contention_permille", ct.c_uint32)]
+                ("cpu_cores", ct.c_uint32), ("contention_permille", ct.c_uint32), ("executors", ct.c_uint32)]
 
 
 class PolicyS(ct.Structure):
@@ -158,7 +158,7 @@ class DeviceWorkload:
         self.desc = WorkloadDesc(w.num_chains, chains, w.num_prio, w.launch_ns, w.launch_akb_ns, w.sync_lo_ns,
                                  w.sync_hi_ns, w.jitter_ns, None if inst is None else inst.ctypes.data,
                                  None if kern is None else kern.ctypes.data, w.rt_bin_ns, w.rt_bins, w.free_ns,
-                                 w.cpu_cores, w.contention_permille)
+                                 w.cpu_cores, w.contention_permille, w.executors)
         self._keep = (keep, chains, inst, kern)
         h = ct.c_void_p()
         _check(lib().urg_create_workload(ct.byref(self.desc), ct.byref(h)))

@@ -73,6 +73,19 @@ def test_validation_loci(L):
     assert "num_chains" in str(_create(w))
 
 
+def test_task_executor_limits(L):
+    """Per-task executors (R32): one lane per task, so at most 32 tasks; unknown modes refused."""
+    from workloads.spec import EXEC_TASK
+    w = paper11()                      # 22 tasks: accepted
+    w.executors = EXEC_TASK
+    w.chains = w.chains + w.chains[:6]   # 34 tasks
+    e = _create(w)
+    assert e.status == -2 and "per-task executors" in str(e)
+    w = paper11()
+    w.executors = 2
+    assert "executors" in str(_create(w))
+
+
 def test_cudafree_needs_positive_cost(L):
     from workloads import w6
     w = w6(False)
