@@ -18,6 +18,8 @@ run through the same C-ABI call (``urg_simulate_batch``) on the current CUDA dev
                       priorities (PAPER.md:386-399; DESIGN.md R29);
 * ``contention``   -- kernel slow-down from co-running kernels (PAPER.md:209-212; DESIGN.md R30);
 * ``memcpy``       -- H2D/D2H memcpys around every task on the copy engine (Table 3; DESIGN.md R31);
+* ``executors``    -- one thread per chain against one executor thread per task, tasks of
+                      successive instances pipelined (PAPER.md:272; DESIGN.md R32);
 * ``utilisation``  -- UrgenGo vs FIFO vs static priorities over an arrival-rate sweep
                       (BASELINE.json configs[2]; PAPER.md:679-683 fig:0_overall analogue).
 
@@ -32,7 +34,7 @@ from typing import Dict, List, Optional
 import numpy as np
 
 from workloads.spec import (COLL_BINS, EDF, F_BIND, F_COLLISIONS, F_DELAY, F_EARLY_EXIT, FIFO, HRRN, LCUF, SJF,
-                            STATIC, SYNC_ASYNC,
+                            EXEC_CHAIN, EXEC_TASK, STATIC, SYNC_ASYNC,
                             SYNC_BATCHED, SYNC_EACH, SYNC_OVERLAP, URGENGO, Batch, Policy, Workload,
                             collision_hist)
 
@@ -50,6 +52,7 @@ class Point:
     cores: Optional[int] = None             # workload override: CPU cores shared by the threads (R29)
     alpha: Optional[int] = None             # workload override: contention slow-down per-mille (R30)
     copies: bool = False                    # workload override: H2D/D2H memcpys around every task (R31)
+    executors: Optional[int] = None         # workload override: EXEC_CHAIN / EXEC_TASK (R32)
 
 
 @dataclass
@@ -133,6 +136,17 @@ def memcpy(base: Policy, b: Batch) -> List[Point]:
             for name, p in pols]
 
 
+def executors(base: Policy, b: Batch) -> List[Point]:
+    """PAPER.md:272 ("each task is executed by a dedicated thread"): the chain-thread model (R6)
+    against per-task executor threads with depth-1 hand-over (R32), under UrgenGo, static
+    priorities and FIFO."""
+    pols = [("UrgenGo", base), ("static (PAAM-like)", Policy(kind=STATIC, flags=0, sync_mode=SYNC_ASYNC)),
+            ("FIFO", Policy(kind=FIFO, flags=0, sync_mode=SYNC_ASYNC))]
+    return [Point(f"{lbl}, {name}", p, b, executors=e) for e, lbl in ((EXEC_CHAIN, "thread per chain"),
+                                                                    (EXEC_TASK, "executor per task"))
+            for name, p in pols]
+
+
 def with_copies(w: Workload, h2d_ns: int = 300_000, d2h_ns: int = 100_000) -> Workload:
     """A copy of w whose tasks start with an H2D and end with a D2H memcpy (R31)."""
     import copy
@@ -168,7 +182,7 @@ def utilisation(base: Policy, batches: List[Batch]) -> List[Point]:
 
 
 STUDIES = ("sync_modes", "delta_eval", "num_prio", "ablation", "collisions", "policies", "cudafree", "cpu_cores",
-           "contention", "memcpy")
+           "contention", "memcpy", "executors")
 
 
 def run(w: Workload, points: List[Point], stream=None) -> List[Result]:
@@ -179,10 +193,11 @@ def run(w: Workload, points: List[Point], stream=None) -> List[Result]:
     try:
         for pt in points:
             npri = pt.num_prio if pt.num_prio is not None else w.num_prio
-            key = (npri, pt.frees, pt.cores, pt.alpha, pt.copies)
+            key = (npri, pt.frees, pt.cores, pt.alpha, pt.copies, pt.executors)
             if key not in cache:
                 ww = replace(w, num_prio=npri, cpu_cores=pt.cores if pt.cores is not None else w.cpu_cores,
-                             contention_permille=pt.alpha if pt.alpha is not None else w.contention_permille)
+                             contention_permille=pt.alpha if pt.alpha is not None else w.contention_permille,
+                             executors=pt.executors if pt.executors is not None else w.executors)
                 if pt.copies:
                     ww = with_copies(ww)
                 cache[key] = DeviceWorkload(with_frees(ww, pt.frees) if pt.frees is not None else ww)

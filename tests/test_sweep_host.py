@@ -49,3 +49,12 @@ def test_workload_transforms():
     assert sorted({p.cores for p in pts}) == [0, 1, 2, 4, 8]
     assert sorted({p.alpha for p in SW.contention(get_config("paper11").policies["urgengo"],
                                                    get_config("paper11").batch)}) == [0, 250, 500, 1000, 2000]
+
+
+def test_executors_study():
+    from paper_2509_12207_b200 import sweep as SW
+    from workloads.spec import EXEC_CHAIN, EXEC_TASK
+    cfg = get_config("paper11")
+    pts = SW.executors(cfg.policies["urgengo"], cfg.batch)
+    assert [p.executors for p in pts] == [EXEC_CHAIN] * 3 + [EXEC_TASK] * 3
+    assert [p.policy.kind for p in pts[:3]] == [p.policy.kind for p in pts[3:]] == [2, 1, 0]

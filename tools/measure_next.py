@@ -22,21 +22,22 @@ out = {"workload": "paper11 (configs[1]) 1000 scenarios x 10 s", "rows": {}}
 dw = DeviceWorkload(w)
 
 
-def gpu_sim(p, reps=3):
-    agg = torch.zeros(dw.agg_words, dtype=torch.int64, device="cuda")
+def gpu_sim(p, reps=3, d=None):
+    d = d or dw
+    agg = torch.zeros(d.agg_words, dtype=torch.int64, device="cuda")
     ts = []
     for _ in range(reps + 1):
         agg.zero_()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(); dw.simulate(p, b, agg); e1.record(); torch.cuda.synchronize()
+        e0.record(); d.simulate(p, b, agg); e1.record(); torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
-    dw.check()
+    d.check()
     ms = sorted(ts[1:])[len(ts[1:]) // 2]
     return int(agg[-2].item()), ms
 
 
-def cpu_sim(p, n=2):
-    r = O.run(w, p, replace(b, scenario_count=n))
+def cpu_sim(p, n=2, wx=None):
+    r = O.run(wx or w, p, replace(b, scenario_count=n))
     return r.launches, r.seconds
 
 
@@ -49,6 +50,27 @@ variants = {
 for name, p in variants.items():
     L, ms = gpu_sim(p)
     cl, cs = cpu_sim(p)
+    out["rows"][name] = {"gpu_launch_events_per_s": L / ms * 1e3, "gpu_ms": ms, "launch_events": L,
+                         "oracle_1core_launch_events_per_s": cl / cs}
+    print(name, out["rows"][name], flush=True)
+
+# rows that change the workload (extended-model build)
+from paper_2509_12207_b200 import sweep as SW  # noqa: E402
+from workloads.spec import EXEC_TASK  # noqa: E402
+
+wvars = {
+    "EDF (R27)": (w, Policy(kind=3, flags=0, sync_mode=base.sync_mode)),
+    "cudaFree at the end of 2 tasks (R28)": (SW.with_frees(w, 2), base),
+    "8 shared CPU cores (R29)": (replace(w, cpu_cores=8), base),
+    "contention alpha 500 permille (R30)": (replace(w, contention_permille=500), base),
+    "H2D/D2H memcpys around every task (R31)": (SW.with_copies(w), base),
+    "per-task executors (R32)": (replace(w, executors=EXEC_TASK), base),
+}
+for name, (wx, p) in wvars.items():
+    d = DeviceWorkload(wx)
+    L, ms = gpu_sim(p, d=d)
+    d.close()
+    cl, cs = cpu_sim(p, wx=wx)
     out["rows"][name] = {"gpu_launch_events_per_s": L / ms * 1e3, "gpu_ms": ms, "launch_events": L,
                          "oracle_1core_launch_events_per_s": cl / cs}
     print(name, out["rows"][name], flush=True)

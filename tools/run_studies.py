@@ -35,6 +35,7 @@ studies = {
     "CPU cores (PAPER.md:386-399)": SW.cpu_cores(base, b),
     "contention (PAPER.md:209-212)": SW.contention(base, b),
     "memcpy (Table 3, PAPER.md:374)": SW.memcpy(base, b),
+    "executors (PAPER.md:272)": SW.executors(base, b),
 }
 cfg3 = get_config("usweep")
 studies["utilisation sweep (configs[2])"] = SW.utilisation(base, [replace(x, scenario_count=SU) for x in cfg3.sweep])
