@@ -98,6 +98,13 @@ typedef struct {
                                              the latest message only (depth 1; R32).  Needs
                                              sum(num_tasks) <= 32 (URG_ERANGE) and no CPU predictor
                                              (urg_policy.cpu_ma_window = 0, else URG_EINVAL at simulate) */
+    uint32_t num_variants;                /* template variants V >= 1 (0 reads as 1; <= 65536): scenario s
+                                             runs on kernel-record set s mod V (SURVEY.md §8(d) cfg 2
+                                             "64 templates"; R33).  Set 0 is the chains' own
+                                             kernels; the records of every set are read from HBM/L2 */
+    const urg_kernel_desc *variant_kernels; /* host, sets 1..V-1: (V-1) x sum(num_kernels) records,
+                                             chain-major like the chains' kernels; flags must equal the
+                                             chains' kernel flags (URG_EINVAL, locus variant_kernels[v][k]) */
 } urg_workload_desc;
 enum { URG_EXEC_CHAIN = 0, URG_EXEC_TASK = 1 };
 

@@ -51,6 +51,7 @@ class OrcInput(ct.Structure):
         ("inst_q16", ct.c_void_p), ("kern_q16", ct.c_void_p),
         ("rt_bin_ns", ct.c_int64), ("rt_bins", ct.c_uint32), ("free_ns", ct.c_int64), ("cpu_cores", ct.c_uint32),
         ("contention_permille", ct.c_uint32), ("task_exec", ct.c_uint32),
+        ("num_variants", ct.c_uint32),
         ("kind", ct.c_uint32), ("flags", ct.c_uint32), ("sync_mode", ct.c_uint32),
         ("delta_eval_ns", ct.c_int64), ("lax_threshold_ns", ct.c_int64), ("sleep_ns", ct.c_int64),
         ("util_exempt_permille", ct.c_uint32),
@@ -114,6 +115,7 @@ def _make_input(w: Workload, p: Policy, b: Batch):
         sync_lo_ns=w.sync_lo_ns, sync_hi_ns=w.sync_hi_ns, jitter_ns=w.jitter_ns,
         inst_q16=_ptr(inst), kern_q16=_ptr(kern), rt_bin_ns=w.rt_bin_ns, rt_bins=w.rt_bins, free_ns=w.free_ns,
         cpu_cores=w.cpu_cores, contention_permille=w.contention_permille, task_exec=w.executors,
+        num_variants=w.num_variants,
         kind=p.kind, flags=p.flags, sync_mode=p.sync_mode, delta_eval_ns=p.delta_eval_ns,
         lax_threshold_ns=p.lax_threshold_ns, sleep_ns=p.sleep_ns, util_exempt_permille=p.util_exempt_permille,
         noise_permille=p.noise_permille, cpu_ma_window=p.cpu_ma_window,

@@ -44,7 +44,7 @@ typedef struct {
     const uint32_t *ch_ntasks, *ch_cpu_sigma, *ch_gpu_sigma;
     const uint32_t *t_cpu_nom, *t_cpu_est, *t_nk;   /* all tasks, chain-major */
     const uint32_t *t_flags;                        /* bit 0: the task ends with cudaFree (R28) */
-    const uint32_t *k_nom, *k_est;                  /* all kernels, chain-major */
+    const uint32_t *k_nom, *k_est;                  /* all kernels, chain-major; num_variants sets */
     const uint16_t *k_util;
     const uint16_t *k_flags;        /* bit 0: the operation is a memcpy on the copy engine (R31) */
     uint32_t num_prio;
@@ -57,6 +57,7 @@ typedef struct {
     uint32_t cpu_cores;         /* CPU cores shared by the chains' threads, 0 = one per thread (R29) */
     uint32_t contention_permille; /* alpha: kernel slow-down per unit of co-running utilisation (R30) */
     uint32_t task_exec;         /* 1: one executor thread per task, hand-over by message (R32) */
+    uint32_t num_variants;      /* kernel-record sets; scenario s uses set s mod num_variants (R33) */
     /* policy */
     uint32_t kind, flags, sync_mode;
     int64_t delta_eval_ns, lax_threshold_ns, sleep_ns;
@@ -1000,10 +1001,21 @@ static void cal_sample(orc_sim *S)
 }
 
 /* Simulate scenario s.  Returns 0 on success. */
-static int sim_scenario(const orc_input *in, uint64_t s, uint32_t *rec, int64_t *agg,
+static int sim_scenario(const orc_input *in_all, uint64_t s, uint32_t *rec, int64_t *agg,
                         int64_t *trace, int64_t trace_cap, int64_t *trace_len,
                         int64_t *cal_L, int64_t cal_cap, int64_t *cal_n, int64_t cal_end)
 {
+    /* template variants (R33): scenario s runs on kernel-record set s mod V */
+    orc_input in_v = *in_all;
+    const orc_input *in = &in_v;
+    if (in_all->num_variants > 1) {
+        uint64_t nk = 0, nt = 0;
+        for (uint32_t c = 0; c < in_all->num_chains; ++c) nt += in_all->ch_ntasks[c];
+        for (uint64_t j = 0; j < nt; ++j) nk += in_all->t_nk[j];
+        uint64_t off = (s % in_all->num_variants) * nk;
+        in_v.k_nom += off; in_v.k_est += off; in_v.k_util += off;
+        if (in_v.k_flags) in_v.k_flags += off;
+    }
     orc_sim S;
     memset(&S, 0, sizeof S);
     S.in = in; S.s = s; S.C = in->num_chains; S.agg = agg;

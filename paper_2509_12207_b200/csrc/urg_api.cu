@@ -45,6 +45,10 @@ struct urg_workload {
     bool has_copy = false;            // some operation is a memcpy (R31)
     uint32_t num_lanes = 0;           // simulated threads: chains, or tasks under per-task executors (R32)
     bool task_exec = false;
+    uint32_t num_variants = 1, nk_total = 0;   // template variants (R33) and kernels per variant
+    UrgKernRec *d_kern = nullptr;     // HBM: [num_variants][nk_total] kernel records
+    UrgVarRec *d_var = nullptr;       // HBM: [num_variants][num_lanes] estimate totals
+    uint64_t kern_bytes = 0;
 };
 
 static thread_local std::string g_err;
@@ -97,6 +101,9 @@ extern "C" urg_status urg_create_workload(const urg_workload_desc *d, urg_worklo
     if (d->cpu_cores > 32) return fail(URG_EINVAL, "cpu_cores must be <= 32 (0 = one core per chain thread)");
     if (d->contention_permille > 100000) return fail(URG_EINVAL, "contention_permille must be <= 100000");
     if (d->executors > URG_EXEC_TASK) return fail(URG_EINVAL, "executors must be URG_EXEC_CHAIN or URG_EXEC_TASK");
+    const uint32_t n_var = d->num_variants ? d->num_variants : 1u;
+    if (n_var > 65536) return fail(URG_EINVAL, "num_variants must be <= 65536");
+    if (n_var > 1 && !d->variant_kernels) return fail(URG_EINVAL, "variant_kernels must not be NULL when num_variants > 1");
 
     uint32_t n_tasks = 0, n_kern = 0;
     for (uint32_t c = 0; c < d->num_chains && d->chains; ++c)
@@ -130,6 +137,23 @@ extern "C" urg_status urg_create_workload(const urg_workload_desc *d, urg_worklo
         }
         n_tasks += ch.num_tasks;
     }
+    // template variants (R33): every set has the chains' structure; memcpy flags are structural
+    if ((uint64_t)n_var * n_kern >= (1ull << 31))
+        return fail(URG_ERANGE, "num_variants x kernels = %llu kernel records exceeds 2^31",
+                    (unsigned long long)n_var * n_kern);
+    for (uint32_t v = 1, g = 0; v < n_var; ++v, g = 0)
+        for (uint32_t c = 0; c < d->num_chains; ++c)
+            for (uint32_t j = 0; j < d->chains[c].num_tasks; ++j)
+                for (uint32_t k = 0; k < d->chains[c].tasks[j].num_kernels; ++k, ++g) {
+                    const urg_kernel_desc &kd = d->variant_kernels[(uint64_t)(v - 1) * n_kern + g];
+                    if (kd.nominal_ns == 0)
+                        return fail(URG_EINVAL, "variant_kernels[%u][%u].nominal_ns must be > 0", v, g);
+                    if (kd.util_permille > 1000)
+                        return fail(URG_EINVAL, "variant_kernels[%u][%u].util_permille must be <= 1000", v, g);
+                    if (kd.flags != d->chains[c].tasks[j].kernels[k].flags)
+                        return fail(URG_EINVAL, "variant_kernels[%u][%u].flags must equal the chains' kernel flags",
+                                    v, g);
+                }
     const bool te = d->executors == URG_EXEC_TASK;
     const uint32_t n_lanes = te ? n_tasks : d->num_chains;
     if (n_lanes > 32)
@@ -144,7 +168,7 @@ extern "C" urg_status urg_create_workload(const urg_workload_desc *d, urg_worklo
     uint32_t off = align16(sizeof(UrgBlobHeader));
     h.off_chains = off; off = align16(off + n_lanes * (uint32_t)sizeof(UrgChainRec));
     h.off_tasks = off;  off = align16(off + n_tasks * (uint32_t)sizeof(UrgTaskRec));
-    h.off_kerns = off;  off = align16(off + n_kern * (uint32_t)sizeof(UrgKernRec));
+    h.off_kerns = 0;    // kernel records are read from global memory (R33), not staged
     if (d->inst_quantiles_q16) { h.off_inst_q = off; off = align16(off + URG_QTABLE * 4); }
     if (d->kern_quantiles_q16) { h.off_kern_q = off; off = align16(off + URG_QTABLE * 4); }
     h.total_bytes = off;
@@ -162,11 +186,13 @@ extern "C" urg_status urg_create_workload(const urg_workload_desc *d, urg_worklo
     w->cpu_cores = d->cpu_cores;
     w->alpha_pm = d->contention_permille;
     w->num_lanes = n_lanes; w->task_exec = te;
+    w->num_variants = n_var; w->nk_total = n_kern;
+    std::vector<UrgKernRec> krs((size_t)n_var * n_kern);
+    std::vector<UrgVarRec> vrs((size_t)n_var * n_lanes);
     w->blob.assign(off, 0);
     memcpy(w->blob.data(), &h, sizeof h);
     UrgChainRec *chs = (UrgChainRec *)(w->blob.data() + h.off_chains);
     UrgTaskRec *tks = (UrgTaskRec *)(w->blob.data() + h.off_tasks);
-    UrgKernRec *krs = (UrgKernRec *)(w->blob.data() + h.off_kerns);
     uint32_t tb = 0, kb = 0, lane = 0;
     for (uint32_t c = 0; c < d->num_chains; ++c) {
         const urg_chain_desc &ch = d->chains[c];
@@ -179,6 +205,8 @@ extern "C" urg_status urg_create_workload(const urg_workload_desc *d, urg_worklo
             r.num_tasks = ch.num_tasks; r.task_base = tb; r.num_kernels = n_local;
             r.kern_base = kb; r.cpu_sigma_ppm = ch.cpu_sigma_ppm; r.gpu_sigma_ppm = ch.gpu_sigma_ppm;
             r.chain_id = c; r.stage = te ? j : 0; r.stage_end = te ? j + 1 : ch.num_tasks; r.k_first = k_first;
+            r.cpu_est_total = 0;
+            for (uint32_t q = r.stage; q < ch.num_tasks; ++q) r.cpu_est_total += ch.tasks[q].cpu_estimate_ns;
         }
         uint32_t local = 0;
         for (uint32_t j = 0; j < ch.num_tasks; ++j) {
@@ -194,10 +222,28 @@ extern "C" urg_status urg_create_workload(const urg_workload_desc *d, urg_worklo
             local += t.num_kernels;
         }
         if (ch.num_tasks > w->max_tasks) w->max_tasks = ch.num_tasks;
+        for (uint32_t v = 1; v < n_var; ++v)
+            for (uint32_t k = 0; k < local; ++k) {
+                const urg_kernel_desc &kd = d->variant_kernels[(uint64_t)(v - 1) * n_kern + kb + k];
+                krs[(size_t)v * n_kern + kb + k] = UrgKernRec{kd.nominal_ns, kd.estimate_ns, kd.util_permille, kd.flags};
+            }
         tb += ch.num_tasks; kb += local;
         w->period.push_back(ch.period_ns);
         w->deadline.push_back(ch.deadline_ns);
     }
+    // per (variant, thread) estimate totals: Eq. 2's kernel sum from the thread's first kernel, and the
+    // chain's total (LCUF, R27)
+    for (uint32_t v = 0; v < n_var; ++v)
+        for (uint32_t l = 0; l < n_lanes; ++l) {
+            const UrgChainRec &r = chs[l];
+            int64_t g = 0, gc = 0;
+            for (uint32_t k = 0; k < r.num_kernels; ++k) {
+                const int64_t e = krs[(size_t)v * n_kern + r.kern_base + k].estimate_ns;
+                gc += e;
+                if (k >= r.k_first) g += e;
+            }
+            vrs[(size_t)v * n_lanes + l] = UrgVarRec{g, gc};
+        }
     if (d->inst_quantiles_q16) memcpy(w->blob.data() + h.off_inst_q, d->inst_quantiles_q16, URG_QTABLE * 4);
     if (d->kern_quantiles_q16) memcpy(w->blob.data() + h.off_kern_q, d->kern_quantiles_q16, URG_QTABLE * 4);
 
@@ -207,9 +253,17 @@ extern "C" urg_status urg_create_workload(const urg_workload_desc *d, urg_worklo
     if ((e = cudaMalloc(&w->d_blob, off)) != cudaSuccess) { delete w; return fail(URG_ENOMEM, "cudaMalloc(blob)"); }
     if ((e = cudaMalloc(&w->d_work, 64)) != cudaSuccess) { cudaFree(w->d_blob); delete w; return fail(URG_ENOMEM, "cudaMalloc(work)"); }
     w->d_err = (long long *)(w->d_work + 2);
+    w->kern_bytes = (uint64_t)krs.size() * sizeof(UrgKernRec);
+    if ((e = cudaMalloc(&w->d_kern, w->kern_bytes)) != cudaSuccess ||
+        (e = cudaMalloc(&w->d_var, vrs.size() * sizeof(UrgVarRec))) != cudaSuccess) {
+        cudaFree(w->d_blob); cudaFree(w->d_work); cudaFree(w->d_kern); delete w;
+        return fail(URG_ENOMEM, "cudaMalloc(kernel records)");
+    }
     if ((e = cudaMemcpy(w->d_blob, w->blob.data(), off, cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaMemcpy(w->d_kern, krs.data(), w->kern_bytes, cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaMemcpy(w->d_var, vrs.data(), vrs.size() * sizeof(UrgVarRec), cudaMemcpyHostToDevice)) != cudaSuccess ||
         (e = cudaMemset(w->d_work, 0, 64)) != cudaSuccess) {
-        cudaFree(w->d_blob); cudaFree(w->d_work); delete w;
+        cudaFree(w->d_blob); cudaFree(w->d_work); cudaFree(w->d_kern); cudaFree(w->d_var); delete w;
         return cuda_fail(e, "copying the template to the device");
     }
     *out = w;
@@ -221,6 +275,8 @@ extern "C" void urg_destroy_workload(urg_workload *w)
     if (!w) return;
     cudaFree(w->d_blob);
     cudaFree(w->d_work);
+    cudaFree(w->d_kern);
+    cudaFree(w->d_var);
     delete w;
 }
 
@@ -231,7 +287,7 @@ extern "C" uint64_t urg_agg_words(const urg_workload *w)
 
 extern "C" uint64_t urg_template_bytes(const urg_workload *w)
 {
-    return w ? (uint64_t)w->blob.size() : 0;
+    return w ? (uint64_t)w->blob.size() + w->kern_bytes : 0;
 }
 
 static urg_status validate_call(const urg_workload *w, const urg_policy *p, const urg_batch *b)
@@ -267,6 +323,7 @@ static void fill_params(const urg_workload *w, const urg_policy *p, const urg_ba
 {
     memset(&P, 0, sizeof P);
     P.num_chains = w->num_chains; P.num_lanes = w->num_lanes; P.task_exec = w->task_exec ? 1u : 0u;
+    P.kern = w->d_kern; P.var = w->d_var; P.nk_total = w->nk_total; P.num_variants = w->num_variants;
     P.num_prio = w->num_prio; P.rt_bins = w->rt_bins;
     P.agg_stride = 5 + w->rt_bins + 101;
     P.launch_ns = w->launch_ns; P.launch_akb_ns = w->launch_akb_ns;

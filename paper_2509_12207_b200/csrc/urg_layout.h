@@ -14,7 +14,7 @@
 
 enum { URG_TAG_ARR = 1, URG_TAG_TIGHT = 2, URG_TAG_INST = 3, URG_TAG_KERN = 4, URG_TAG_SYNC = 5, URG_TAG_NOISE = 6 };
 
-struct __align__(16) UrgChainRec {     // 96 B, one per thread (lane): a chain, or one task of it (R32)
+struct __align__(16) UrgChainRec {     // 80 B, one per thread (lane): a chain, or one task of it (R32)
     int64_t period_ns, deadline_ns, offset_ns;
     uint32_t num_tasks, task_base;     // the chain's tasks [task_base, task_base + num_tasks)
     uint32_t num_kernels, kern_base;   // the chain's kernels [kern_base, kern_base + num_kernels)
@@ -22,10 +22,13 @@ struct __align__(16) UrgChainRec {     // 96 B, one per thread (lane): a chain, 
     uint32_t chain_id;                 // chain of this thread (randomness, records)
     uint32_t stage, stage_end;         // tasks [stage, stage_end) it runs per instance
     uint32_t k_first;                  // chain-local index of the first kernel of task `stage`
-    int64_t gpu_est_total;             // filled in-kernel at staging: estimates of kernels >= k_first
-    int64_t cpu_est_total;             // filled in-kernel at staging: estimates of tasks >= stage
-    int64_t gpu_est_chain;             // filled in-kernel at staging: all kernel estimates of the chain
+    int64_t cpu_est_total;             // CPU estimates of tasks >= stage (Eq. 2 start value)
     int64_t pad_;
+};
+
+struct __align__(16) UrgVarRec {       // 16 B, per (template variant, thread), global memory (R33)
+    int64_t gpu_est_total;             // kernel estimates of the variant from k_first on (Eq. 2 start value)
+    int64_t gpu_est_chain;             // all kernel estimates of the chain in the variant (LCUF key, R27)
 };
 
 struct __align__(16) UrgTaskRec {      // 16 B
@@ -56,6 +59,11 @@ struct UrgSimParams {
     uint32_t fa_num, fa_den, fd_num, fd_den, ftight_permille, tight_explicit, tight_mask;
     // threads: num_lanes = num_chains, or the number of tasks with per-task executors (R32)
     uint32_t num_lanes, task_exec;
+    // template variants (R33): [num_variants][nk_total] kernel records and [num_variants][num_lanes]
+    // estimate totals, global memory
+    const UrgKernRec *kern;
+    const UrgVarRec *var;
+    uint32_t nk_total, num_variants;
     // staging
     uint32_t blob_bytes, snap_offset, mbar_offset, smem_bytes;
     // estimation noise (R25) and CPU moving-average predictor (R26)

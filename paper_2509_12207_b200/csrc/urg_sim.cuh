@@ -115,10 +115,32 @@ __device__ __forceinline__ void stage_blob(uint8_t *dst, const uint8_t *src, uin
 struct Tmpl {   // shared-memory views of the staged template
     const UrgChainRec *ch;
     const UrgTaskRec *task;
-    const UrgKernRec *kern;
     const int32_t *inst_q;
     const uint32_t *kern_q;
 };
+
+// One kernel record from HBM/L2 (read-only path, one 16-byte load).  The records of all
+// template variants live in global memory (R33); a CTA's warps work on scenarios of the
+// same variant at the same time (grouped work order), so the record lines stay in L1.
+__device__ __forceinline__ UrgKernRec kern_rec(const UrgKernRec *k)
+{
+    const uint4 q = __ldg(reinterpret_cast<const uint4 *>(k));
+    UrgKernRec r;
+    r.nominal_ns = q.x; r.estimate_ns = q.y; r.util_permille = q.z; r.flags = q.w;
+    return r;
+}
+
+// Work index -> scenario offset, grouping the scenarios of one template variant (offsets o with
+// (begin + o) mod V fixed) into consecutive work indices (R33).  Identity when V = 1.
+__device__ __forceinline__ uint64_t work_offset(uint64_t j, uint64_t S, uint32_t V)
+{
+    if (V <= 1) return j;
+    const uint64_t q = S / V, m = S % V;
+    uint64_t g, r;
+    if (j < m * (q + 1)) { g = j / (q + 1); r = j % (q + 1); }
+    else { const uint64_t jj = j - m * (q + 1); g = m + jj / q; r = jj % q; }
+    return g + r * V;
+}
 
 // One instantiation per (policy kind, UrgenGo flags, per-kernel factor table present):
 // the policy is uniform over a launch, so its branches are resolved at compile time
@@ -149,7 +171,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                long long *__restrict__ err)
 {
     extern __shared__ __align__(128) uint8_t sm[];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
     // ---- A0: template staging (once per CTA) ----
     stage_blob(sm, blob, P.blob_bytes, (uint64_t *)(sm + P.mbar_offset));
@@ -158,31 +180,10 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
     Tmpl T;
     T.ch = chs;
     T.task = (const UrgTaskRec *)(sm + hdr->off_tasks);
-    T.kern = (const UrgKernRec *)(sm + hdr->off_kerns);
     T.inst_q = hdr->off_inst_q ? (const int32_t *)(sm + hdr->off_inst_q) : nullptr;
     T.kern_q = hdr->off_kern_q ? (const uint32_t *)(sm + hdr->off_kern_q) : nullptr;
     const uint32_t C = P.num_lanes;    // threads: chains, or tasks under per-task executors (R32)
     const uint32_t NC = P.num_chains;  // chains: records and aggregates
-    // per-thread totals of the estimates from its first task on (the remaining-work sums of Eq. 2
-    // start from them)
-    for (uint32_t c = warp; c < C; c += nwarps) {
-        int64_t g = 0, cp = 0, gc = 0;
-        for (uint32_t k = lane; k < chs[c].num_kernels; k += 32) {
-            const int64_t e = T.kern[chs[c].kern_base + k].estimate_ns;
-            gc += e;
-            if (k >= chs[c].k_first) g += e;
-        }
-        for (uint32_t j = chs[c].stage + lane; j < chs[c].num_tasks; j += 32)
-            cp += T.task[chs[c].task_base + j].cpu_estimate_ns;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            g += (int64_t)__shfl_xor_sync(FULL, (unsigned long long)g, o);
-            cp += (int64_t)__shfl_xor_sync(FULL, (unsigned long long)cp, o);
-            gc += (int64_t)__shfl_xor_sync(FULL, (unsigned long long)gc, o);
-        }
-        if (lane == 0) { chs[c].gpu_est_total = g; chs[c].cpu_est_total = cp; chs[c].gpu_est_chain = gc; }
-    }
-    __syncthreads();
 
     // per-warp Phase B snapshot (R21): last laxity of each lane, then its stream level
     // per-warp Phase B snapshot (R21), 1 KB: last laxity, two policy keys, stream level
@@ -261,7 +262,12 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         if (jw >= P.scenario_count) break;
         jw += (unsigned long long)half;                        // PK: the upper half takes the next one
         const bool valid = valid_c && jw < P.scenario_count;
+        if (jw < P.scenario_count) jw = work_offset(jw, P.scenario_count, P.num_variants);
         const uint32_t s = (uint32_t)(P.scenario_begin + jw);
+        // R33: this scenario's template variant -- its kernel records and estimate totals
+        const uint32_t vidx = P.num_variants > 1 ? s % P.num_variants : 0u;
+        const UrgKernRec *KR = P.kern + (size_t)vidx * P.nk_total + kbase;
+        const UrgVarRec *VR = P.var + (size_t)vidx * C + (valid_c ? c : 0u);
 
         // ---- A1: scenario init (R3, R15 STATIC) ----
         int64_t Pp = 0, Dp = 0;
@@ -366,7 +372,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         auto cls_key_a = [&]() -> int64_t {
             return KIND == K_EDF ? t_arr + Dp : KIND == K_HRRN ? t_arr : KIND == K_LCUF ? Pp : 0;
         };
-        auto cls_key_b = [&]() -> int64_t { return KIND == K_LCUF ? CRF(gpu_est_chain) : rem_g + rem_c; };
+        auto cls_key_b = [&]() -> int64_t { return KIND == K_LCUF ? VR->gpu_est_chain : rem_g + rem_c; };
         // "chain o ranks before chain s" (ties by smaller chain id; exact 128-bit ratios)
         auto cls_before = [&](int64_t oA, int64_t oB, int o, int64_t sA, int64_t sB, int sl, int64_t t) -> bool {
             if (KIND == K_EDF || KIND == K_SJF) {
@@ -416,8 +422,9 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             head_end = INF64;
             if (launched > done) {
                 head_ready = t;
-                head_u = T.kern[kbase + done].util_permille;
-                if (has_copy) head_copy = T.kern[kbase + done].flags & 1u;
+                const UrgKernRec kr = kern_rec(KR + done);
+                head_u = kr.util_permille;
+                if (has_copy) head_copy = kr.flags & 1u;
             }
             if (pc == PC_SYNC_WAIT && done >= sync_target) { pc = PC_SYNC_RET; cpu_busy(t, sync_cost); }
         };
@@ -425,7 +432,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         auto start_head = [&](int64_t t, uint32_t u_run) {
             uint64_t G = 65536u;
             if (KQ) G = T.kern_q[rng_word(P.seed, s, URG_TAG_KERN, cid, inst, done) >> 20];
-            uint64_t d = ((((uint64_t)T.kern[kbase + done].nominal_ns * Fg) >> 16) * G) >> 16;
+            uint64_t d = ((((uint64_t)kern_rec(KR + done).nominal_ns * Fg) >> 16) * G) >> 16;
             d = d < 1 ? 1 : (d > 0xFFFFFFFFull ? 0xFFFFFFFFull : d);
             if (contend && !head_copy) d += d * (uint64_t)P.alpha_pm * u_run / 1000000ull;   // R30
             head_util = head_copy ? 0u : head_u;   // a memcpy uses the copy engine, not the SMs (R31)
@@ -485,7 +492,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     Fg = inst_factor(rng_word(P.seed, s, URG_TAG_INST, cid, inst, 0), CRF(gpu_sigma_ppm));
                     Fc = inst_factor(rng_word(P.seed, s, URG_TAG_INST, cid, inst, 1), CRF(cpu_sigma_ppm));
                     task = stage; launched = k_first; done = k_first; sync_ord = stage << 16;
-                    rem_g = CRF(gpu_est_total); rem_c = CRF(cpu_est_total);
+                    rem_g = VR->gpu_est_total; rem_c = CRF(cpu_est_total);
                     if (ma) {   // R26: this instance's ~E^cpu_j, floor mean of the last min(W, h_j) measurements
                         rem_c = 0;
                         for (uint32_t j = 0; j < CRF(num_tasks); ++j) {
@@ -552,7 +559,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                 }
                 if (pc == PC_ENQUEUE) {   // the kernel reaches its stream (R16) + sync decision (R17)
                     const uint32_t n = launched;
-                    const UrgKernRec kr = T.kern[kbase + n];
+                    const UrgKernRec kr = kern_rec(KR + n);
                     const int64_t est = kr.estimate_ns;
                     if (launched == done) {   // stream was empty: head now
                         head_ready = t; head_u = kr.util_permille; newhead = true;
@@ -618,7 +625,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     if (urg) { lax = laxity(t); L_last = lax; }
                     const bool own_urgent = lax >= 0 && lax <= P.lax_threshold_ns;
                     if (f_delay && !own_urgent && (urgent_m & ~(1u << lane)) &&
-                        T.kern[kbase + launched].util_permille >= P.util_exempt) {
+                        kern_rec(KR + launched).util_permille >= P.util_exempt) {
                         pc = PC_ATTEMPT;
                         cpu_next = t + P.sleep_ns;
                         break;

@@ -46,7 +46,11 @@ class WorkloadDesc(ct.Structure):
                 ("sync_lo_ns", ct.c_int64), ("sync_hi_ns", ct.c_int64), ("jitter_ns", ct.c_int64),
                 ("inst_quantiles_q16", ct.c_void_p), ("kern_quantiles_q16", ct.c_void_p),
                 ("rt_bin_ns", ct.c_int64), ("rt_bins", ct.c_uint32), ("free_ns", ct.c_int64),
-                ("cpu_cores", ct.c_uint32), ("contention_permille", ct.c_uint32), ("executors", ct.c_uint32)]
+                ("cpu_cores", ct.c_uint32), ("contention_permille", ct.c_uint32), ("executors", ct.c_uint32),
+                ("num_variants", ct.c_uint32), ("variant_kernels", ct.c_void_p)]
+
+# urg_kernel_desc as a numpy record (12 B: u32 nominal, u32 estimate, u16 util, u16 flags)
+_KDESC = np.dtype([("nominal_ns", "<u4"), ("estimate_ns", "<u4"), ("util_permille", "<u2"), ("flags", "<u2")])
 
 
 class PolicyS(ct.Structure):
@@ -155,11 +159,16 @@ class DeviceWorkload:
                                    ch.cpu_sigma_ppm, ch.gpu_sigma_ppm)
         inst = None if w.inst_quantiles_q16 is None else np.ascontiguousarray(w.inst_quantiles_q16, np.int32)
         kern = None if w.kern_quantiles_q16 is None else np.ascontiguousarray(w.kern_quantiles_q16, np.uint32)
+        var = None
+        if w.kernel_variants:   # template variants 1..V-1 (R33), chain-major records
+            var = np.array([(k.nominal_ns, k.estimate_ns, k.util_permille, k.flags)
+                            for v in w.kernel_variants for k in v], dtype=_KDESC)
         self.desc = WorkloadDesc(w.num_chains, chains, w.num_prio, w.launch_ns, w.launch_akb_ns, w.sync_lo_ns,
                                  w.sync_hi_ns, w.jitter_ns, None if inst is None else inst.ctypes.data,
                                  None if kern is None else kern.ctypes.data, w.rt_bin_ns, w.rt_bins, w.free_ns,
-                                 w.cpu_cores, w.contention_permille, w.executors)
-        self._keep = (keep, chains, inst, kern)
+                                 w.cpu_cores, w.contention_permille, w.executors, w.num_variants,
+                                 None if var is None else var.ctypes.data)
+        self._keep = (keep, chains, inst, kern, var)
         h = ct.c_void_p()
         _check(lib().urg_create_workload(ct.byref(self.desc), ct.byref(h)))
         self.handle = h

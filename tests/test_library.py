@@ -86,6 +86,19 @@ def test_task_executor_limits(L):
     assert "executors" in str(_create(w))
 
 
+def test_template_variant_validation(L):
+    """Template variants (R33): records validated with their locus; memcpy flags are structural."""
+    from workloads.spec import Kernel as K
+    w = toy2()
+    n = w.total_kernels()
+    w.kernel_variants = [[K(1000, 1000, 500) for _ in range(n)] for _ in range(2)]
+    w.kernel_variants[1][7] = K(0, 1000, 500)
+    e = _create(w)
+    assert e.status == -1 and "variant_kernels[2][7].nominal_ns" in str(e)
+    w.kernel_variants[1][7] = K(1000, 1000, 500, 1)
+    assert "variant_kernels[2][7].flags" in str(_create(w))
+
+
 def test_cudafree_needs_positive_cost(L):
     from workloads import w6
     w = w6(False)
@@ -97,8 +110,8 @@ def test_cudafree_needs_positive_cost(L):
 def test_template_over_shared_memory_budget(L):
     """A template larger than the shared-memory budget is refused with URG_ERANGE before any
     device work (SURVEY.md §8(b) 'template larger than the smem budget -> URG_ERANGE')."""
-    ks = [Kernel(1000, 1000, 500)] * 10_500          # 10.5k kernel records x 16 B > 160 KB
-    w = Workload(chains=[Chain(100_000_000, 50_000_000, 0, [Task(1000, 1000, ks)])])
+    tasks = [Task(1000, 1000, [Kernel(1000, 1000, 500)])] * 10_500   # 10.5k task records x 16 B > 160 KB
+    w = Workload(chains=[Chain(100_000_000, 50_000_000, 0, tasks)])
     e = _create(w)
     assert e.status == -2 and "shared memory" in str(e)
 

@@ -78,6 +78,9 @@ class Workload:
     cpu_cores: int = 0                 # cores shared by the chains' threads, 0 = one each (8; R29)
     contention_permille: int = 0       # kernel slow-down per co-running utilisation (R30)
     executors: int = EXEC_CHAIN        # EXEC_TASK: one thread per task, depth-1 hand-over (R32)
+    # template variants (R33): kernel-record sets 1..V-1, each a chain-major list of
+    # total_kernels() records of the same structure; scenario s uses set s mod V (set 0 = the chains')
+    kernel_variants: Optional[List[List[Kernel]]] = None
 
     @property
     def num_chains(self) -> int:
@@ -85,6 +88,10 @@ class Workload:
 
     def total_kernels(self) -> int:
         return sum(len(t.kernels) for c in self.chains for t in c.tasks)
+
+    @property
+    def num_variants(self) -> int:
+        return 1 + len(self.kernel_variants or [])
 
     def flat(self) -> dict:
         """Flatten to SoA numpy arrays (chains, then tasks in chain order, then kernels)."""
@@ -100,6 +107,12 @@ class Workload:
                 for k in t.kernels:
                     k_nom.append(k.nominal_ns); k_est.append(k.estimate_ns)
                     k_util.append(k.util_permille); k_flags.append(k.flags)
+        n0 = len(k_nom)
+        for var in self.kernel_variants or []:
+            assert len(var) == n0, "every kernel variant has one record per kernel of the chains"
+            for k in var:
+                k_nom.append(k.nominal_ns); k_est.append(k.estimate_ns)
+                k_util.append(k.util_permille); k_flags.append(k.flags)
         return dict(
             ch_period=np.asarray(ch_period, np.int64), ch_deadline=np.asarray(ch_deadline, np.int64),
             ch_offset=np.asarray(ch_offset, np.int64), ch_ntasks=np.asarray(ch_ntasks, np.uint32),

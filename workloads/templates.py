@@ -20,6 +20,8 @@ from __future__ import annotations
 
 from typing import List, Sequence
 
+import functools
+
 import numpy as np
 
 from .quantiles import inst_z_table
@@ -104,6 +106,24 @@ def paper11(template_seed: int = 0x5EED0002, chains: Sequence[int] = tuple(range
                              cpu_sigma_ppm=int(round(scpu / ecpu * 1e6)),
                              gpu_sigma_ppm=int(round(sgpu / egpu * 1e6))))
     return Workload(chains=out, inst_quantiles_q16=inst_z_table())
+
+
+def paper11_variants(num_variants: int = 64, template_seed: int = 0x5EED0002,
+                     chains: Sequence[int] = tuple(range(11))) -> Workload:
+    """paper11 with num_variants kernel-record sets (SURVEY.md §8(d) cfg 2: "64 templates, scenario s
+    uses template s mod 64"; R33): set v is the kernel synthesis of template seed
+    template_seed + v -- same chains, tasks, kernel counts and per-task totals, different per-kernel
+    durations and utilisations.  Set 0 is paper11(template_seed)."""
+    w = paper11(template_seed, chains)
+    w.kernel_variants = [[Kernel(*r) for r in _kernel_rows(template_seed + v, tuple(chains))]
+                         for v in range(1, num_variants)]
+    return w
+
+
+@functools.lru_cache(maxsize=256)
+def _kernel_rows(template_seed: int, chains: tuple) -> tuple:
+    return tuple((k.nominal_ns, k.estimate_ns, k.util_permille, k.flags)
+                 for ch in paper11(template_seed, chains).chains for t in ch.tasks for k in t.kernels)
 
 
 def toy2() -> Workload:
