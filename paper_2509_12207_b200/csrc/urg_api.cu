@@ -367,6 +367,14 @@ static urg_status geometry(const urg_workload *w, const void *fn, uint64_t count
     const uint64_t resident = (uint64_t)w->num_sms * (uint64_t)per_sm;
     ctas = (int)(blocks_needed < resident ? blocks_needed : resident);
     if (ctas < 1) ctas = 1;
+    {   // leave the rest of the SM's 256 KB to L1: the kernel records of the template variants are
+        // read through it (R33); shared memory only for the CTAs an SM actually holds
+        const uint64_t per_sm_used = ((uint64_t)ctas + w->num_sms - 1) / w->num_sms;
+        uint64_t pct = (100ull * per_sm_used * (smem + 1024u) + 228u * 1024u - 1) / (228u * 1024u);
+        if (pct > 100) pct = 100;
+        CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, (int)pct),
+                 "cudaFuncSetAttribute(carveout)");
+    }
     return URG_OK;
 }
 

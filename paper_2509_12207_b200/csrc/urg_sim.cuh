@@ -187,10 +187,11 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
 
     // per-warp Phase B snapshot (R21): last laxity of each lane, then its stream level
     // per-warp Phase B snapshot (R21), 1 KB: last laxity, two policy keys, stream level
-    int64_t *snapL = (int64_t *)(sm + P.snap_offset) + warp * 128;
+    int64_t *snapL = (int64_t *)(sm + P.snap_offset) + warp * (URG_SNAP_BYTES_PER_LANE * 32 / 8);
     int64_t *snapA = snapL + 32, *snapB = snapL + 64;
     uint32_t *snapLev = (uint32_t *)(snapL + 96);
     uint32_t *mbox = (uint32_t *)(snapL + 112);   // R32: message published to each lane this round
+    UrgVarRec *myvar = (UrgVarRec *)(snapL + 128);  // R33: each lane's variant estimate totals
     constexpr bool urg = KIND == K_URGENGO;
     constexpr bool cls = KIND >= K_EDF;        // classical policies (R27): AKB-tracking, no urgency
     constexpr bool akb_on = urg || cls;
@@ -255,9 +256,16 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
     const uint32_t stage = EXT ? cr.stage : 0u, k_first = EXT ? cr.k_first : 0u;
     const bool last_stage = !EXT || cr.stage_end == cr.num_tasks;
 
+    bool first_fetch = true;
     for (;;) {
+        // work fetch: the first scenario of every warp is static (consecutive within a CTA, so a
+        // CTA's warps share template variants, R33), later ones come from one atomic counter
         unsigned long long jw = 0;
-        if (lane == 0) jw = atomicAdd(work, PK ? 2ull : 1ull);
+        const unsigned long long per_fetch = PK ? 2ull : 1ull;
+        if (lane == 0)
+            jw = first_fetch ? ((unsigned long long)blockIdx.x * (blockDim.x >> 5) + warp) * per_fetch
+                             : (unsigned long long)gridDim.x * (blockDim.x >> 5) * per_fetch + atomicAdd(work, per_fetch);
+        first_fetch = false;
         jw = __shfl_sync(FULL, jw, 0);
         if (jw >= P.scenario_count) break;
         jw += (unsigned long long)half;                        // PK: the upper half takes the next one
@@ -267,7 +275,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         // R33: this scenario's template variant -- its kernel records and estimate totals
         const uint32_t vidx = P.num_variants > 1 ? s % P.num_variants : 0u;
         const UrgKernRec *KR = P.kern + (size_t)vidx * P.nk_total + kbase;
-        const UrgVarRec *VR = P.var + (size_t)vidx * C + (valid_c ? c : 0u);
+        if (valid_c) myvar[lane] = P.var[(size_t)vidx * C + c];   // the variant's estimate totals, per lane
 
         // ---- A1: scenario init (R3, R15 STATIC) ----
         int64_t Pp = 0, Dp = 0;
@@ -372,7 +380,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         auto cls_key_a = [&]() -> int64_t {
             return KIND == K_EDF ? t_arr + Dp : KIND == K_HRRN ? t_arr : KIND == K_LCUF ? Pp : 0;
         };
-        auto cls_key_b = [&]() -> int64_t { return KIND == K_LCUF ? VR->gpu_est_chain : rem_g + rem_c; };
+        auto cls_key_b = [&]() -> int64_t { return KIND == K_LCUF ? myvar[lane].gpu_est_chain : rem_g + rem_c; };
         // "chain o ranks before chain s" (ties by smaller chain id; exact 128-bit ratios)
         auto cls_before = [&](int64_t oA, int64_t oB, int o, int64_t sA, int64_t sB, int sl, int64_t t) -> bool {
             if (KIND == K_EDF || KIND == K_SJF) {
@@ -492,7 +500,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     Fg = inst_factor(rng_word(P.seed, s, URG_TAG_INST, cid, inst, 0), CRF(gpu_sigma_ppm));
                     Fc = inst_factor(rng_word(P.seed, s, URG_TAG_INST, cid, inst, 1), CRF(cpu_sigma_ppm));
                     task = stage; launched = k_first; done = k_first; sync_ord = stage << 16;
-                    rem_g = VR->gpu_est_total; rem_c = CRF(cpu_est_total);
+                    rem_g = myvar[lane].gpu_est_total; rem_c = CRF(cpu_est_total);
                     if (ma) {   // R26: this instance's ~E^cpu_j, floor mean of the last min(W, h_j) measurements
                         rem_c = 0;
                         for (uint32_t j = 0; j < CRF(num_tasks); ++j) {

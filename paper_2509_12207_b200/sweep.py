@@ -152,9 +152,16 @@ def with_copies(w: Workload, h2d_ns: int = 300_000, d2h_ns: int = 100_000) -> Wo
     import copy
     from workloads.spec import Kernel
     w2 = copy.deepcopy(w)
+    h2d, d2h = Kernel(h2d_ns, h2d_ns, 200, 1), Kernel(d2h_ns, d2h_ns, 200, 1)
+    variants = [iter(v) for v in (w2.kernel_variants or [])]
+    new_variants = [[] for _ in variants]
     for ch in w2.chains:
         for t in ch.tasks:
-            t.kernels = [Kernel(h2d_ns, h2d_ns, 200, 1)] + t.kernels + [Kernel(d2h_ns, d2h_ns, 200, 1)]
+            for it, nv in zip(variants, new_variants):   # every template variant gets the same copies (R33)
+                nv += [copy.copy(h2d)] + [next(it) for _ in t.kernels] + [copy.copy(d2h)]
+            t.kernels = [copy.copy(h2d)] + t.kernels + [copy.copy(d2h)]
+    if variants:
+        w2.kernel_variants = new_variants
     return w2
 
 

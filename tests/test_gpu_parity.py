@@ -571,13 +571,9 @@ def test_largest_template_that_fits():
 
 
 def _with_copies(w, h2d_ns=300 * US, d2h_ns=100 * US):
-    """Every task starts with an H2D memcpy and ends with a D2H memcpy (R31)."""
-    import copy as _copy
-    w2 = _copy.deepcopy(w)
-    for ch in w2.chains:
-        for t in ch.tasks:
-            t.kernels = [Kernel(h2d_ns, h2d_ns, 200, 1)] + t.kernels + [Kernel(d2h_ns, d2h_ns, 200, 1)]
-    return w2
+    """Every task starts with an H2D memcpy and ends with a D2H memcpy (R31), in every template variant."""
+    from paper_2509_12207_b200.sweep import with_copies
+    return with_copies(w, h2d_ns, d2h_ns)
 
 
 def test_copy_engine():

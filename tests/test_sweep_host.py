@@ -58,3 +58,13 @@ def test_executors_study():
     pts = SW.executors(cfg.policies["urgengo"], cfg.batch)
     assert [p.executors for p in pts] == [EXEC_CHAIN] * 3 + [EXEC_TASK] * 3
     assert [p.policy.kind for p in pts[:3]] == [p.policy.kind for p in pts[3:]] == [2, 1, 0]
+
+
+def test_copies_keep_template_variants_aligned():
+    from paper_2509_12207_b200 import sweep as SW
+    from workloads import paper11_variants
+    w = SW.with_copies(paper11_variants(3))
+    n = w.total_kernels()
+    assert all(len(v) == n for v in w.kernel_variants)
+    flags0 = [k.flags for ch in w.chains for t in ch.tasks for k in t.kernels]
+    assert all([k.flags for k in v] == flags0 for v in w.kernel_variants)

@@ -15,7 +15,7 @@ from typing import Callable, Dict, List
 from .quantiles import pareto_table
 from .spec import (F_ALL, FIFO, MS, STATIC, SYNC_ASYNC, SYNC_OVERLAP, URGENGO, Batch, Policy,
                    Workload)
-from .templates import paper11, toy2
+from .templates import paper11_variants, toy2
 
 _CAL = os.path.join(os.path.dirname(__file__), "calibrated.json")
 
@@ -57,9 +57,15 @@ def _cfg1() -> Config:
                   "configs[0]: 2 chains, 3 tasks x 5 kernels, 2 streams, 1 s, 1 scenario")
 
 
+def paper11_64():
+    """The Table-2 workload with 64 template variants: scenario s uses template s mod 64
+    (SURVEY.md §8(d) cfg 2; R33).  Template 0 is paper11(0x5EED0002)."""
+    return paper11_variants(64)
+
+
 def _cfg2() -> Config:
     lth = calibrated_lth("paper11")
-    return Config("paper11", paper11, {"urgengo": urgengo(lth), "fifo": fifo(), "static": static()},
+    return Config("paper11", paper11_64, {"urgengo": urgengo(lth), "fifo": fifo(), "static": static()},
                   Batch(seed=0x5EED0002, scenario_count=1000, horizon_ns=10_000 * MS, ftight_permille=400),
                   "configs[1]: 11 chains (Table 2), 10 s horizon, 1k randomized scenarios")
 
@@ -69,12 +75,12 @@ def _cfg3() -> Config:
     # utilisation u = sum_c Egpu_c / P'_c is 1.2082 at f_a = 1 (Table 2); f_a = u / 1.2082 (rational)
     sweep = [Batch(seed=0x5EED0003, scenario_count=100_000, horizon_ns=10_000 * MS, ftight_permille=400,
                    fa_num=u10 * 1000, fa_den=12082) for u10 in range(5, 13)]
-    return Config("usweep", paper11, {"urgengo": urgengo(lth), "fifo": fifo(), "static": static()},
+    return Config("usweep", paper11_64, {"urgengo": urgengo(lth), "fifo": fifo(), "static": static()},
                   sweep[0], "configs[2]: utilisation sweep 0.5-1.2 x 100k scenarios", sweep)
 
 
 def _paper11_heavy() -> Workload:
-    w = paper11()
+    w = paper11_64()
     w.kern_quantiles_q16 = pareto_table()
     return w
 
@@ -88,7 +94,7 @@ def _cfg4() -> Config:
 
 def _cfg5() -> Config:
     lth = calibrated_lth("paper11")
-    return Config("scaleout", paper11, {"urgengo": urgengo(lth)},
+    return Config("scaleout", paper11_64, {"urgengo": urgengo(lth)},
                   Batch(seed=0x5EED0005, scenario_count=100_000_000, horizon_ns=1_000 * MS, ftight_permille=400),
                   "configs[4]: 100M scenarios, 1 s horizon, sharded over GPUs")
 
