@@ -189,6 +189,7 @@ def workload_batch(a):
 def config_json(cfg, w, b, a, n):
     return {"workload": f"{cfg.name} (BASELINE.json {cfg.note.split(':')[0]})", "policy": a.policy,
             "chains": w.num_chains, "kernels_per_template": w.total_kernels(),
+            "template_variants": w.num_variants,
             "scenarios_per_gpu": b.scenario_count, "scenarios_total": b.scenario_count * n,
             "horizon_s": b.horizon_ns / 1e9, "seed": hex(b.seed), "l2": "flushed (256 MiB write) between steps",
             "parallelism": f"scenario shards x{n}"}
