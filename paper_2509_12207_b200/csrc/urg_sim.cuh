@@ -345,6 +345,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         int64_t head_ready = 0;                // time the waiting head became head (R20 key)
         uint32_t head_util = 0;                // util of the running kernel
         uint32_t head_u = 0xFFFFu;             // util of the waiting head (valid while one waits)
+        uint32_t head_nom = 0;                 // its nominal duration (read with the record)
         bool head_copy = false;                // R31: the head is a memcpy (copy engine)
         uint32_t n_total = 0, n_miss = 0, n_early = 0, n_unfin = 0, n_launch = 0, hash = 2166136261u;
         uint64_t sum_rt = 0;
@@ -431,7 +432,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             if (launched > done) {
                 head_ready = t;
                 const UrgKernRec kr = kern_rec(KR + done);
-                head_u = kr.util_permille;
+                head_u = kr.util_permille; head_nom = kr.nominal_ns;
                 if (has_copy) head_copy = kr.flags & 1u;
             }
             if (pc == PC_SYNC_WAIT && done >= sync_target) { pc = PC_SYNC_RET; cpu_busy(t, sync_cost); }
@@ -440,7 +441,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         auto start_head = [&](int64_t t, uint32_t u_run) {
             uint64_t G = 65536u;
             if (KQ) G = T.kern_q[rng_word(P.seed, s, URG_TAG_KERN, cid, inst, done) >> 20];
-            uint64_t d = ((((uint64_t)kern_rec(KR + done).nominal_ns * Fg) >> 16) * G) >> 16;
+            uint64_t d = ((((uint64_t)head_nom * Fg) >> 16) * G) >> 16;
             d = d < 1 ? 1 : (d > 0xFFFFFFFFull ? 0xFFFFFFFFull : d);
             if (contend && !head_copy) d += d * (uint64_t)P.alpha_pm * u_run / 1000000ull;   // R30
             head_util = head_copy ? 0u : head_u;   // a memcpy uses the copy engine, not the SMs (R31)
@@ -570,7 +571,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     const UrgKernRec kr = kern_rec(KR + n);
                     const int64_t est = kr.estimate_ns;
                     if (launched == done) {   // stream was empty: head now
-                        head_ready = t; head_u = kr.util_permille; newhead = true;
+                        head_ready = t; head_u = kr.util_permille; head_nom = kr.nominal_ns; newhead = true;
                         if (has_copy) head_copy = kr.flags & 1u;
                     }
                     ++launched; ++n_launch;
