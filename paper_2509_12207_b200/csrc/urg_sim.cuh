@@ -346,6 +346,9 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         uint32_t head_util = 0;                // util of the running kernel
         uint32_t head_u = 0xFFFFu;             // util of the waiting head (valid while one waits)
         uint32_t head_nom = 0;                 // its nominal duration (read with the record)
+        UrgKernRec nxt = {};                   // latency build: record of the next kernel to launch (kernel
+                                               // `launched`), loaded one launch ahead (off the critical path;
+                                               // the throughput builds reload it: registers)
         bool head_copy = false;                // R31: the head is a memcpy (copy engine)
         uint32_t n_total = 0, n_miss = 0, n_early = 0, n_unfin = 0, n_launch = 0, hash = 2166136261u;
         uint64_t sum_rt = 0;
@@ -501,6 +504,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     Fg = inst_factor(rng_word(P.seed, s, URG_TAG_INST, cid, inst, 0), CRF(gpu_sigma_ppm));
                     Fc = inst_factor(rng_word(P.seed, s, URG_TAG_INST, cid, inst, 1), CRF(cpu_sigma_ppm));
                     task = stage; launched = k_first; done = k_first; sync_ord = stage << 16;
+                    if (!WIDE) nxt = kern_rec(KR + k_first);
                     rem_g = myvar[lane].gpu_est_total; rem_c = CRF(cpu_est_total);
                     if (ma) {   // R26: this instance's ~E^cpu_j, floor mean of the last min(W, h_j) measurements
                         rem_c = 0;
@@ -568,13 +572,14 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                 }
                 if (pc == PC_ENQUEUE) {   // the kernel reaches its stream (R16) + sync decision (R17)
                     const uint32_t n = launched;
-                    const UrgKernRec kr = kern_rec(KR + n);
+                    const UrgKernRec kr = WIDE ? kern_rec(KR + n) : nxt;
                     const int64_t est = kr.estimate_ns;
                     if (launched == done) {   // stream was empty: head now
                         head_ready = t; head_u = kr.util_permille; head_nom = kr.nominal_ns; newhead = true;
                         if (has_copy) head_copy = kr.flags & 1u;
                     }
                     ++launched; ++n_launch;
+                    if (!WIDE && launched < CRF(num_kernels)) nxt = kern_rec(KR + launched);
                     rem_g -= est;
                     if (akb_on) ++akb;
                     if (coll && L_last >= 0 && L_last <= P.lax_threshold_ns) {
@@ -634,7 +639,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     if (urg) { lax = laxity(t); L_last = lax; }
                     const bool own_urgent = lax >= 0 && lax <= P.lax_threshold_ns;
                     if (f_delay && !own_urgent && (urgent_m & ~(1u << lane)) &&
-                        kern_rec(KR + launched).util_permille >= P.util_exempt) {
+                        (WIDE ? kern_rec(KR + launched) : nxt).util_permille >= P.util_exempt) {
                         pc = PC_ATTEMPT;
                         cpu_next = t + P.sleep_ns;
                         break;
