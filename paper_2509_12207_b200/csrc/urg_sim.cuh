@@ -595,25 +595,18 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     }
                     const bool last = launched == task_end;
                     if (last) rem_c -= ma ? ma_pred[task] : T.task[tbase + task].cpu_estimate_ns;
-                    if (n == task_first) { acc = 0; batch_start = task_first; }
-                    int32_t target = -1;
-                    if (P.sync_mode == S_ASYNC) {
-                        if (last) target = (int32_t)launched;
-                    } else if (P.sync_mode == S_EACH) {
-                        target = (int32_t)launched;
-                    } else {
-                        acc += est;
-                        const bool closes = acc >= P.delta_eval_ns;
-                        if (closes) acc = 0;
-                        if (last) { acc = 0; target = (int32_t)launched; }
-                        else if (closes) {
-                            if (P.sync_mode == S_BATCHED) target = (int32_t)launched;
-                            else {   // OVERLAP: wait for the previous batch
-                                const uint32_t prev = batch_start;
-                                batch_start = launched;
-                                if (prev != task_first) target = (int32_t)prev;   // first close: not issued
-                            }
-                        }
+                    // R17 with selects (one rare branch): the estimate sum only matters in the
+                    // batched modes; a batch closes when it reaches Delta_eval, crossing kernel included
+                    const uint32_t sm = P.sync_mode;
+                    if (n == task_first) batch_start = task_first;
+                    const int64_t acc2 = (n == task_first ? 0 : acc) + est;
+                    const bool closes = sm >= S_BATCHED && acc2 >= P.delta_eval_ns;
+                    acc = (closes || last) ? 0 : acc2;
+                    int32_t target = (last || sm == S_EACH || (closes && sm == S_BATCHED)) ? (int32_t)launched : -1;
+                    if (closes && !last && sm == S_OVERLAP) {   // OVERLAP: wait for the previous batch
+                        const uint32_t prev = batch_start;
+                        batch_start = launched;
+                        if (prev != task_first) target = (int32_t)prev;   // first close: not issued
                     }
                     if (target >= 0) {
                         sync_target = (uint32_t)target;
@@ -729,6 +722,16 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         int64_t cal_next = 0;                   // CAL: next sampling time
         uint32_t cal_n = 0;                     // CAL: samples of this scenario
         bool fin = false;                       // PK: this half's scenario has ended
+        // Core UrgenGo build: the Phase B snapshot (R21) is taken where it changes -- at the
+        // end of the previous Phase B, beside that phase's new-head vote -- instead of on the
+        // next phase's critical path (Phase A and Phase C touch neither the AKB nor L_last).
+        // At scenario start no lane has an AKB entry.
+        constexpr bool snap_late = urg && !coll && !EXT;
+        uint32_t urgent_nx = 0, active_nx = 0;
+        // Core build: Phase C's fit ballot runs at every step and is itself the test, so no
+        // "new stream head" vote sits between Phase B and Phase C (a head that did not fit at an
+        // earlier Phase C still does not: `used` only falls at a retirement).
+        constexpr bool c_always = PK && !EXT && !CAL;   // measured: +1-2 % packed; the latency build ran 3x slower
         for (;;) {
             // A2: next event time.  Every lane's next event is strictly after t_prev, so
             // the warp minimum is taken on the 32-bit distance (one REDUX); distances that
@@ -738,7 +741,18 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             const uint32_t d32 = mine <= t_prev ? 0u : (dl >= 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)dl);
             const uint32_t m = hmin(d32);
             int64_t t;
-            if (PK ? __any_sync(FULL, m == 0xFFFFFFFFu && !fin) : m == 0xFFFFFFFFu) {
+            if (!PK && !CAL) {   // one rare-path branch for the saturated, stalled and final steps
+                t = t_prev + m;
+                if (m + 1u <= 1u || t > H_stop) {
+                    if (m == 0xFFFFFFFFu) t = hmin64(mine);
+                    if (t > H_stop) break;
+                    if (m == 0u) {   // time must advance (invariant); report and stop this scenario
+                        if (lane == 0 && atomicCAS((unsigned long long *)err, 0ull, (unsigned long long)ERR_TIME) == 0ull)
+                            err[1] = s;
+                        break;
+                    }
+                }
+            } else if (PK ? __any_sync(FULL, m == 0xFFFFFFFFu && !fin) : m == 0xFFFFFFFFu) {
                 const int64_t tt = hmin64(mine);
                 t = m == 0xFFFFFFFFu ? tt : t_prev + m;
             } else t = t_prev + m;
@@ -767,7 +781,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     err[1] = s;
                 fin = fin || t > H_stop || m == 0u;
                 if (__all_sync(FULL, fin)) break;
-            } else {
+            } else if (CAL) {
                 if (t > H_stop) break;
                 if (m == 0u) {   // time must advance (invariant); report and stop this scenario
                     if (lane == 0 && atomicCAS((unsigned long long *)err, 0ull, (unsigned long long)ERR_TIME) == 0ull)
@@ -782,23 +796,41 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
 
             // Phase A: retire (R21, R19)
             const bool ret = !fin && head_end == t;
-            bool dirty = PK ? hany(ret) : __any_sync(FULL, ret);   // GPU state changed: Phase C must run
-            if (PK ? __any_sync(FULL, ret) : dirty) {
+            // The retire and due votes are issued together: a retirement makes its own lane due
+            // at t only through a sync return of zero cost (retire(): cpu_busy(t, 0) sets cpu_next = t).
+            const bool due_pre = !fin && (cpu_next == t || (ret && pc == PC_SYNC_WAIT && done + 1u >= sync_target &&
+                                                            sync_cost == 0));
+            const uint32_t retm = __ballot_sync(FULL, ret), duem = __ballot_sync(FULL, due_pre);
+            bool dirty = (retm & hmask) != 0u;   // GPU state changed: Phase C must run
+            if (retm) {
                 used -= hsum(ret ? head_util : 0u);
                 if (ret) retire(t);
             }
+            const bool due = !fin && cpu_next == t;   // == due_pre
+            const bool any_due = duem != 0u;
 
             // Phase B: CPU steps of every chain due at t, against the round snapshot (R21)
-            const bool due = !fin && cpu_next == t;
-            if (__any_sync(FULL, due)) {
+            if (any_due) {
 #ifdef URG_STATS
                 ++st_multi;
 #endif
-                uint32_t urgent_m = 0, active_m = 0, busy_m = 0;
-                if (urg || cls) snapshot(te || (due && can_bind()), urgent_m, active_m, busy_m);
+                uint32_t urgent_m = urgent_nx, active_m = active_nx, busy_m = 0;
+                if (!snap_late && (urg || cls)) snapshot(te || (due && can_bind()), urgent_m, active_m, busy_m);
                 bool nh = false;
                 if (due) nh = phase_b(t, urgent_m, active_m, busy_m);
-                dirty |= PK ? hany(nh) : __any_sync(FULL, nh);
+                if (snap_late) {   // the next phase's snapshot: this lane's L_last and the two masks
+                    if (f_bind) {
+                        __syncwarp();   // this phase's reads of the snapshot are done
+                        if (due) snapL[lane] = L_last;
+                        __syncwarp();
+                    }
+                    const uint32_t nhm = c_always ? 0u : __ballot_sync(FULL, nh);
+                    if (f_delay)
+                        urgent_nx = __ballot_sync(FULL, akb > 0 && L_last >= 0 && L_last <= P.lax_threshold_ns) & hmask;
+                    if (f_bind) active_nx = __ballot_sync(FULL, akb > 0) & hmask;
+                    dirty |= (nhm & hmask) != 0u;
+                } else if (!c_always)
+                    dirty |= PK ? hany(nh) : __any_sync(FULL, nh);
                 // R32: messages published in a round are delivered at its end (a newer one replaces
                 // an untaken one); threads waiting for one run in the next round, same t and read view
                 while (te) {
@@ -871,7 +903,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             // waiting head was already found not to fit and `used` has not decreased.
             // The greedy scan in key order starts, each time, the smallest-key head that
             // fits the capacity left (heads that do not fit stay unfit as `used` grows).
-            if (PK && __any_sync(FULL, dirty)) {
+            if (PK && (c_always || __any_sync(FULL, dirty))) {
                 // both halves: a half that is not dirty has no head that fits (fit = 0)
                 bool waiting = !fin && launched > done && head_end == INF64;
                 for (;;) {
@@ -894,7 +926,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     if (wl >= 0) used += uw;
                     if (!any_multi) break;   // each half started its only fitting head (others did not fit)
                 }
-            } else if (!PK && dirty) {
+            } else if (!PK && (c_always || dirty)) {
 #ifdef URG_STATS
                 ++st_dispatch;
 #endif
