@@ -92,9 +92,9 @@ def _cpu_model():
     return "unknown"
 
 
-def oracle_pool(cfg_name, pol_name, cores):
+def oracle_pool(cfg_name, pol_name, cores, method="fork"):
     import multiprocessing as mp
-    ctx = mp.get_context("fork")
+    ctx = mp.get_context(method)
     return ctx.Pool(cores, initializer=_oracle_init, initargs=(cfg_name, pol_name))
 
 
@@ -248,7 +248,8 @@ def main():
     rank = _env_int("RANK", 0)
     local = _env_int("LOCAL_RANK", 0)
     want_cpu = rank == 0 and world == 1 and not a.no_cpu_baseline
-    pool = oracle_pool(a.config, a.policy, _cores()) if want_cpu else None   # fork before CUDA init
+    # the oracle pool is started only after the GPU legs (an idle pool forked at start-up was
+    # measured to slow the e2e leg 2-3x on some hosts), spawned so no child inherits CUDA state
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device (the product path has no CPU fallback)")
     # one process per GPU; URG_BENCH_BACKEND=gloo (test only) lets several ranks share one
@@ -338,8 +339,10 @@ def main():
         hw = ct.c_void_p()
         assert L.urg_create_workload(ct.byref(dw.desc), ct.byref(hw)) == 0, L.urg_last_error()
         host_agg[:] = 0
+        t1 = time.perf_counter()
         st = L.urg_simulate_batch_host(hw, ct.byref(ps), ct.byref(bs), ct.byref(o), ct.c_void_p(stream.cuda_stream))
         assert st == 0, L.urg_last_error()
+        t2 = time.perf_counter()
         ht = torch.from_numpy(host_agg.copy())
         if world > 1:     # the same single collective, on host-returned results
             ht = ht.cuda()
@@ -347,6 +350,9 @@ def main():
             ht = ht.cpu()
         L.urg_destroy_workload(hw)
         dt = time.perf_counter() - t0
+        if os.environ.get("URG_BENCH_DEBUG"):
+            print(f"e2e step {i}: {dt * 1e3:.1f} ms (create {1e3 * (t1 - t0):.1f}, simulate {1e3 * (t2 - t1):.1f})",
+                  file=sys.stderr, flush=True)
         if i > 0:
             e2e_t.append(dt)
     tt = torch.tensor([sum(e2e_t) / len(e2e_t)], dtype=torch.float64, device="cuda")
@@ -421,9 +427,11 @@ def main():
             "launch_events_per_gpu": tl}
 
     # ---- cpu_baseline: the oracle, unchanged, on a bounded sample (rank 0, N = 1 only) ----
-    if pool is not None:
+    if want_cpu:
         cores = _cores()
-        one, dt1 = oracle_sample(pool, [b.scenario_begin], b.horizon_ns)       # size the sample
+        pool = oracle_pool(a.config, a.policy, cores, "spawn")
+        one, _ = oracle_sample(pool, [b.scenario_begin] * cores, b.horizon_ns)  # warm every worker
+        dt1 = max(r[3] for r in one)                                            # size the sample
         per_core = max(1, int(a.cpu_seconds / max(dt1, 1e-3)))
         m = min(S, cores * per_core)
         begins = [b.scenario_begin + i for i in range(m)]
