@@ -165,7 +165,10 @@ template <int KIND, int FLAGS, bool KQ, bool WIDE, bool CAL = false, bool EXT = 
 #ifndef URG_PK_THREADS
 #define URG_PK_THREADS 768   // measured: 80 registers beat 64 with spills (configs[2]/[4] +3-4 %)
 #endif
-__global__ void __launch_bounds__(WIDE ? (PK ? URG_PK_THREADS : 1024) : 512, 1)
+#ifndef URG_LAT_THREADS
+#define URG_LAT_THREADS 512
+#endif
+__global__ void __launch_bounds__(WIDE ? (PK ? URG_PK_THREADS : 1024) : URG_LAT_THREADS, 1)
 urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t *__restrict__ records,
                unsigned long long *__restrict__ agg, unsigned long long *__restrict__ work,
                long long *__restrict__ err)
