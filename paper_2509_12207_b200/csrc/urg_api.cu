@@ -20,7 +20,7 @@
 typedef void (*urg_sim_fn)(const uint8_t *blob, const UrgSimParams P, uint32_t *records, unsigned long long *agg,
                            unsigned long long *work, long long *err);
 const void *urg_sim_kernel_for(uint32_t kind, uint32_t flags, bool kern_q, bool wide, bool cal, bool ext,
-                               bool pk);   // urg_sim.cu
+                               bool pk, bool small);   // urg_sim.cu
 extern "C" __global__ void urg_cal_hist_kernel(const int64_t *buf, uint64_t count, uint64_t cap, long long *ws,
                                                int pass);
 extern "C" __global__ void urg_cal_pick_kernel(long long *ws, int pass, int pct, long long *result);
@@ -392,8 +392,11 @@ static urg_status prepare_launch(const urg_workload *w, const urg_policy *p, con
     // two scenarios per warp in the throughput core build when the chains fit a half warp
     bool pk = wide && !cal && !ext && w->num_chains <= 16;
     if (const char *ep = getenv("URG_PACK")) pk = pk && atoi(ep) != 0;          // test hook: disable packing
+    // the small latency core build (255-register cap) when the batch needs at most 8 warps per SM
+    bool small = !wide && !cal && !ext && b->scenario_count <= (uint64_t)w->num_sms * 8u;
+    if (const char *es = getenv("URG_SMALL")) small = small && atoi(es) != 0;    // test hook: disable it
     fn = (urg_sim_fn)urg_sim_kernel_for(p->kind, p->kind == URG_URGENGO ? p->flags : 0, w->has_kern_q, wide && !cal,
-                                        cal, ext, pk);
+                                        cal, ext, pk, small);
     if (!fn) return fail(URG_EINTERNAL, "no kernel instantiation for kind %u flags %u", p->kind, p->flags);
     P.blob_bytes = (uint32_t)w->blob.size();
     P.mbar_offset = align16(P.blob_bytes);

@@ -16,14 +16,15 @@ URG_DECL(0) URG_DECL(1) URG_DECL(2) URG_DECL(3) URG_DECL(4) URG_DECL(5) URG_DECL
 URG_DECL(9) URG_DECL(10) URG_DECL(11) URG_DECL(12)
 #undef URG_DECL
 
-const void *urg_sim_kernel_for(uint32_t kind, uint32_t flags, bool kern_q, bool wide, bool cal, bool ext, bool pk)
+const void *urg_sim_kernel_for(uint32_t kind, uint32_t flags, bool kern_q, bool wide, bool cal, bool ext, bool pk,
+                               bool small)
 {
     const uint32_t row = cal                ? 18 + (flags & 15u)
                          : kind == K_FIFO    ? 0
                          : kind == K_STATIC  ? 1
                          : kind == K_URGENGO ? 2 + (flags & 15u)
                                              : 34 + (kind - K_EDF);
-    const uint32_t col = (kern_q ? 1u : 0u) + (wide ? 2u : 0u) + (ext ? 4u : 0u) + (pk ? 8u : 0u);
+    const uint32_t col = (kern_q ? 1u : 0u) + (wide ? 2u : 0u) + (ext ? 4u : 0u) + (pk ? 8u : 0u) + (small ? 16u : 0u);
     const void *(*parts[URG_PARTS])(uint32_t, uint32_t) = {urg_sim_part0, urg_sim_part1, urg_sim_part2,
                                                           urg_sim_part3, urg_sim_part4, urg_sim_part5,
                                                           urg_sim_part6, urg_sim_part7, urg_sim_part8,

@@ -161,14 +161,19 @@ __device__ __forceinline__ uint64_t work_offset(uint64_t j, uint64_t S, uint32_t
 // PK: two scenarios per warp (lanes 0-15 and 16-31, at most 16 chains), throughput core
 // build only: the halves step in lockstep, every warp collective is segmented per half,
 // so the step's overhead is shared by two scenarios.
-template <int KIND, int FLAGS, bool KQ, bool WIDE, bool CAL = false, bool EXT = true, bool PK = false>
+//
+// SMALL: the latency core build for batches of at most 8 warps per SM: 256-thread CTAs, so
+// ptxas may use up to 255 registers (it takes ~134; measured 2.3 % faster on configs[1]
+// than the 128-register cap of the 512-thread build).
+template <int KIND, int FLAGS, bool KQ, bool WIDE, bool CAL = false, bool EXT = true, bool PK = false,
+          bool SMALL = false>
 #ifndef URG_PK_THREADS
 #define URG_PK_THREADS 768   // measured: 80 registers beat 64 with spills (configs[2]/[4] +3-4 %)
 #endif
 #ifndef URG_LAT_THREADS
 #define URG_LAT_THREADS 512
 #endif
-__global__ void __launch_bounds__(WIDE ? (PK ? URG_PK_THREADS : 1024) : URG_LAT_THREADS, 1)
+__global__ void __launch_bounds__(WIDE ? (PK ? URG_PK_THREADS : 1024) : (SMALL ? 256 : URG_LAT_THREADS), 1)
 urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t *__restrict__ records,
                unsigned long long *__restrict__ agg, unsigned long long *__restrict__ work,
                long long *__restrict__ err)
@@ -1032,10 +1037,13 @@ struct UrgRow {
     static constexpr int F = ROW < 2 || ROW >= 34 ? 0 : ROW < 18 ? ROW - 2 : ROW - 18;
     static constexpr bool C = ROW >= 18 && ROW < 34;
     // col: bit 0 per-kernel factor table, bit 1 throughput build, bit 2 extended model,
-    // bit 3 two scenarios per warp (throughput core build only)
+    // bit 3 two scenarios per warp (throughput core build only), bit 4 small latency core build
     static const void *get(uint32_t col)
     {
         if constexpr (!C) {
+            if ((col & 30u) == 16u)   // bit 4: the small latency core build
+                return (col & 1u) ? (const void *)urg_sim_kernel<K, F, true, false, false, false, false, true>
+                                  : (const void *)urg_sim_kernel<K, F, false, false, false, false, false, true>;
             if ((col & 14u) == 10u)
                 return (col & 1u) ? (const void *)urg_sim_kernel<K, F, true, true, false, false, true>
                                   : (const void *)urg_sim_kernel<K, F, false, true, false, false, true>;

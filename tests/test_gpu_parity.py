@@ -100,6 +100,28 @@ def test_random_small_workloads(seed):
     both(w, p, b, f"seed {seed}")
 
 
+@pytest.mark.parametrize("seed", range(8))
+def test_random_small_workloads_512_thread_build(seed, monkeypatch):
+    """URG_SMALL=0: batches of at most 8 warps per SM on the 512-thread latency build (the one
+    bigger batches up to 16 warps per SM use) -- equal to the oracle like the default small build."""
+    monkeypatch.setenv("URG_SMALL", "0")
+    test_random_small_workloads(seed + 100)
+
+
+def test_small_build_equals_512_thread_build(monkeypatch):
+    """The 256-thread latency build (255-register cap) and the 512-thread one give identical
+    records and aggregates on configs[1]'s workload, for every policy of the config."""
+    cfg = get_config("paper11")
+    w = cfg.workload()
+    b = Batch(seed=cfg.batch.seed, scenario_count=300, horizon_ns=2_000 * MS, ftight_permille=400)
+    for name, p in cfg.policies.items():
+        r1, a1 = gpu_run(w, p, b)
+        monkeypatch.setenv("URG_SMALL", "0")
+        r2, a2 = gpu_run(w, p, b)
+        monkeypatch.delenv("URG_SMALL")
+        assert np.array_equal(r1, r2) and np.array_equal(a1, a2), name
+
+
 @pytest.mark.parametrize("name", ["urgengo", "fifo", "static"])
 def test_paper11_small(name):
     """configs[1] workload at a size the oracle finishes in seconds: 48 scenarios x 2 s, spanning many CTAs."""
