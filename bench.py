@@ -37,11 +37,18 @@ METRIC = "simulated launch events/s"
 UNIT = "launch events/s"
 
 # Algorithmic warp-instructions of the event loop: per loop step
-# (one distinct event time of one scenario) and per launch event.  Peak issue rate
-# = 148 SMs x 4 schedulers x 1 warp-instruction/clk x sm_max_mhz.
+# (one distinct event time of one scenario) and per launch event, all of them and the
+# ALU-pipe ones (integer compare/add/select/shift/logic; the rest are warp collectives,
+# loads, branches and the two IMAD.WIDE of the duration).  The bound is the ALU pipe:
+# one warp-instruction per 2 cycles per scheduler (B300_MICROARCH.md "alu-pipe rt_SMSP=2";
+# ncu: 84 % busy in the throughput build), so peak = SMs x 4 x 0.5 x sm_max_mhz; the
+# issue peak (1 warp-instruction/clk/scheduler) is reported beside it.
 ALG_INST_PER_STEP = 24
 ALG_INST_PER_LAUNCH = 40
+ALG_ALU_PER_STEP = 18
+ALG_ALU_PER_LAUNCH = 34
 SMSP_PER_SM = 4
+ALU_RT_CYCLES = 2
 
 
 def _env_int(k, d):
@@ -361,15 +368,18 @@ def main():
     e2e_step = tt.item()
     assert np.array_equal(host_rec, rec.cpu().numpy().view(np.uint32)), "host-buffer path differs from device path"
 
-    # ---- roofline: issue-bound event loop ----
+    # ---- roofline: ALU-pipe-bound event loop ----
     props = torch.cuda.get_device_properties(dev)
     sms = props.multi_processor_count
     peak_mhz = clocks["sm_max_mhz"] or 1965.0
     # per-rank algorithmic instruction count of one launch of urg_sim_kernel
     launches_rank, steps_rank = launches_all / n, steps_all / n
     alg_inst = steps_rank * ALG_INST_PER_STEP + launches_rank * ALG_INST_PER_LAUNCH
-    achieved = alg_inst / k_max / 1e9            # G warp-inst/s
-    peak = sms * SMSP_PER_SM * peak_mhz * 1e6 / 1e9
+    alg_alu = steps_rank * ALG_ALU_PER_STEP + launches_rank * ALG_ALU_PER_LAUNCH
+    achieved = alg_alu / k_max / 1e9              # G ALU-pipe warp-inst/s
+    peak = sms * SMSP_PER_SM * peak_mhz * 1e6 / ALU_RT_CYCLES / 1e9
+    issue_achieved = alg_inst / k_max / 1e9
+    issue_peak = sms * SMSP_PER_SM * peak_mhz * 1e6 / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
@@ -388,8 +398,11 @@ def main():
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gwarp-inst/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "urg_sim_kernel",
-                         "note": f"algorithmic = {ALG_INST_PER_STEP} warp-inst/loop step + {ALG_INST_PER_LAUNCH}"
-                                 f"/launch event (DESIGN.md §7); peak = {sms} SMs x 4 issue/clk x {peak_mhz:.0f} MHz"},
+                         "issue": {"achieved": issue_achieved, "peak": issue_peak, "frac": issue_achieved / issue_peak},
+                         "note": f"algorithmic ALU-pipe warp-inst = {ALG_ALU_PER_STEP}/loop step + "
+                                 f"{ALG_ALU_PER_LAUNCH}/launch event (DESIGN.md §7); peak = ALU pipe, {sms} SMs x 4 "
+                                 f"schedulers x 1/{ALU_RT_CYCLES} warp-inst/clk x {peak_mhz:.0f} MHz; 'issue' = all "
+                                 f"{ALG_INST_PER_STEP}/{ALG_INST_PER_LAUNCH} algorithmic warp-inst against the issue peak"},
             "e2e": {"value": launches_all / e2e_step, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": a.steps,
