@@ -14,6 +14,8 @@ KEYS = ["Kernel Name", "dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__ti
         "launch__registers_per_thread", "sass__inst_executed_local_loads", "sass__inst_executed_local_stores",
         "sm__inst_executed.avg.per_cycle_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
         "smsp__inst_executed.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
         "smsp__thread_inst_executed_per_inst_executed.ratio", "lts__t_sector_hit_rate.pct",
         "l1tex__t_sector_hit_rate.pct", "launch__shared_mem_per_block_dynamic"]
 STALLS = "smsp__average_warps_issue_stalled_"
