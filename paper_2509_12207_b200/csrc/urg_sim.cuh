@@ -17,6 +17,12 @@
 
 #define FULL 0xFFFFFFFFu
 #define INF64 0x7FFFFFFFFFFFFFFFLL
+// 32-bit distances of a lane's next CPU event and kernel end from the last step time (see
+// the event loop): D_INF = none, D_FAR = at least 2^31 ns away (a lower bound), and every
+// value drifts down by less than D_SLOW between two exact refreshes
+#define D_INF 0xFFFFFFFFu
+#define D_FAR 0x80000000u
+#define D_SLOW 0x40000000u
 
 enum { K_FIFO = 0, K_STATIC = 1, K_URGENGO = 2, K_EDF = 3, K_SJF = 4, K_HRRN = 5, K_LCUF = 6 };
 enum { F_BIND = 1, F_DELAY = 2, F_EARLY = 4, F_COLL = 8 };
@@ -333,6 +339,8 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             for (uint32_t j = 0; j < P.ma_max_tasks; ++j) ma_cnt[j] = 0;
         int pc = PC_DONE;
         int64_t cpu_next = INF64;
+        uint32_t dc = D_INF, dh = D_INF;       // distances of cpu_next and head_end from the last step time
+        auto dsat = [](int64_t d) -> uint32_t { return d >= (int64_t)D_FAR ? D_FAR : (uint32_t)d; };
         uint32_t inst = 0;
         int64_t t_arr = 0;
         uint32_t Fg = 65536u, Fc = 65536u;
@@ -384,8 +392,8 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         };
         // R29: the thread is busy for d ns from t; with shared cores that is a CPU job
         auto cpu_busy = [&](int64_t t, int64_t d) {
-            if (!cores_on || d == 0) { cpu_next = t + d; return; }
-            job = true; job_run = false; job_rem = d; job_ready = t; cpu_next = INF64; cpu_chg = true;
+            if (!cores_on || d == 0) { cpu_next = t + d; dc = dsat(d); return; }
+            job = true; job_run = false; job_rem = d; job_ready = t; cpu_next = INF64; dc = D_INF; cpu_chg = true;
         };
         // R27 policy keys of this chain: EDF (t_arr + D', -), SJF (-, R), HRRN (t_arr, R),
         // LCUF (P', sum of kernel estimates); R = the remaining estimated work of Eq. 2
@@ -416,7 +424,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         if (valid) {
             t_arr = arrival(0);
             if (te && stage > 0) pc = PC_WAIT_MSG;   // R32: waits for the previous task's message
-            else if (t_arr < H) { pc = PC_ARRIVE; cpu_next = t_arr; }
+            else if (t_arr < H) { pc = PC_ARRIVE; cpu_next = t_arr; dc = dsat(t_arr + 1); }   // t_prev = -1
         }
         // R32: take the delivered message (instance msg - 1); on the chain's last stage, record
         // the instances the message sequence skipped as misses, in order
@@ -440,6 +448,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         auto retire = [&](int64_t t) {
             ++done;
             head_end = INF64;
+            dh = D_INF;
             if (launched > done) {
                 head_ready = t;
                 const UrgKernRec kr = kern_rec(KR + done);
@@ -457,6 +466,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             if (contend && !head_copy) d += d * (uint64_t)P.alpha_pm * u_run / 1000000ull;   // R30
             head_util = head_copy ? 0u : head_u;   // a memcpy uses the copy engine, not the SMs (R31)
             head_end = t + (int64_t)d;
+            dh = dsat((int64_t)d);
         };
         // Phase B: this lane's CPU program at t, until it has to wait for time to pass.
         // urgent_m / active_m / snapL are the round snapshot of the other chains (R14, R15).
@@ -468,7 +478,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             for (uint32_t guard = 0;; ++guard) {
                 if (guard > (1u << 24)) {
                     if (atomicCAS((unsigned long long *)err, 0ull, (unsigned long long)ERR_GUARD) == 0ull) err[1] = s;
-                    cpu_next = INF64;
+                    cpu_next = INF64; dc = D_INF;
                     break;
                 }
                 if ((uint32_t)(pc - PC_SYNC_RET) <= (uint32_t)(PC_TASK_START - PC_SYNC_RET)) {
@@ -481,7 +491,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                         // R28: the task ends with cudaFree -- request the device barrier and block
                         pc = PC_FREE_WAIT;
                         free_req = t;
-                        cpu_next = INF64;
+                        cpu_next = INF64; dc = D_INF;
                         break;
                     } else task_done = true;
                 }
@@ -566,15 +576,15 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     if (te && stage > 0) {   // R32: the next message, or wait for one
                         if (msg) { take_msg(); continue; }
                         pc = PC_WAIT_MSG;
-                        cpu_next = INF64;
+                        cpu_next = INF64; dc = D_INF;
                         break;
                     }
                     ++inst;
                     t_arr = arrival(inst);
-                    if (t_arr >= H) { pc = PC_DONE; cpu_next = INF64; break; }   // not admitted
+                    if (t_arr >= H) { pc = PC_DONE; cpu_next = INF64; dc = D_INF; break; }   // not admitted
                     pc = PC_ARRIVE;
                     cpu_next = t_arr;
-                    if (t_arr > t) break;
+                    if (t_arr > t) { dc = dsat(t_arr - t); break; }
                     continue;
                 }
                 }
@@ -630,7 +640,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                             continue;
                         }
                         pc = PC_SYNC_WAIT;
-                        cpu_next = INF64;
+                        cpu_next = INF64; dc = D_INF;
                         break;
                     }
                     pc = PC_ATTEMPT;
@@ -643,6 +653,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                         (WIDE ? kern_rec(KR + launched) : nxt).util_permille >= P.util_exempt) {
                         pc = PC_ATTEMPT;
                         cpu_next = t + P.sleep_ns;
+                        dc = dsat(P.sleep_ns);
                         break;
                     }
                     if (launched == task_first) {   // task-level stream binding
@@ -725,6 +736,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         // Warp-uniform: t_prev (time of the previous loop step) and `used`, the util
         // per-mille of the running kernels (kept incrementally).
         int64_t t_prev = -1;
+        uint32_t adv = 0;                       // sum of fast-path advances since the last exact refresh
         uint32_t used = 0;
         bool bar_prev = false;                  // R28: a barrier was pending at the previous step
         int64_t cal_next = 0;                   // CAL: next sampling time
@@ -741,29 +753,51 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         // earlier Phase C still does not: `used` only falls at a retirement).
         constexpr bool c_always = PK && !EXT && !CAL;   // measured: +1-2 % packed; the latency build ran 3x slower
         for (;;) {
-            // A2: next event time.  Every lane's next event is strictly after t_prev, so
-            // the warp minimum is taken on the 32-bit distance (one REDUX); distances that
-            // do not fit 32 bits saturate and fall back to the exact 64-bit minimum.
-            const int64_t mine = fin ? INF64 : (head_end < cpu_next ? head_end : cpu_next);
-            const uint64_t dl = (uint64_t)mine - (uint64_t)t_prev;   // exact when mine > t_prev
-            const uint32_t d32 = mine <= t_prev ? 0u : (dl >= 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)dl);
-            const uint32_t m = hmin(d32);
+            // A2: next event time.  Each lane keeps 32-bit distances dc / dh of its next CPU event
+            // and kernel end from t_prev (exact below 2^31, lower bounds above), so the step is one
+            // REDUX of min(dc, dh) and a subtraction.  A distance of 0 (time did not advance), one
+            // of 2^30 or more (a far lane may be nearer than it says), a drift of 2^30 since the
+            // last refresh, or the end of the horizon take the rare path: the exact 64-bit
+            // minimum, with every distance recomputed from it.
+            // (the packed build keeps 64-bit times at the head: the distances cost it registers,
+            // measured 3 % slower)
             int64_t t;
-            if (!PK && !CAL) {   // one rare-path branch for the saturated, stalled and final steps
-                t = t_prev + m;
-                if (m + 1u <= 1u || t > H_stop) {
-                    if (m == 0xFFFFFFFFu) t = hmin64(mine);
-                    if (t > H_stop) break;
-                    if (m == 0u) {   // time must advance (invariant); report and stop this scenario
-                        if (lane == 0 && atomicCAS((unsigned long long *)err, 0ull, (unsigned long long)ERR_TIME) == 0ull)
-                            err[1] = s;
-                        break;
+            bool bad = false;   // time did not advance (invariant)
+            if constexpr (!PK) {
+                const uint32_t m = hmin(dc < dh ? dc : dh);
+                t = t_prev + (int64_t)m;
+                if ((m - 1u) >= D_SLOW - 1u || adv + m >= D_SLOW || t > H_stop) {
+                    t = hmin64(head_end < cpu_next ? head_end : cpu_next);
+                    bad = t <= t_prev;
+                    if (t != INF64) {
+                        dc = cpu_next == INF64 ? D_INF : dsat(cpu_next - t);
+                        dh = head_end == INF64 ? D_INF : dsat(head_end - t);
                     }
+                    adv = 0;
+                    if (!CAL) {
+                        if (t > H_stop) break;
+                        if (bad) {   // report and stop this scenario
+                            if (lane == 0 && atomicCAS((unsigned long long *)err, 0ull, (unsigned long long)ERR_TIME) == 0ull)
+                                err[1] = s;
+                            break;
+                        }
+                    }
+                } else {
+                    dc -= m;
+                    dh -= m;
+                    adv += m;
                 }
-            } else if (PK ? __any_sync(FULL, m == 0xFFFFFFFFu && !fin) : m == 0xFFFFFFFFu) {
-                const int64_t tt = hmin64(mine);
-                t = m == 0xFFFFFFFFu ? tt : t_prev + m;
-            } else t = t_prev + m;
+            } else {   // 64-bit next-event times; 32-bit distances from t_prev, saturated
+                const int64_t mine = fin ? INF64 : (head_end < cpu_next ? head_end : cpu_next);
+                const uint64_t dl = (uint64_t)mine - (uint64_t)t_prev;   // exact when mine > t_prev
+                const uint32_t d32 = mine <= t_prev ? 0u : (dl >= 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)dl);
+                const uint32_t m = hmin(d32);
+                if (__any_sync(FULL, m == 0xFFFFFFFFu && !fin)) {
+                    const int64_t tt = hmin64(mine);
+                    t = m == 0xFFFFFFFFu ? tt : t_prev + m;
+                } else t = t_prev + m;
+                bad = !fin && m == 0u;
+            }
             if (CAL && cal_next < P.cal_end && cal_next < t) {
                 // the state between two steps is constant: one warp max of the AKB urgency
                 // keys (order-preserving unsigned), then one sample per elapsed 1 ms tick
@@ -784,14 +818,14 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             }
             if (CAL && cal_next >= P.cal_end) break;   // no sample left to take
             if (PK) {   // each half ends on its own; the warp goes on while one half runs
-                if (!fin && m == 0u && lane == hbase &&
+                if (bad && lane == hbase &&
                     atomicCAS((unsigned long long *)err, 0ull, (unsigned long long)ERR_TIME) == 0ull)
                     err[1] = s;
-                fin = fin || t > H_stop || m == 0u;
+                fin = fin || t > H_stop || bad;
                 if (__all_sync(FULL, fin)) break;
             } else if (CAL) {
                 if (t > H_stop) break;
-                if (m == 0u) {   // time must advance (invariant); report and stop this scenario
+                if (bad) {   // time must advance (invariant); report and stop this scenario
                     if (lane == 0 && atomicCAS((unsigned long long *)err, 0ull, (unsigned long long)ERR_TIME) == 0ull)
                         err[1] = s;
                     break;
@@ -803,10 +837,10 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             }
 
             // Phase A: retire (R21, R19)
-            const bool ret = !fin && head_end == t;
+            const bool ret = !fin && (PK ? head_end == t : dh == 0u);
             // The retire and due votes are issued together: a retirement makes its own lane due
             // at t only through a sync return of zero cost (retire(): cpu_busy(t, 0) sets cpu_next = t).
-            const bool due_pre = !fin && (cpu_next == t || (ret && pc == PC_SYNC_WAIT && done + 1u >= sync_target &&
+            const bool due_pre = !fin && ((PK ? cpu_next == t : dc == 0u) || (ret && pc == PC_SYNC_WAIT && done + 1u >= sync_target &&
                                                             sync_cost == 0));
             const uint32_t retm = __ballot_sync(FULL, ret), duem = __ballot_sync(FULL, due_pre);
             bool dirty = (retm & hmask) != 0u;   // GPU state changed: Phase C must run
@@ -814,7 +848,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                 used -= hsum(ret ? head_util : 0u);
                 if (ret) retire(t);
             }
-            const bool due = !fin && cpu_next == t;   // == due_pre
+            const bool due = !fin && (PK ? cpu_next == t : dc == 0u);   // == due_pre
             const bool any_due = duem != 0u;
 
             // Phase B: CPU steps of every chain due at t, against the round snapshot (R21)
@@ -882,8 +916,8 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                         want = job && better < P.cpu_cores;
                         __syncwarp();
                     }
-                    if (want && !job_run) { job_run = true; run_start = t; cpu_next = t + job_rem; }
-                    else if (job && !want && job_run) { job_run = false; job_rem -= t - run_start; cpu_next = INF64; }
+                    if (want && !job_run) { job_run = true; run_start = t; cpu_next = t + job_rem; dc = dsat(job_rem); }
+                    else if (job && !want && job_run) { job_run = false; job_rem -= t - run_start; cpu_next = INF64; dc = D_INF; }
                 }
             }
 
@@ -899,7 +933,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                         const int64_t rq = w8 ? free_req : INF64;
                         const int64_t mrq = warp_min_nonneg(rq);
                         const int head = __ffs(__ballot_sync(FULL, w8 && free_req == mrq)) - 1;
-                        if (lane == head) { pc = PC_FREE_RET; cpu_next = t + P.free_ns; }
+                        if (lane == head) { pc = PC_FREE_RET; cpu_next = t + P.free_ns; dc = dsat(P.free_ns); }
                     }
                     continue;   // no dispatch during a barrier
                 }
