@@ -428,7 +428,7 @@ def main():
             torch.cuda.synchronize()
             tt_ms.append(e0.elapsed_time(e1))
         tdw.check(stream)
-        tl = int(tagg[-2].item())
+        tl, tsteps = int(tagg[-2].item()), int(tagg[-1].item())
         tdw.close()
         x = torch.tensor([max(tt_ms)], dtype=torch.float64, device="cuda")
         if world > 1:
@@ -437,7 +437,11 @@ def main():
             "workload": f"scaleout (BASELINE.json configs[4]) workload, {tS} scenarios x 1 s per GPU, UrgenGo; "
                         "throughput build (two scenarios per warp); reported beside the headline, not the metric",
             "value": tl * n / (x.item() / 1e3), "unit": UNIT, "ms_per_launch": x.item(),
-            "launch_events_per_gpu": tl}
+            "launch_events_per_gpu": tl,
+            # the same ALU-pipe roofline as the headline's (algorithmic ALU-pipe warp-inst / kernel time)
+            "roofline": {"bound": "alu", "unit": "Gwarp-inst/s", "peak": peak,
+                         "achieved": (tsteps * ALG_ALU_PER_STEP + tl * ALG_ALU_PER_LAUNCH) / (x.item() / 1e3) / 1e9,
+                         "frac": (tsteps * ALG_ALU_PER_STEP + tl * ALG_ALU_PER_LAUNCH) / (x.item() / 1e3) / 1e9 / peak}}
 
     # ---- cpu_baseline: the oracle, unchanged, on a bounded sample (rank 0, N = 1 only) ----
     if want_cpu:
