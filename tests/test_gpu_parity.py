@@ -122,6 +122,31 @@ def test_small_build_equals_512_thread_build(monkeypatch):
         assert np.array_equal(r1, r2) and np.array_equal(a1, a2), name
 
 
+@pytest.mark.parametrize("build", ["small", "512", "packed"])
+@pytest.mark.parametrize("kind", [URGENGO, FIFO, STATIC])
+def test_long_gaps_and_long_kernels(kind, build, monkeypatch):
+    """Events 2^30..2^33 ns apart and kernels / CPU segments longer than 2^31 ns beside a chain
+    with frequent small events: the kernel's 32-bit next-event distances go far, drift and
+    are refreshed exactly, results equal to the oracle's -- in the small and
+    512-thread latency builds and in the packed throughput build (64-bit head)."""
+    if build == "512":
+        monkeypatch.setenv("URG_SMALL", "0")
+    elif build == "packed":
+        monkeypatch.setenv("URG_WIDE", "1")
+    S = 1_000 * MS
+    a = Chain(6 * S, 5 * S, 0, [Task(1 * MS, 1 * MS, [Kernel(3 * S, 3 * S, 1000), Kernel(1 * MS, 1 * MS, 500)])])
+    b = Chain(1_500 * MS, 1 * S, 2_200 * MS, [Task(2_500 * MS, 2_500 * MS, [Kernel(10 * MS, 10 * MS, 600)])])
+    c = Chain(40 * MS, 30 * MS, 0, [Task(1 * MS, 1 * MS, [Kernel(200 * US, 200 * US, 300), Kernel(2 * MS, 2 * MS, 800)])])
+    idle = Chain(9 * S, 1 * S, 4_400 * MS, [Task(0, 0, [Kernel(5 * MS, 5 * MS, 100)])])
+    for chains in ([a, b, c, idle], [a, idle], [b, idle]):
+        w = Workload(chains=chains, num_prio=6, launch_ns=21_672, launch_akb_ns=500, sync_lo_ns=10 * US,
+                     sync_hi_ns=200 * US, jitter_ns=30 * MS, rt_bins=64, rt_bin_ns=100 * MS)
+        p = Policy(kind=kind, flags=F_ALL if kind == URGENGO else 0, sync_mode=SYNC_OVERLAP,
+                   delta_eval_ns=500 * US, lax_threshold_ns=20 * MS, sleep_ns=1 * MS, util_exempt_permille=100)
+        bb = Batch(seed=0x5EED00AA, scenario_count=5, horizon_ns=20 * S)
+        both(w, p, bb, f"long gaps, {len(chains)} chains, kind {kind}")
+
+
 @pytest.mark.parametrize("name", ["urgengo", "fifo", "static"])
 def test_paper11_small(name):
     """configs[1] workload at a size the oracle finishes in seconds: 48 scenarios x 2 s, spanning many CTAs."""
