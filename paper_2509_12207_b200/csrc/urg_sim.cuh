@@ -23,6 +23,11 @@
 #define D_INF 0xFFFFFFFFu
 #define D_FAR 0x80000000u
 #define D_SLOW 0x40000000u
+#ifdef URG_NO_DIST
+#define URG_DIST_OFF true
+#else
+#define URG_DIST_OFF false
+#endif
 
 enum { K_FIFO = 0, K_STATIC = 1, K_URGENGO = 2, K_EDF = 3, K_SJF = 4, K_HRRN = 5, K_LCUF = 6 };
 enum { F_BIND = 1, F_DELAY = 2, F_EARLY = 4, F_COLL = 8 };
@@ -174,7 +179,7 @@ __device__ __forceinline__ uint64_t work_offset(uint64_t j, uint64_t S, uint32_t
 template <int KIND, int FLAGS, bool KQ, bool WIDE, bool CAL = false, bool EXT = true, bool PK = false,
           bool SMALL = false>
 #ifndef URG_PK_THREADS
-#define URG_PK_THREADS 768   // measured: 80 registers beat 64 with spills (configs[2]/[4] +3-4 %)
+#define URG_PK_THREADS 640   // measured: 96 registers (20 warps/SM) beat 80 at 768 threads with the kept distances
 #endif
 #ifndef URG_LAT_THREADS
 #define URG_LAT_THREADS 512
@@ -759,22 +764,21 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             // of 2^30 or more (a far lane may be nearer than it says), a drift of 2^30 since the
             // last refresh, or the end of the horizon take the rare path: the exact 64-bit
             // minimum, with every distance recomputed from it.
-            // (the packed build keeps 64-bit times at the head: the distances cost it registers,
-            // measured 3 % slower)
             int64_t t;
             bool bad = false;   // time did not advance (invariant)
-            if constexpr (!PK) {
-                const uint32_t m = hmin(dc < dh ? dc : dh);
+            if constexpr (!URG_DIST_OFF) {   // (the 64-bit head below is kept for A/B: -DURG_NO_DIST)
+                const uint32_t m = hmin(fin ? D_INF : (dc < dh ? dc : dh));
                 t = t_prev + (int64_t)m;
-                if ((m - 1u) >= D_SLOW - 1u || adv + m >= D_SLOW || t > H_stop) {
-                    t = hmin64(head_end < cpu_next ? head_end : cpu_next);
-                    bad = t <= t_prev;
-                    if (t != INF64) {
+                const bool slow = !fin && ((m - 1u) >= D_SLOW - 1u || adv + m >= D_SLOW || t > H_stop);
+                if (PK ? __any_sync(FULL, slow) : slow) {
+                    t = hmin64(fin ? INF64 : (head_end < cpu_next ? head_end : cpu_next));
+                    bad = !fin && t <= t_prev;
+                    if (!fin && t != INF64) {
                         dc = cpu_next == INF64 ? D_INF : dsat(cpu_next - t);
                         dh = head_end == INF64 ? D_INF : dsat(head_end - t);
                     }
                     adv = 0;
-                    if (!CAL) {
+                    if (!PK && !CAL) {
                         if (t > H_stop) break;
                         if (bad) {   // report and stop this scenario
                             if (lane == 0 && atomicCAS((unsigned long long *)err, 0ull, (unsigned long long)ERR_TIME) == 0ull)
@@ -837,10 +841,10 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             }
 
             // Phase A: retire (R21, R19)
-            const bool ret = !fin && (PK ? head_end == t : dh == 0u);
+            const bool ret = !fin && (URG_DIST_OFF ? head_end == t : dh == 0u);
             // The retire and due votes are issued together: a retirement makes its own lane due
             // at t only through a sync return of zero cost (retire(): cpu_busy(t, 0) sets cpu_next = t).
-            const bool due_pre = !fin && ((PK ? cpu_next == t : dc == 0u) || (ret && pc == PC_SYNC_WAIT && done + 1u >= sync_target &&
+            const bool due_pre = !fin && ((URG_DIST_OFF ? cpu_next == t : dc == 0u) || (ret && pc == PC_SYNC_WAIT && done + 1u >= sync_target &&
                                                             sync_cost == 0));
             const uint32_t retm = __ballot_sync(FULL, ret), duem = __ballot_sync(FULL, due_pre);
             bool dirty = (retm & hmask) != 0u;   // GPU state changed: Phase C must run
@@ -848,7 +852,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                 used -= hsum(ret ? head_util : 0u);
                 if (ret) retire(t);
             }
-            const bool due = !fin && (PK ? cpu_next == t : dc == 0u);   // == due_pre
+            const bool due = !fin && (URG_DIST_OFF ? cpu_next == t : dc == 0u);   // == due_pre
             const bool any_due = duem != 0u;
 
             // Phase B: CPU steps of every chain due at t, against the round snapshot (R21)
