@@ -41,7 +41,7 @@ UNIT = "launch events/s"
 # ALU-pipe ones (integer compare/add/select/shift/logic; the rest are warp collectives,
 # loads, branches and the two IMAD.WIDE of the duration).  The bound is the ALU pipe:
 # one warp-instruction per 2 cycles per scheduler (B300_MICROARCH.md "alu-pipe rt_SMSP=2";
-# ncu: 84 % busy in the throughput build), so peak = SMs x 4 x 0.5 x sm_max_mhz; the
+# ncu: 80-84 % busy in the throughput build), so peak = SMs x 4 x 0.5 x sm_max_mhz; the
 # issue peak (1 warp-instruction/clk/scheduler) is reported beside it.
 ALG_INST_PER_STEP = 24
 ALG_INST_PER_LAUNCH = 40
