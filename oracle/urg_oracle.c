@@ -25,7 +25,10 @@
  * Everything the paper leaves open is a DESIGN.md "Model M0" reading (R0-R23);
  * comments name the rule.  All time is int64 nanoseconds, no floating point.
  *
- * Parity pins for every exported function: tests/test_oracle_*.py.
+ * Parity pins for every exported function and every scenario draw: tests/test_oracle_*.py
+ * (the draws R3-R5 -- factors, tight subset, arrivals, per-instance / per-kernel factors, sync
+ * costs -- in test_oracle_draws.py; R15's levels at NUM_PRI > 2 in the W11 fixture and an exact
+ * trace replay; R21's same-t continuation in the W10 fixture).
  * Unpinned: the Table 2 C2/C7 rank tie (Q7) -- "parity unpinned".
  */
 #include <stdint.h>
@@ -33,6 +36,9 @@
 #include <string.h>
 
 #define ORC_INF INT64_MAX
+/* The oracle's own size limit: the rank / dispatch / CPU-job scratch arrays hold 64 entries.  It is
+ * not the GPU path's limit (one warp lane per chain: 32, rejected there with URG_ERANGE). */
+#define ORC_MAX_CHAINS 64
 
 /* ------------------------------------------------------------------ */
 /* Input records (mirrors workloads/spec.py; oracle-private definition) */
@@ -465,8 +471,10 @@ uint32_t orc_classical_rank(uint32_t kind, const int64_t *tarr, const int64_t *D
     orc_sim S;
     memset(&S, 0, sizeof S);
     S.in = &in;
-    orc_cl_item it[64];
-    for (uint32_t i = 0; i < n && i < 64; ++i) {
+    orc_cl_item it[ORC_MAX_CHAINS];
+    if (n > ORC_MAX_CHAINS) n = ORC_MAX_CHAINS;
+    if (self >= n) return 0;
+    for (uint32_t i = 0; i < n; ++i) {
         it[i].chain = i; it[i].tarr = tarr[i]; it[i].D = D[i]; it[i].R = R[i]; it[i].G = G[i]; it[i].Pp = Pp[i];
     }
     uint32_t r = 1;
@@ -483,7 +491,7 @@ static uint32_t bind_level(orc_sim *S, uint32_t c, int64_t own_L, int64_t t)
     if (classical(S)) {
         /* rank among the chain itself and every other chain with active kernels (read view),
          * normalised like UrgenGo's non-urgent ranks (R15) */
-        orc_cl_item it[64];
+        orc_cl_item it[ORC_MAX_CHAINS];
         uint32_t n = 0;
         for (uint32_t o = 0; o < S->nL; ++o) {
             if (o != c && S->snap_n[o] == 0) continue;
@@ -504,7 +512,7 @@ static uint32_t bind_level(orc_sim *S, uint32_t c, int64_t own_L, int64_t t)
     }
     if (!(in->flags & ORC_BIND)) return in->num_prio - 1;
     if (orc_is_urgent(own_L, in->lax_threshold_ns)) return 0;
-    int64_t keys[64]; uint32_t chains[64], ranks[64], n = 0;
+    int64_t keys[ORC_MAX_CHAINS]; uint32_t chains[ORC_MAX_CHAINS], ranks[ORC_MAX_CHAINS], n = 0;
     keys[n] = orc_urgency_key(own_L); chains[n] = c; ++n;
     for (uint32_t o = 0; o < S->nL; ++o)
         if (o != c && S->snap_n[o] > 0) { keys[n] = orc_urgency_key(S->snap_L[o]); chains[n] = o; ++n; }
@@ -868,7 +876,7 @@ static int is_copy(const orc_sim *S, uint32_t c, uint32_t K)
 
 static void dispatch(orc_sim *S, int64_t t)
 {
-    orc_cand cand[64];
+    orc_cand cand[ORC_MAX_CHAINS];
     uint32_t n = 0;
     if (barrier(S, t)) return;
     /* the copy engine (Table 3 "cuMemCpy: no stream priority"; SPEC.md:271;
@@ -964,7 +972,7 @@ static void cpu_schedule(orc_sim *S, int64_t t)
     }
     if (!S->cpu_dirty) return;
     S->cpu_dirty = 0;
-    orc_job jobs[64];
+    orc_job jobs[ORC_MAX_CHAINS];
     uint32_t n = 0;
     for (uint32_t c = 0; c < S->nL; ++c) {
         const orc_lane *L = &S->lane[c];
@@ -1053,8 +1061,8 @@ static int sim_scenario(const orc_input *in_all, uint64_t s, uint32_t *rec, int6
         tb += M; kb += N;
     }
     /* scenario factors (R3): P' = P / f_a, D' = D * f_d, tight set halved */
-    uint32_t tight = 0;
-    if (in->tight_explicit) tight = in->tight_mask;
+    uint64_t tight = 0;
+    if (in->tight_explicit) tight = in->tight_mask;   /* an explicit mask names chains 0..31 */
     else if (in->ftight_permille) {
         uint32_t n_tight = (in->ftight_permille * S.C + 999) / 1000;
         for (uint32_t c = 0; c < S.C; ++c) {
@@ -1063,7 +1071,7 @@ static int sim_scenario(const orc_input *in_all, uint64_t s, uint32_t *rec, int6
                 uint32_t wo = orc_word(in->seed, s, TAG_TIGHT, o, 0, 0);
                 if (wo < wc || (wo == wc && o < c)) ++rank;
             }
-            if (rank < n_tight) tight |= 1u << c;
+            if (rank < n_tight) tight |= 1ull << c;
         }
     }
     int64_t maxD = 0;
@@ -1072,7 +1080,7 @@ static int sim_scenario(const orc_input *in_all, uint64_t s, uint32_t *rec, int6
         orc_lane *L = &S.lane[c];
         L->Pp = in->ch_period[L->chain] * (int64_t)in->fa_den / (int64_t)in->fa_num;
         L->Dp = in->ch_deadline[L->chain] * (int64_t)in->fd_num / (int64_t)in->fd_den;
-        if (tight & (1u << L->chain)) L->Dp /= 2;
+        if (tight & (1ull << L->chain)) L->Dp /= 2;
         if (L->Dp > maxD) maxD = L->Dp;
         chD[L->chain] = L->Dp;
     }
@@ -1189,7 +1197,7 @@ static int sim_scenario(const orc_input *in_all, uint64_t s, uint32_t *rec, int6
 int orc_run(const orc_input *in, uint32_t *records, int64_t *agg,
             int64_t *trace, int64_t trace_cap, int64_t *trace_len)
 {
-    if (!in || in->num_chains == 0 || in->num_chains > 32) return -1;
+    if (!in || in->num_chains == 0 || in->num_chains > ORC_MAX_CHAINS) return -1;
     if (in->fa_num == 0 || in->fa_den == 0 || in->fd_den == 0 || in->rt_bins == 0 || in->rt_bin_ns <= 0) return -1;
     if (in->t_flags) {                                /* a served cudaFree takes time (R28) */
         uint32_t nt = 0;
@@ -1198,10 +1206,10 @@ int orc_run(const orc_input *in, uint32_t *records, int64_t *agg,
     }
     for (uint32_t c = 0; c < in->num_chains; ++c)     /* arrivals strictly increasing: P' > J (R3) */
         if (in->ch_period[c] * (int64_t)in->fa_den / (int64_t)in->fa_num <= in->jitter_ns) return -2;
-    if (in->task_exec) {                              /* R32: at most 32 threads; no R26 predictor */
+    if (in->task_exec) {                              /* R32: at most ORC_MAX_CHAINS threads; no R26 predictor */
         uint32_t nt = 0;
         for (uint32_t c = 0; c < in->num_chains; ++c) nt += in->ch_ntasks[c];
-        if (nt > 32) return -2;
+        if (nt > ORC_MAX_CHAINS) return -2;
         if (in->cpu_ma_window) return -1;
     }
     if (trace_len) *trace_len = 0;

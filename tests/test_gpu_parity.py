@@ -69,6 +69,43 @@ def test_w3():
     both(w3(), Policy(kind=FIFO, flags=0, sync_mode=SYNC_ASYNC), Batch(horizon_ns=1 * MS))
 
 
+@pytest.mark.parametrize("build", ["small", "512", "packed", "ext"])
+def test_w10_zero_cost_satisfied_sync(build, monkeypatch):
+    """Fixture W10 (tests/golden/w10.json): a satisfied zero-cost OVERLAP sync continues in the same
+    Phase B step against the step's snapshot (R21) -- in every build."""
+    from workloads import w10
+    from workloads.spec import F_DELAY
+    _build_env(build, monkeypatch)
+    p = Policy(kind=URGENGO, flags=F_DELAY, sync_mode=SYNC_OVERLAP, delta_eval_ns=500 * US, lax_threshold_ns=5 * MS)
+    o, r, a = both(w10(), p, Batch(horizon_ns=1 * MS, scenario_count=_count(build)), f"w10 {build}")
+    assert int(r[0, 0, 6]) == 1_600_000 and int(r[0, 1, 6]) == 2_200_000
+
+
+@pytest.mark.parametrize("build", ["small", "512", "packed", "ext"])
+def test_w11_binding_levels_num_pri_6(build, monkeypatch):
+    """Fixture W11 (tests/golden/w11.json): NUM_PRI = 6 rank normalisation decides the dispatch order."""
+    from workloads import w11
+    from workloads.spec import F_BIND
+    _build_env(build, monkeypatch)
+    p = Policy(kind=URGENGO, flags=F_BIND, sync_mode=SYNC_ASYNC, lax_threshold_ns=1 * MS)
+    o, r, a = both(w11(), p, Batch(horizon_ns=10 * MS, scenario_count=_count(build)), f"w11 {build}")
+    assert [int(r[0, c, 6]) // MS for c in range(6)] == [51, 52, 53, 103, 101, 102]
+
+
+def _build_env(build, monkeypatch):
+    """Select a kernel build through the test hooks of urg_api.cu (fixture batches are tiny)."""
+    if build == "512":
+        monkeypatch.setenv("URG_SMALL", "0")
+    elif build == "packed":
+        monkeypatch.setenv("URG_WIDE", "1")
+    elif build == "ext":
+        monkeypatch.setenv("URG_EXT", "1")
+
+
+def _count(build):
+    return 2 if build == "packed" else 1   # both halves of a packed warp run the same fixture
+
+
 @pytest.mark.parametrize("mode", [SYNC_ASYNC, SYNC_EACH, SYNC_BATCHED, SYNC_OVERLAP])
 def test_toy2_all_policies(mode):
     """BASELINE.json configs[0]: every policy and UrgenGo flag combination, bit-exact."""

@@ -194,6 +194,6 @@ def test_rejects_predictor_and_too_many_threads():
     w.executors = EXEC_TASK
     with pytest.raises(ValueError):
         O.run(w, Policy(cpu_ma_window=4), Batch())
-    w.chains = w.chains + w.chains[:6]   # 17 chains, 34 tasks > 32 threads
+    w.chains = w.chains * 3              # 33 chains, 66 tasks > the oracle's 64 threads
     with pytest.raises(ValueError):
         O.run(w, Policy(), Batch())

@@ -358,3 +358,66 @@ def test_toy2_fifo_first_dispatches():
            if k == O.TRACE_CODES["DISPATCH"]][:8]
     want = [[c, i, k, int(round(s * MS)), int(round(e * MS))] for c, i, k, s, e in g["dispatches"]]
     assert got == want
+
+
+# ---------------------------------------------------------------------------
+# W10: a zero-cost, already-satisfied OVERLAP sync (R21 same-t continuation)
+# ---------------------------------------------------------------------------
+
+def _w10_policy():
+    from workloads.spec import F_DELAY
+    return Policy(kind=URGENGO, flags=F_DELAY, sync_mode=SYNC_OVERLAP, delta_eval_ns=500 * US,
+                  lax_threshold_ns=5 * MS, sleep_ns=1 * MS, util_exempt_permille=100)
+
+
+def test_w10_zero_cost_satisfied_sync():
+    """PAPER.md:504-509 with sigma = 0: A's second batch close at 1.2 ms waits for a batch that is
+    already complete; the sync returns at the same t and A's next launch attempt reads the Phase B
+    snapshot taken before B's kernel reached the AKB -> no delay, rt_A = 1.6 ms (the per-round
+    reading of SURVEY.md:529-532 would give 3.5 ms)."""
+    from workloads import w10
+    g = _gold("w10.json")
+    r = O.run(w10(), _w10_policy(), Batch(horizon_ns=1 * MS), trace_cap=1000)
+    rec = r.records[0]
+    for c in range(2):
+        assert rec[c, REC_TOTAL] == 1
+        assert _sum_rt(rec[c]) == int(round(g["rt_ms"][c] * MS))
+        assert rec[c, REC_MISS] == g["miss"][c]
+    assert r.launches == g["launches"]
+    K = O.TRACE_CODES
+    assert sum(1 for row in r.trace if row[1] == K["DELAY"]) == g["delays"]
+    s = g["satisfied_sync"]
+    t12 = int(round(s["t_ms"] * MS))
+    calls = [(int(t), int(a), int(b)) for t, k, c, i, a, b in r.trace if k == K["SYNC_CALL"] and c == s["chain"]]
+    assert (t12, s["target"], s["cost"]) in calls
+    rets = [int(t) for t, k, c, i, a, b in r.trace if k == K["SYNC_RET"] and c == s["chain"]]
+    assert t12 in rets, "the satisfied zero-cost sync returns at the call time"
+    # the next launch attempt of A is evaluated at that same t (one loop step: exactly one STEP at 1.2 ms)
+    assert sum(1 for row in r.trace if row[1] == K["STEP"] and row[0] == t12) == 1
+    enq = [(int(t), int(a)) for t, k, c, i, a, b in r.trace if k == K["ENQUEUE"] and c == 0]
+    assert enq == [(1_100_000, 0), (1_200_000, 1), (1_300_000, 2)]
+
+
+# ---------------------------------------------------------------------------
+# W11: UrgenGo's rank normalisation at NUM_PRI = 6 inside a simulation (R15)
+# ---------------------------------------------------------------------------
+
+def test_w11_binding_levels_num_pri_6():
+    from workloads import w11
+    from workloads.spec import F_BIND
+    g = _gold("w11.json")
+    p = Policy(kind=URGENGO, flags=F_BIND, sync_mode=SYNC_ASYNC, lax_threshold_ns=1 * MS)
+    r = O.run(w11(), p, Batch(horizon_ns=10 * MS), trace_cap=1000)
+    K = O.TRACE_CODES
+    ev = {int(c): int(a) for t, k, c, i, a, b in r.trace if k == K["EVAL"] and int(t) == (int(c) + 1) * MS}
+    assert [ev[c] for c in range(6)] == [x * MS for x in g["laxity_at_binding_ms"]]
+    binds = sorted((int(c), int(a)) for t, k, c, i, a, b in r.trace if k == K["BIND"])
+    assert [lv for _, lv in binds] == g["levels"]
+    rec = r.records[0]
+    assert [_sum_rt(rec[c]) for c in range(6)] == [x * MS for x in g["rt_ms"]]
+    assert rec[:, REC_MISS].tolist() == g["miss"]
+    assert O.overall_miss_ratio(rec[:, REC_MISS], rec[:, REC_TOTAL]) == g["eq3"]
+    assert r.launches == g["launches"]
+    # without binding every task sits at NUM_PRI - 1 and the waiting heads go in ready order
+    rf = O.run(w11(), Policy(kind=FIFO, flags=0, sync_mode=SYNC_ASYNC), Batch(horizon_ns=10 * MS))
+    assert [_sum_rt(rf.records[0, c]) for c in range(6)] == [x * MS for x in g["fifo_rt_ms"]]

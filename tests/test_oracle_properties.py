@@ -164,6 +164,70 @@ def test_delay_and_binding_rules_in_trace():
     assert checked_delay > 0 and checked_bind > 0
 
 
+def _ul_rank_key(L, chain):
+    """Sort key: most urgent first by UL = 1/L (L = 0 saturates to +inf),
+    ties by the smaller chain id.  Exact rationals -- no laxity key trick."""
+    from fractions import Fraction
+    ul = Fraction(10**30) if L == 0 else Fraction(1, L)
+    return (-ul, chain)
+
+
+def _normalised_level(r, n_r, num_prio):
+    """R15 written from PAPER.md:466 "normalize these rankings to the range (1, NUM_PRI-1)" and
+    SPEC.md:402-404 (n_r = 4: rank 1 -> 1, rank 4 -> 5; n_r = 1 -> the middle level)."""
+    if num_prio <= 2:
+        return num_prio - 1
+    if n_r == 1:
+        return 1 + (num_prio - 2) // 2
+    return 1 + ((r - 1) * (num_prio - 2)) // (n_r - 1)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_binding_level_exact_in_trace(seed):
+    """Every UrgenGo binding (R15) replayed from the trace with NUM_PRI in {3, 4, 6, 8}: an urgent
+    task takes level 0; any other ranks among itself and the chains AKB-active in the Phase B
+    snapshot by the exact 1/L order, and takes the normalised level recomputed here."""
+    rng = random.Random(4242 + seed)
+    checked = {0: 0, 1: 0}
+    for trial in range(6):
+        w = random_workload(rng, C=rng.randint(3, 7))
+        w.num_prio = rng.choice([3, 4, 6, 8])
+        p = Policy(kind=URGENGO, flags=F_BIND | rng.choice([0, F_DELAY]), sync_mode=rng.choice([SYNC_ASYNC, SYNC_OVERLAP]),
+                   lax_threshold_ns=rng.choice([1 * MS, 5 * MS, 15 * MS]))
+        r = O.run(w, p, Batch(seed=trial, horizon_ns=200 * MS), trace_cap=2_000_000)
+        akb = [0] * w.num_chains
+        launched = [0] * w.num_chains
+        L = [0] * w.num_chains
+        snapL, snapA = list(L), list(akb)
+        for t, kind, c, i, a, bb in r.trace:
+            t, kind, c, i, a, bb = map(int, (t, kind, c, i, a, bb))
+            if kind == K["STEP"]:
+                snapL, snapA = list(L), list(akb)
+            elif kind == K["EVAL"]:
+                L[c] = a
+            elif kind == K["ENQUEUE"]:
+                akb[c] += 1
+                launched[c] = a + 1
+            elif kind == K["INST_START"]:
+                launched[c] = 0
+            elif kind == K["EARLY_EXIT"]:
+                akb[c] = 0
+            elif kind == K["SYNC_RET"]:
+                akb[c] = launched[c] - a
+            elif kind == K["BIND"]:
+                own = L[c]                       # the EVAL of this launch attempt
+                if 0 <= own <= p.lax_threshold_ns:
+                    assert a == 0
+                    checked[0] += 1
+                    continue
+                members = [(own, c)] + [(snapL[o], o) for o in range(w.num_chains) if o != c and snapA[o] > 0]
+                order = sorted(members, key=lambda m: _ul_rank_key(*m))
+                rnk = 1 + [m[1] for m in order].index(c)
+                assert a == _normalised_level(rnk, len(members), w.num_prio), (t, c, rnk, len(members))
+                checked[1] += 1
+    assert checked[1] > 20
+
+
 def _records(w, p, b):
     return O.run(w, p, b).records
 
@@ -607,3 +671,24 @@ def test_copy_engine_invariants(seed):
             else:
                 used -= util[c][a]
     assert n_copy > 0
+
+
+def test_oracle_is_not_limited_to_a_warp():
+    """The oracle's chain limit is its own (64, its scratch arrays), not the GPU path's 32 lanes: a
+    40-chain workload simulates under three policies with every trace invariant and every arrival
+    admitted; 65 chains are rejected."""
+    rng = random.Random(5)
+    w = random_workload(rng, C=40)
+    for p in (Policy(kind=FIFO, flags=0, sync_mode=SYNC_ASYNC),
+              Policy(kind=URGENGO, flags=F_BIND | F_DELAY, sync_mode=SYNC_OVERLAP, lax_threshold_ns=5 * MS),
+              Policy(kind=STATIC, flags=0, sync_mode=SYNC_EACH)):
+        b = Batch(seed=11, horizon_ns=100 * MS, ftight_permille=400)
+        r = O.run(w, p, b, trace_cap=2_000_000)
+        check_trace_invariants(w, p, b, r)
+        assert r.records.shape[1] == 40
+        for c, ch in enumerate(w.chains):
+            n = 0 if ch.offset_ns >= b.horizon_ns else -(-(b.horizon_ns - ch.offset_ns) // ch.period_ns)
+            assert r.records[0, c, 0] == n
+    w.chains = w.chains + w.chains[:25]
+    with pytest.raises(ValueError):
+        O.run(w, Policy(kind=FIFO, flags=0, sync_mode=SYNC_ASYNC), Batch(horizon_ns=10 * MS))

@@ -224,3 +224,31 @@ def w9(copies: bool = True) -> Workload:
     a = Chain(1000 * MS, 100 * MS, 0, [Task(1 * MS, 1 * MS, [Kernel(1 * MS, 1 * MS, 500, f), Kernel(2 * MS, 2 * MS, 500)])])
     b = Chain(1000 * MS, 100 * MS, 0, [Task(500 * US, 500 * US, [Kernel(2 * MS, 2 * MS, 500, f), Kernel(1 * MS, 1 * MS, 500)])])
     return Workload(chains=[a, b], num_prio=2, launch_ns=0, launch_akb_ns=0, sync_lo_ns=0, sync_hi_ns=0, jitter_ns=0)
+
+
+def w10() -> Workload:
+    """Fixture W10 (tests/golden/w10.json): a zero-cost, already-satisfied OVERLAP sync (PAPER.md:504-509,
+    sigma = 0 at the low end of P:494's range made exact) -- the same-t continuation of DESIGN.md R21.
+    Chain A overlaps its batches; chain B is urgent and becomes AKB-active at the very time A's
+    satisfied sync returns."""
+    a = Chain(1000 * MS, 100 * MS, 0, [Task(1 * MS, 1 * MS, [Kernel(50 * US, 600 * US, 100),
+                                                            Kernel(200 * US, 600 * US, 100),
+                                                            Kernel(200 * US, 600 * US, 500)])])
+    b = Chain(1000 * MS, 4 * MS, 0, [Task(1_100_000, 1_100_000, [Kernel(1 * MS, 1 * MS, 100)])])
+    return Workload(chains=[a, b], num_prio=2, launch_ns=100 * US, launch_akb_ns=0, sync_lo_ns=0, sync_hi_ns=0,
+                    jitter_ns=0)
+
+
+W11_ESTIMATES_MS = (49, 58, 52, 36, 53, 44)
+
+
+def w11() -> Workload:
+    """Fixture W11 (tests/golden/w11.json): UrgenGo's rank normalisation with NUM_PRI = 6 inside a
+    simulation ("normalize ... to (1, NUM_PRI-1)").  Six chains bind
+    one after another (CPU segments of 1..6 ms) while the earlier ones stay AKB-active; kernel
+    estimates are chosen so the laxities at binding are 50, 40, 45, 60, 42, 50 ms.  Each kernel
+    takes 300 permille, so only three run at once and the levels decide the later dispatch order."""
+    chains = [Chain(1000 * MS, 100 * MS, 0, [Task((i + 1) * MS, 0, [Kernel(50 * MS, e * MS, 300)])])
+              for i, e in enumerate(W11_ESTIMATES_MS)]
+    return Workload(chains=chains, num_prio=6, launch_ns=0, launch_akb_ns=0, sync_lo_ns=0, sync_hi_ns=0,
+                    jitter_ns=0)
