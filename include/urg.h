@@ -178,12 +178,18 @@ urg_status urg_simulate_batch(const urg_workload *w, const urg_policy *p, const 
                               const urg_outputs *o, void *cuda_stream);
 
 /* Same with HOST output buffers: allocates device outputs, simulates, copies
- * records and agg back (agg is ADDED into the host buffer).  Synchronous. */
+ * records and agg back (agg is ADDED into the host buffer).  Synchronous; a device
+ * invariant trip of this call is returned as URG_EINTERNAL (as urg_check would). */
 urg_status urg_simulate_batch_host(const urg_workload *w, const urg_policy *p, const urg_batch *b,
                                    const urg_outputs *host_o, void *cuda_stream);
 
 /* Synchronise cuda_stream and report a device-side invariant trip recorded by an
- * earlier urg_simulate_batch (URG_EINTERNAL, *scenario_out = offending scenario). */
+ * earlier urg_simulate_batch (URG_EINTERNAL, *scenario_out = offending scenario).
+ * The first trip since the last report is kept; reporting clears the device error
+ * word, so a later trip on the same workload is reported by a later call.
+ * Thread safety: calls on one workload must be ordered (one stream); launches of
+ * different workloads from several host threads are safe (the per-kernel attribute
+ * set and the launch are serialised inside the library). */
 urg_status urg_check(const urg_workload *w, void *cuda_stream, int64_t *scenario_out);
 
 /* TH_urgent calibration ("periodically recording the highest urgency

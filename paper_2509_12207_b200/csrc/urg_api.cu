@@ -11,6 +11,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -52,6 +53,11 @@ struct urg_workload {
 };
 
 static thread_local std::string g_err;
+
+// cudaFuncSetAttribute (dynamic shared memory, carveout) is process-global per kernel function:
+// the attribute set of one launch and its <<<>>> stay together under this lock, so two host
+// threads launching the same instantiation with different geometries cannot interleave.
+static std::mutex g_launch_mu;
 
 static urg_status fail(urg_status st, const char *fmt, ...)
 {
@@ -430,6 +436,7 @@ extern "C" urg_status urg_simulate_batch(const urg_workload *w, const urg_policy
     UrgSimParams P;
     urg_sim_fn fn;
     int warps, ctas;
+    std::lock_guard<std::mutex> lk(g_launch_mu);
     st = prepare_launch(w, p, b, wide, false, P, fn, warps, ctas);
     if (st != URG_OK) return st;
     CUDA_TRY(cudaMemsetAsync(w->d_work, 0, 8, s), "cudaMemsetAsync(work counter)");
@@ -468,6 +475,7 @@ extern "C" urg_status urg_calibrate(const urg_workload *w, const urg_policy *p, 
     UrgSimParams P;
     urg_sim_fn fn;
     int warps, ctas;
+    std::lock_guard<std::mutex> lk(g_launch_mu);
     st = prepare_launch(w, &pc, b, false, true, P, fn, warps, ctas);
     if (st != URG_OK) return st;
     P.cal_end = cal_end(b, window_ns);
@@ -486,6 +494,8 @@ extern "C" urg_status urg_calibrate(const urg_workload *w, const urg_policy *p, 
     CUDA_TRY(cudaGetLastError(), "launching the nearest-rank selection");
     return URG_OK;
 }
+
+extern "C" urg_status urg_check(const urg_workload *w, void *cuda_stream, int64_t *scenario_out);
 
 extern "C" urg_status urg_simulate_batch_host(const urg_workload *w, const urg_policy *p, const urg_batch *b,
                                               const urg_outputs *host_o, void *cuda_stream)
@@ -513,6 +523,9 @@ extern "C" urg_status urg_simulate_batch_host(const urg_workload *w, const urg_p
     cudaFreeAsync(d.agg, s);
     if (d.records) cudaFreeAsync(d.records, s);
     if (st != URG_OK) return st;
+    // a synchronous call reports a device invariant trip itself (and clears the word)
+    st = urg_check(w, cuda_stream, nullptr);
+    if (st != URG_OK) return st;
     for (uint64_t i = 0; i < nagg; ++i) host_o->agg[i] += tmp[i];
     return URG_OK;
 }
@@ -526,9 +539,13 @@ extern "C" urg_status urg_check(const urg_workload *w, void *cuda_stream, int64_
     CUDA_TRY(cudaMemcpyAsync(e2, w->d_err, sizeof e2, cudaMemcpyDeviceToHost, s), "reading the error word");
     CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
     if (scenario_out) *scenario_out = e2[1];
-    if (e2[0] != 0)
+    if (e2[0] != 0) {
+        // reported once: cleared so a later trip on this workload is recorded and reported too
+        CUDA_TRY(cudaMemsetAsync(w->d_err, 0, sizeof e2, s), "clearing the error word");
+        CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
         return fail(URG_EINTERNAL, "device invariant %lld tripped in scenario %lld (%s)", e2[0], e2[1],
-                    e2[0] == 1 ? "time did not advance" : "step iteration guard");
+                    e2[0] == 1 ? "time did not advance" : e2[0] == 2 ? "step iteration guard" : "debug-build invariant");
+    }
     return URG_OK;
 }
 

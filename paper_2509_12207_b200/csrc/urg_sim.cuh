@@ -67,6 +67,15 @@ static __device__ __noinline__ uint32_t rng_word(uint64_t seed, uint32_t s, uint
 }
 
 
+// All four words of the block holding word (tag, c, i, k): words k & ~3 .. k | 3 share one
+// Philox call (R4; the per-kernel draws are cached four at a time).
+static __device__ __noinline__ uint4 rng_block(uint64_t seed, uint32_t s, uint32_t tag, uint32_t c, uint32_t i,
+                                               uint32_t k)
+{
+    return philox4x32_10(make_uint4(s, (tag << 24) | (c << 16), i, k >> 2),
+                         make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
+}
+
 // ---------------------------------------------------------------------------
 // small warp helpers
 // ---------------------------------------------------------------------------
@@ -211,12 +220,25 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
     uint32_t *snapLev = (uint32_t *)(snapL + 96);
     uint32_t *mbox = (uint32_t *)(snapL + 112);   // R32: message published to each lane this round
     UrgVarRec *myvar = (UrgVarRec *)(snapL + 128);  // R33: each lane's variant estimate totals
+    uint4 *kqw = (uint4 *)(snapL + 192);            // R4: the lane's current block of four KERN words
     constexpr bool urg = KIND == K_URGENGO;
     constexpr bool cls = KIND >= K_EDF;        // classical policies (R27): AKB-tracking, no urgency
     constexpr bool akb_on = urg || cls;
     constexpr bool f_bind = urg && (FLAGS & F_BIND), f_delay = urg && (FLAGS & F_DELAY),
                    f_early = urg && (FLAGS & F_EARLY);
     constexpr bool coll = urg && (FLAGS & F_COLL);   // collision metric (R24): not in the schedule
+    // Core build: Phase C's fit ballot runs at every step and is itself the test, so no "new
+    // stream head" vote sits between Phase B and Phase C (a head that did not fit at an earlier
+    // Phase C still does not: `used` only falls at a retirement).
+    // Measured: +1-2 % on UrgenGo packed; the latency build ran 3x slower; the ASYNC policies
+    // (FIFO / STATIC) lost 13 % with it (configs[2]) and keep the new-head vote.
+#ifdef URG_OLD_CALWAYS
+    constexpr bool c_always = PK && !EXT && !CAL;
+    constexpr bool r17_sel = true;
+#else
+    constexpr bool c_always = PK && !EXT && !CAL && urg;
+    constexpr bool r17_sel = urg;   // R17 with selects for UrgenGo, branches for the others
+#endif
     const bool noise = EXT && urg && P.noise_pm > 0;       // R25
     const bool ma = EXT && akb_on && P.ma_w > 0;           // R26 (every policy that estimates remaining work)
     const bool has_free = EXT && P.has_free != 0;          // R28: some task ends with cudaFree
@@ -465,7 +487,17 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         // Phase C start of this lane's waiting head: non-preemptive, exact duration (R4, R19, R20)
         auto start_head = [&](int64_t t, uint32_t u_run) {
             uint64_t G = 65536u;
+#ifdef URG_NO_KQCACHE
             if (KQ) G = T.kern_q[rng_word(P.seed, s, URG_TAG_KERN, cid, inst, done) >> 20];
+#else
+            if (KQ) {
+                // A lane starts its kernels in stream order: kernel `done` follows `done` - 1 of the
+                // same instance, so the four words of a Philox block are drawn once and kept in the
+                // lane's shared-memory slot; a new block (or the instance's first kernel) refills it.
+                if ((done & 3u) == 0u || done == k_first) kqw[lane] = rng_block(P.seed, s, URG_TAG_KERN, cid, inst, done);
+                G = T.kern_q[((const uint32_t *)&kqw[lane])[done & 3u] >> 20];
+            }
+#endif
             uint64_t d = ((((uint64_t)head_nom * Fg) >> 16) * G) >> 16;
             d = d < 1 ? 1 : (d > 0xFFFFFFFFull ? 0xFFFFFFFFull : d);
             if (contend && !head_copy) d += d * (uint64_t)P.alpha_pm * u_run / 1000000ull;   // R30
@@ -618,18 +650,36 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     }
                     const bool last = launched == task_end;
                     if (last) rem_c -= ma ? ma_pred[task] : T.task[tbase + task].cpu_estimate_ns;
-                    // R17 with selects (one rare branch): the estimate sum only matters in the
-                    // batched modes; a batch closes when it reaches Delta_eval, crossing kernel included
                     const uint32_t sm = P.sync_mode;
-                    if (n == task_first) batch_start = task_first;
-                    const int64_t acc2 = (n == task_first ? 0 : acc) + est;
-                    const bool closes = sm >= S_BATCHED && acc2 >= P.delta_eval_ns;
-                    acc = (closes || last) ? 0 : acc2;
-                    int32_t target = (last || sm == S_EACH || (closes && sm == S_BATCHED)) ? (int32_t)launched : -1;
-                    if (closes && !last && sm == S_OVERLAP) {   // OVERLAP: wait for the previous batch
-                        const uint32_t prev = batch_start;
-                        batch_start = launched;
-                        if (prev != task_first) target = (int32_t)prev;   // first close: not issued
+                    int32_t target = -1;
+                    if (r17_sel) {
+                        // R17 with selects (one rare branch): the estimate sum only matters in the
+                        // batched modes; a batch closes when it reaches Delta_eval, crossing kernel included
+                        if (n == task_first) batch_start = task_first;
+                        const int64_t acc2 = (n == task_first ? 0 : acc) + est;
+                        const bool closes = sm >= S_BATCHED && acc2 >= P.delta_eval_ns;
+                        acc = (closes || last) ? 0 : acc2;
+                        target = (last || sm == S_EACH || (closes && sm == S_BATCHED)) ? (int32_t)launched : -1;
+                        if (closes && !last && sm == S_OVERLAP) {   // OVERLAP: wait for the previous batch
+                            const uint32_t prev = batch_start;
+                            batch_start = launched;
+                            if (prev != task_first) target = (int32_t)prev;   // first close: not issued
+                        }
+                    } else if (sm == S_ASYNC) {   // the other policies' benchmarks sync once per task
+                        if (last) target = (int32_t)launched;
+                    } else if (sm == S_EACH) {
+                        target = (int32_t)launched;
+                    } else {
+                        if (n == task_first) { acc = 0; batch_start = task_first; }
+                        acc += est;
+                        const bool closes = acc >= P.delta_eval_ns;
+                        if (closes || last) acc = 0;
+                        if (last || (closes && sm == S_BATCHED)) target = (int32_t)launched;
+                        else if (closes) {   // OVERLAP: wait for the previous batch
+                            const uint32_t prev = batch_start;
+                            batch_start = launched;
+                            if (prev != task_first) target = (int32_t)prev;   // first close: not issued
+                        }
                     }
                     if (target >= 0) {
                         sync_target = (uint32_t)target;
@@ -753,10 +803,6 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         // At scenario start no lane has an AKB entry.
         constexpr bool snap_late = urg && !coll && !EXT;
         uint32_t urgent_nx = 0, active_nx = 0;
-        // Core build: Phase C's fit ballot runs at every step and is itself the test, so no
-        // "new stream head" vote sits between Phase B and Phase C (a head that did not fit at an
-        // earlier Phase C still does not: `used` only falls at a retirement).
-        constexpr bool c_always = PK && !EXT && !CAL;   // measured: +1-2 % packed; the latency build ran 3x slower
         for (;;) {
             // A2: next event time.  Each lane keeps 32-bit distances dc / dh of its next CPU event
             // and kernel end from t_prev (exact below 2^31, lower bounds above), so the step is one

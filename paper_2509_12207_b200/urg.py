@@ -134,6 +134,18 @@ def batch_struct(b: Batch) -> BatchS:
                   b.fd_den, b.ftight_permille, b.tight_explicit, b.tight_mask)
 
 
+RECORD_WORDS_ = 8   # urg_outputs.records: 8 uint32 per (scenario, chain), include/urg.h
+
+
+def _current_device() -> int:
+    """The CUDA device urg_create_workload bound the workload to (cudaGetDevice at create)."""
+    try:
+        import torch
+        return torch.cuda.current_device()
+    except Exception:
+        return 0
+
+
 def _stream_handle(stream) -> Optional[int]:
     if stream is None:
         return None
@@ -172,6 +184,7 @@ class DeviceWorkload:
         h = ct.c_void_p()
         _check(lib().urg_create_workload(ct.byref(self.desc), ct.byref(h)))
         self.handle = h
+        self.device = _current_device()
         self.num_chains = w.num_chains
         self.agg_words = int(lib().urg_agg_words(h))
         self.template_bytes = int(lib().urg_template_bytes(h))
@@ -193,9 +206,24 @@ class DeviceWorkload:
     def __exit__(self, *a):
         self.close()
 
-    # -- device buffers (torch tensors on the current CUDA device) --
+    # -- device buffers (torch tensors on the workload's CUDA device) --
+    def _check_device_buffers(self, b: Batch, agg, records):
+        """The kernel writes 8 words per (scenario, chain) into records and int64 atomics into agg:
+        refuse buffers it would overrun or misread (wrong dtype, size, layout or device)."""
+        import torch
+        dev = torch.device("cuda", self.device)
+        if not (isinstance(agg, torch.Tensor) and agg.dtype == torch.int64 and agg.is_contiguous()
+                and agg.device == dev and agg.numel() == self.agg_words):
+            raise ValueError(f"agg must be a contiguous int64 tensor of {self.agg_words} words on {dev}")
+        if records is not None:
+            need = b.scenario_count * self.num_chains * RECORD_WORDS_
+            if not (isinstance(records, torch.Tensor) and records.dtype in (torch.int32, getattr(torch, "uint32", None))
+                    and records.is_contiguous() and records.device == dev and records.numel() >= need):
+                raise ValueError(f"records must be a contiguous 32-bit tensor of >= {need} words on {dev}")
+
     def simulate(self, p: Policy, b: Batch, agg, records=None, stream=None):
         """urg_simulate_batch: asynchronous on `stream`; adds into `agg` (int64 device tensor)."""
+        self._check_device_buffers(b, agg, records)
         o = OutputsS(None if records is None else records.data_ptr(), agg.data_ptr())
         _check(lib().urg_simulate_batch(self.handle, ct.byref(policy_struct(p)), ct.byref(batch_struct(b)),
                                         ct.byref(o), _stream_handle(stream)))
@@ -204,7 +232,14 @@ class DeviceWorkload:
     def simulate_host(self, p: Policy, b: Batch, agg: np.ndarray, records: Optional[np.ndarray] = None,
                       stream=None):
         """urg_simulate_batch_host: synchronous; agg (int64[agg_words]) is added into."""
-        assert agg.dtype == np.int64 and agg.flags.c_contiguous
+        if not (isinstance(agg, np.ndarray) and agg.dtype == np.int64 and agg.flags.c_contiguous
+                and agg.size == self.agg_words):
+            raise ValueError(f"agg must be a C-contiguous int64 array of {self.agg_words} words")
+        if records is not None:
+            need = b.scenario_count * self.num_chains * RECORD_WORDS_
+            if not (isinstance(records, np.ndarray) and records.dtype in (np.uint32, np.int32)
+                    and records.flags.c_contiguous and records.size >= need):
+                raise ValueError(f"records must be a C-contiguous 32-bit array of >= {need} words")
         o = OutputsS(None if records is None else records.ctypes.data, agg.ctypes.data)
         _check(lib().urg_simulate_batch_host(self.handle, ct.byref(policy_struct(p)), ct.byref(batch_struct(b)),
                                              ct.byref(o), _stream_handle(stream)))

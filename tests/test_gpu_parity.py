@@ -685,3 +685,29 @@ def test_copy_engine():
     w.cpu_cores = 2
     w.chains[0].tasks[0].frees = True
     both(w, cfg.policies["urgengo"], b, "paper11 copies + cores + free")
+
+
+def test_binding_rejects_bad_buffers():
+    """urg.py refuses buffers the kernel would overrun or misread: wrong dtype, size,
+    layout or device of agg / records, before any launch."""
+    import torch
+
+    from paper_2509_12207_b200.urg import DeviceWorkload
+    w, p = w1(), Policy(kind=FIFO, flags=0, sync_mode=SYNC_ASYNC)
+    b = Batch(horizon_ns=1 * MS, scenario_count=4)
+    with DeviceWorkload(w) as dw:
+        good = torch.zeros(dw.agg_words, dtype=torch.int64, device="cuda")
+        rec = torch.zeros((4, 2, 8), dtype=torch.int32, device="cuda")
+        for bad in (good.to(torch.int32), good[:-1], good.cpu(), torch.zeros(2 * dw.agg_words, dtype=torch.int64,
+                                                                             device="cuda")[::2]):
+            with pytest.raises(ValueError):
+                dw.simulate(p, b, bad, rec)
+        for bad in (rec[:3], rec.to(torch.int64), rec.cpu(), rec.transpose(0, 1)):
+            with pytest.raises(ValueError):
+                dw.simulate(p, b, good, bad)
+        dw.simulate(p, b, good, rec)
+        dw.check()
+        with pytest.raises(ValueError):
+            dw.simulate_host(p, b, np.zeros(dw.agg_words, np.int32))
+        with pytest.raises(ValueError):
+            dw.simulate_host(p, b, np.zeros(dw.agg_words, np.int64), np.zeros((3, 2, 8), np.uint32))
