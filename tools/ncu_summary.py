@@ -20,6 +20,7 @@ KEYS = ["Kernel Name", "dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__ti
         "l1tex__t_sector_hit_rate.pct", "launch__shared_mem_per_block_dynamic"]
 STALLS = "smsp__average_warps_issue_stalled_"
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+TUNIT = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}   # -> ms
 
 
 def summary(rep):
@@ -31,6 +32,11 @@ def summary(rep):
         if h in KEYS or (h.startswith(STALLS) and h.endswith("_per_issue_active.ratio")):
             res[h] = [v, u]
     return res
+
+
+def kernel_ms(res):
+    v, u = res["gpu__time_duration.sum"]
+    return float(v.replace(",", "")) * TUNIT.get(u, 1.0)
 
 
 def dram_bytes(res):
@@ -53,9 +59,10 @@ if __name__ == "__main__":
         root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
         tp = os.path.join(root, "profiles", "traffic.json")
         t = json.load(open(tp)) if os.path.exists(tp) else {}
-        t.setdefault(cfg, {})[pol] = dram_bytes(res)
-        t["_source"] = (f"{os.path.relpath(dst, root)}: dram__bytes_read.sum + dram__bytes_write.sum of one "
-                        f"urg_sim_kernel launch (ncu --set full), bench.py default workload")
+        t.setdefault(cfg, {})[pol] = {
+            "bytes_per_launch": dram_bytes(res), "kernel_ms": kernel_ms(res),
+            "source": f"{os.path.relpath(dst, root)}: dram__bytes_read.sum + dram__bytes_write.sum and "
+                      "gpu__time_duration.sum of one urg_sim_kernel launch of bench.py's step (ncu)"}
         with open(tp, "w") as f:
-            json.dump(t, f)
+            json.dump(t, f, indent=1)
         print("traffic", t[cfg][pol])
