@@ -215,6 +215,31 @@ urg_status urg_miss_ratios(const urg_workload *w, const int64_t *agg_host, doubl
 /* Thread-local description of the last error (empty string if none). */
 const char *urg_last_error(void);
 
+/* ---- debug and test hooks (not part of the simulation path) ---- */
+
+/* Record the event trace of global scenario `scenario` during the following simulate calls of
+ * this process into dev_buf (DEVICE int64: [0] = number of rows written, then cap_rows rows of
+ * (t, kind, lane, instance, a, b) -- the CPU oracle's trace schema and kind codes
+ * "time_ns, seq, kind, chain, instance, detail" with seq = row order per lane).  dev_buf = NULL
+ * turns it off.  Only the debug build (liburg_debug.so, compiled with -DURG_DEBUG) writes rows;
+ * it also checks the invariants of SPEC.md:171-174 on device (a kernel never starts before it is
+ * ready, capacity <= 1000 permille, a kernel retires exactly at its end, every kernel of a
+ * finished instance launched and completed once, record counts consistent, no event scheduled
+ * in the past, urgent tasks at level 0) and reports a violation through urg_check
+ * (URG_EINTERNAL, codes 17-23). */
+urg_status urg_debug_set_trace(int64_t *dev_buf, uint64_t cap_rows, uint64_t scenario);
+
+/* 1 in the debug build, 0 in the product build. */
+int urg_debug_build(void);
+
+/* Device Philox4x32-10 of n (ctr, key) pairs (DEVICE uint32 [n][4], [n][2], out [n][4]) --
+ * the known-answer test of the device RNG copy. */
+urg_status urg_debug_philox(const void *d_ctr, const void *d_key, void *d_out, int n, void *cuda_stream);
+
+/* Event-loop counters of the profiling build (liburg_stats.so, -DURG_STATS) since the last call:
+ * [single-chain steps, multi-chain steps, Phase C dispatches, 64-bit rebases]; zeros otherwise. */
+urg_status urg_debug_stats(const urg_workload *w, uint64_t *out4);
+
 #ifdef __cplusplus
 }
 #endif

@@ -20,6 +20,7 @@ HEADERS = [os.path.join(CSRC, f) for f in ("urg_layout.h", "urg_sim.cuh")] + \
           [os.path.join(os.path.dirname(HERE), "include", "urg.h")]
 OUT = os.path.join(HERE, "liburg.so")
 STATS_OUT = os.path.join(HERE, "liburg_stats.so")   # profiling variant (-DURG_STATS event-loop counters)
+DEBUG_OUT = os.path.join(HERE, "liburg_debug.so")   # debug variant (-DURG_DEBUG: device invariants, event trace)
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CFLAGS = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
@@ -62,10 +63,10 @@ def _compile_all(out: str, defines, verbose: bool) -> str:
     return out
 
 
-def build(force: bool = False, verbose: bool = False, stats: bool = False) -> str:
-    out = STATS_OUT if stats else OUT
+def build(force: bool = False, verbose: bool = False, stats: bool = False, debug: bool = False) -> str:
+    out = STATS_OUT if stats else DEBUG_OUT if debug else OUT
     if force or needs_build(out):
-        _compile_all(out, ["URG_STATS"] if stats else [], verbose)
+        _compile_all(out, ["URG_STATS"] if stats else ["URG_DEBUG"] if debug else [], verbose)
     return out
 
 

@@ -54,6 +54,9 @@ struct urg_workload {
 
 static thread_local std::string g_err;
 
+// debug-build event trace (urg_debug_set_trace; liburg_debug.so records, the product build ignores it)
+static struct { int64_t *buf; uint64_t cap, scenario; } g_trace = {nullptr, 0, 0};
+
 // cudaFuncSetAttribute (dynamic shared memory, carveout) is process-global per kernel function:
 // the attribute set of one launch and its <<<>>> stay together under this lock, so two host
 // threads launching the same instantiation with different geometries cannot interleave.
@@ -344,6 +347,7 @@ static void fill_params(const urg_workload *w, const urg_policy *p, const urg_ba
     P.horizon_ns = b->horizon_ns;
     P.fa_num = b->fa_num; P.fa_den = b->fa_den; P.fd_num = b->fd_num; P.fd_den = b->fd_den;
     P.ftight_permille = b->ftight_permille; P.tight_explicit = b->tight_explicit; P.tight_mask = b->tight_mask;
+    P.trace_buf = g_trace.buf; P.trace_cap = g_trace.cap; P.trace_scn = g_trace.scenario;
 }
 
 // Launch geometry: one warp per scenario in flight, persistent CTAs pulling scenarios
@@ -544,7 +548,15 @@ extern "C" urg_status urg_check(const urg_workload *w, void *cuda_stream, int64_
         CUDA_TRY(cudaMemsetAsync(w->d_err, 0, sizeof e2, s), "clearing the error word");
         CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
         return fail(URG_EINTERNAL, "device invariant %lld tripped in scenario %lld (%s)", e2[0], e2[1],
-                    e2[0] == 1 ? "time did not advance" : e2[0] == 2 ? "step iteration guard" : "debug-build invariant");
+                    e2[0] == 1 ? "time did not advance" : e2[0] == 2 ? "step iteration guard"
+                               : e2[0] == 17 ? "debug: kernel started before it was ready"
+                               : e2[0] == 18 ? "debug: GPU capacity exceeded"
+                               : e2[0] == 19 ? "debug: kernel retired at a time other than its end"
+                               : e2[0] == 20 ? "debug: instance completed with kernels not launched or not done"
+                               : e2[0] == 21 ? "debug: record counts inconsistent"
+                               : e2[0] == 22 ? "debug: event scheduled in the past"
+                               : e2[0] == 23 ? "debug: stream level out of range or urgent task not at level 0"
+                                             : "unknown");
     }
     return URG_OK;
 }
@@ -576,6 +588,26 @@ extern "C" urg_status urg_debug_stats(const urg_workload *w, uint64_t *out4)
     CUDA_TRY(cudaMemcpy(out4, w->d_work + 4, 32, cudaMemcpyDeviceToHost), "reading stats");
     CUDA_TRY(cudaMemset(w->d_work + 4, 0, 32), "clearing stats");
     return URG_OK;
+}
+
+// debug hook: record the event trace of global scenario `scenario` into dev_buf (DEVICE int64:
+// [0] row counter, then cap_rows rows of 6) during the following simulate calls of this process;
+// dev_buf = NULL turns it off.  Only the debug build (liburg_debug.so, -DURG_DEBUG) writes rows.
+extern "C" urg_status urg_debug_set_trace(int64_t *dev_buf, uint64_t cap_rows, uint64_t scenario)
+{
+    std::lock_guard<std::mutex> lk(g_launch_mu);
+    g_trace.buf = dev_buf; g_trace.cap = dev_buf ? cap_rows : 0; g_trace.scenario = scenario;
+    return URG_OK;
+}
+
+// 1 if this library is the debug build (device invariant asserts, event trace), else 0
+extern "C" int urg_debug_build(void)
+{
+#ifdef URG_DEBUG
+    return 1;
+#else
+    return 0;
+#endif
 }
 
 // test hook: device Philox on n (ctr, key) pairs in device memory (Philox KAT / oracle cross-check)

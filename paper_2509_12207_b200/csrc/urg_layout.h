@@ -79,4 +79,8 @@ struct UrgSimParams {
     int64_t cal_end;
     int64_t *cal_buf;
     uint64_t cal_cap;
+    // debug build only (-DURG_DEBUG, liburg_debug.so): event trace of one scenario, [0] = row
+    // counter, then rows (t, kind, chain, instance, a, b) in the oracle's trace schema
+    int64_t *trace_buf;
+    uint64_t trace_cap, trace_scn;
 };

@@ -36,7 +36,24 @@ enum { S_ASYNC = 0, S_EACH = 1, S_BATCHED = 2, S_OVERLAP = 3 };
 // per-task / per-instance states on the common path
 enum { PC_ENQUEUE = 0, PC_ATTEMPT, PC_CPU_DONE, PC_SYNC_RET, PC_FREE_RET, PC_ARRIVE, PC_TASK_START, PC_SYNC_WAIT,
        PC_FREE_WAIT, PC_WAIT_MSG, PC_DONE };
-enum { ERR_TIME = 1, ERR_GUARD = 2 };
+enum { ERR_TIME = 1, ERR_GUARD = 2, ERR_DEBUG = 16 };   // debug build: 16 + invariant id
+// debug-build event kinds (the oracle's trace codes, oracle/oracle.py TRACE_KINDS)
+enum { TR_STEP = 1, TR_INST_START, TR_TASK_START, TR_EVAL, TR_DELAY, TR_BIND, TR_ENQUEUE, TR_DISPATCH, TR_RETIRE,
+       TR_SYNC_CALL, TR_SYNC_RET, TR_FREE_CLOSE, TR_INST_DONE, TR_EARLY_EXIT, TR_COLLISION };
+// debug-build invariants (SPEC.md:171-174 and DESIGN.md R16-R21), checked on device
+enum { INV_START_BEFORE_READY = 1, INV_CAPACITY, INV_RETIRE_TIME, INV_CONSERVATION, INV_COUNTS, INV_PAST_EVENT,
+       INV_LEVEL };
+#ifdef URG_DEBUG
+#define URG_TR(t, kind, a, b) trace_row((t), (kind), (a), (b))
+#define URG_DASSERT(cond, id)                                                                                    \
+    do {                                                                                                         \
+        if (!(cond) && atomicCAS((unsigned long long *)err, 0ull, (unsigned long long)(ERR_DEBUG + (id))) == 0ull) \
+            err[1] = s;                                                                                          \
+    } while (0)
+#else
+#define URG_TR(t, kind, a, b) ((void)0)
+#define URG_DASSERT(cond, id) ((void)0)
+#endif
 
 // ---------------------------------------------------------------------------
 // Philox4x32-10 (Salmon et al., SC'11) -- device copy, KAT-tested (tests/test_gpu_*.py)
@@ -397,6 +414,17 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         uint64_t sum_rt = 0;
         uint32_t msg = 0;                      // R32: delivered, untaken message (instance + 1), 0 = none
         uint32_t expect = 0;                   // R32, last stage: next instance to record
+#ifdef URG_DEBUG
+        // one scenario's event trace, rows (t, kind, lane, instance, a, b) as the oracle writes them
+        auto trace_row = [&](int64_t t, int kind, int64_t a, int64_t b) {
+            if (!P.trace_buf || !valid || (uint64_t)s != P.trace_scn) return;
+            const unsigned long long i = atomicAdd((unsigned long long *)P.trace_buf, 1ull);
+            if (i >= P.trace_cap) return;
+            int64_t *r = P.trace_buf + 1 + 6 * i;
+            r[0] = t; r[1] = kind; r[2] = kind == TR_STEP ? -1 : (int64_t)c; r[3] = kind == TR_STEP ? -1 : (int64_t)inst;
+            r[4] = a; r[5] = b;
+        };
+#endif
 
         auto arrival = [&](uint32_t i) -> int64_t {
             int64_t jit = 0;
@@ -473,6 +501,8 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         //      step and by the single-lane ("solo") steps below ----
         // Phase A for a lane whose running kernel ends at t (R19)
         auto retire = [&](int64_t t) {
+            URG_DASSERT(head_end == t, INV_RETIRE_TIME);
+            URG_TR(t, TR_RETIRE, done, 0);
             ++done;
             head_end = INF64;
             dh = D_INF;
@@ -504,6 +534,8 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             head_util = head_copy ? 0u : head_u;   // a memcpy uses the copy engine, not the SMs (R31)
             head_end = t + (int64_t)d;
             dh = dsat((int64_t)d);
+            URG_DASSERT(t >= head_ready && launched > done, INV_START_BEFORE_READY);
+            URG_TR(t, TR_DISPATCH, done, head_end);
         };
         // Phase B: this lane's CPU program at t, until it has to wait for time to pass.
         // urgent_m / active_m / snapL are the round snapshot of the other chains (R14, R15).
@@ -522,6 +554,8 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                 bool next_inst = false;
                 bool task_done = false;
                 if (pc == PC_SYNC_RET) {   // sync returned: covered kernels leave the AKB
+                    URG_TR(t, TR_SYNC_RET, sync_target, 0);
+                    if (urg) URG_TR(t, TR_EVAL, laxity(t), launched);   // P:496 (the next attempt re-evaluates)
                     if (akb_on) akb = launched - sync_target;
                     if (launched < task_end) pc = PC_ATTEMPT;
                     else if (has_free && (T.task[tbase + task].flags & 1u)) {
@@ -544,6 +578,8 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     } else {   // instance complete (R18, R22)
                         expect = inst + 1u;
                         const int64_t rt = t - t_arr;
+                        URG_DASSERT(te || (done == launched && launched == CRF(num_kernels)), INV_CONSERVATION);
+                        URG_TR(t, TR_INST_DONE, rt, rt > Dp ? 1 : 0);
                         if (rt > Dp) ++n_miss;
                         sum_rt += (uint64_t)rt;
                         hash = (hash ^ (uint32_t)rt) * 16777619u;
@@ -555,6 +591,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     }
                 }
                 if (pc == PC_ARRIVE) {   // frame arrival / instance start (R6; R32: the thread's task)
+                    URG_TR(t, TR_INST_START, t_arr, 0);
                     if (!te) ++n_total;
                     Fg = inst_factor(rng_word(P.seed, s, URG_TAG_INST, cid, inst, 0), CRF(gpu_sigma_ppm));
                     Fc = inst_factor(rng_word(P.seed, s, URG_TAG_INST, cid, inst, 1), CRF(cpu_sigma_ppm));
@@ -581,13 +618,16 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                 }
                 if (pc == PC_TASK_START) {   // new CPU segment: evaluate, early exit
                     bool exited = false;
+                    URG_TR(t, TR_TASK_START, task, 0);
                     if (urg) {
                         if (noise)
                             nz = (int32_t)(rng_word(P.seed, s, URG_TAG_NOISE, cid, inst, task) %
                                            (2u * P.noise_pm + 1u)) - (int32_t)P.noise_pm;
                         const int64_t lax = laxity(t);   // Eq. 2 (R9)
                         L_last = lax;
+                        URG_TR(t, TR_EVAL, lax, launched);
                         if (f_early && lax < 0) {
+                            URG_TR(t, TR_EARLY_EXIT, 0, 0);
                             akb = 0;
                             ++n_early;
                             if (last_stage) {   // R32: an earlier task's exit is a gap the last task records
@@ -633,6 +673,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                         head_ready = t; head_u = kr.util_permille; head_nom = kr.nominal_ns; newhead = true;
                         if (has_copy) head_copy = kr.flags & 1u;
                     }
+                    URG_TR(t, TR_ENQUEUE, n, level);
                     ++launched; ++n_launch;
                     if (!WIDE && launched < CRF(num_kernels)) nxt = kern_rec(KR + launched);
                     rem_g -= est;
@@ -647,6 +688,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                             k += (snapLev[o] <= level && urgency_key(snapL[o]) < own) ? 1u : 0u;
                         }
                         if (k && !CAL) atomicAdd(&agg[(uint64_t)NC * stride + (k + 1 > 32 ? 32 : k + 1)], 1ull);
+                        if (k) URG_TR(t, TR_COLLISION, k + 1 > 32 ? 32 : k + 1, level);
                     }
                     const bool last = launched == task_end;
                     if (last) rem_c -= ma ? ma_pred[task] : T.task[tbase + task].cpu_estimate_ns;
@@ -664,6 +706,9 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                             const uint32_t prev = batch_start;
                             batch_start = launched;
                             if (prev != task_first) target = (int32_t)prev;   // first close: not issued
+#ifdef URG_DEBUG
+                            else { URG_TR(t, TR_FREE_CLOSE, launched, 0); if (urg) URG_TR(t, TR_EVAL, laxity(t), launched); }
+#endif
                         }
                     } else if (sm == S_ASYNC) {   // the other policies' benchmarks sync once per task
                         if (last) target = (int32_t)launched;
@@ -679,6 +724,9 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                             const uint32_t prev = batch_start;
                             batch_start = launched;
                             if (prev != task_first) target = (int32_t)prev;   // first close: not issued
+#ifdef URG_DEBUG
+                            else { URG_TR(t, TR_FREE_CLOSE, launched, 0); if (urg) URG_TR(t, TR_EVAL, laxity(t), launched); }
+#endif
                         }
                     }
                     if (target >= 0) {
@@ -688,6 +736,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                             sync_cost += (int64_t)(rng_word(P.seed, s, URG_TAG_SYNC, cid, inst, sync_ord) %
                                                    (uint32_t)(P.sync_hi_ns - P.sync_lo_ns + 1));
                         ++sync_ord;
+                        URG_TR(t, TR_SYNC_CALL, sync_target, sync_cost);
                         if (done >= sync_target) {
                             pc = PC_SYNC_RET;
                             cpu_busy(t, sync_cost);
@@ -702,10 +751,11 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                 }
                 if (pc == PC_CPU_DONE || pc == PC_ATTEMPT) {   // launch attempt for kernel n = launched (R14-R16)
                     int64_t lax = 0;
-                    if (urg) { lax = laxity(t); L_last = lax; }
+                    if (urg) { lax = laxity(t); L_last = lax; URG_TR(t, TR_EVAL, lax, launched); }
                     const bool own_urgent = lax >= 0 && lax <= P.lax_threshold_ns;
                     if (f_delay && !own_urgent && (urgent_m & ~(1u << lane)) &&
                         (WIDE ? kern_rec(KR + launched) : nxt).util_permille >= P.util_exempt) {
+                        URG_TR(t, TR_DELAY, launched, 0);
                         pc = PC_ATTEMPT;
                         cpu_next = t + P.sleep_ns;
                         dc = dsat(P.sleep_ns);
@@ -744,6 +794,8 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                                     : n_r <= 1      ? 1 + (P.num_prio - 2) / 2
                                                     : 1 + (uint32_t)(((uint64_t)(r - 1) * (P.num_prio - 2)) / (n_r - 1));
                         }
+                        URG_DASSERT(level < P.num_prio && (!f_bind || !own_urgent || level == 0), INV_LEVEL);
+                        URG_TR(t, TR_BIND, level, launched);
                     }
                     pc = PC_ENQUEUE;
                     cpu_busy(t, busy_launch);
@@ -884,6 +936,9 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             if (!fin) {
                 t_prev = t;
                 if (lane == hbase) ++my_steps;   // one loop step of this half's scenario
+#ifdef URG_DEBUG
+                if (lane == hbase) trace_row(t, TR_STEP, 0, 0);
+#endif
             }
 
             // Phase A: retire (R21, R19)
@@ -910,6 +965,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                 if (!snap_late && (urg || cls)) snapshot(te || (due && can_bind()), urgent_m, active_m, busy_m);
                 bool nh = false;
                 if (due) nh = phase_b(t, urgent_m, active_m, busy_m);
+                URG_DASSERT(!due || cpu_next > t, INV_PAST_EVENT);
                 if (snap_late) {   // the next phase's snapshot: this lane's L_last and the two masks
                     if (f_bind) {
                         __syncwarp();   // this phase's reads of the snapshot are done
@@ -1016,6 +1072,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     const uint32_t uw = __shfl_sync(FULL, head_u, wl >= 0 ? wl : lane);
                     if (lane == wl) { start_head(t, used); waiting = false; }
                     if (wl >= 0) used += uw;
+                    URG_DASSERT(used <= 1000u, INV_CAPACITY);
                     if (!any_multi) break;   // each half started its only fitting head (others did not fit)
                 }
             } else if (!PK && (c_always || dirty)) {
@@ -1047,6 +1104,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     }
                     const uint32_t u_run = used;
                     used += __shfl_sync(FULL, head_u, wl);
+                    URG_DASSERT(used <= 1000u, INV_CAPACITY);
                     if (lane == wl) { start_head(t, u_run); waiting = false; }
                     if ((fit & (fit - 1)) == 0) break;   // the others did not fit before; `used` only grew
                 }
@@ -1079,6 +1137,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     for (uint32_t i = first_unstarted; arrival(i) < H; ++i) { ++n_unfin; ++n_total; }
             }
             n_miss += n_unfin;
+            URG_DASSERT(n_miss <= n_total && n_early + n_unfin <= n_miss, INV_COUNTS);
             if (records) {
                 uint4 *r = (uint4 *)(records + ((uint64_t)jw * NC + cid) * 8);
                 r[0] = make_uint4(n_total, n_miss, n_early, n_unfin);

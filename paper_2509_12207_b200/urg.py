@@ -75,7 +75,9 @@ SYMBOLS = ["urg_create_workload", "urg_destroy_workload", "urg_agg_words", "urg_
            "urg_simulate_batch_host", "urg_check", "urg_miss_ratios", "urg_last_error",
            "urg_calibration_words", "urg_calibrate"]
 
+DEBUG_LIB_PATH = os.path.join(_HERE, "liburg_debug.so")
 _lib = None
+_lib_debug = None
 
 
 def lib():
@@ -83,10 +85,25 @@ def lib():
     global _lib
     if _lib is None:
         # URG_LIB selects another build of the same library (liburg_stats.so, the profiling variant)
-        path = os.environ.get("URG_LIB") or LIB_PATH
-        if not os.path.exists(path):
-            raise RuntimeError(f"{path} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
-                               "(the CUDA path has no CPU fallback)")
+        _lib = _load(os.environ.get("URG_LIB") or LIB_PATH)
+    return _lib
+
+
+def lib_debug():
+    """Load liburg_debug.so: the same kernels compiled with -DURG_DEBUG (device invariant checks and
+    the one-scenario event trace).  A separate handle beside liburg.so; tests only."""
+    global _lib_debug
+    if _lib_debug is None:
+        _lib_debug = _load(DEBUG_LIB_PATH)
+        assert _lib_debug.urg_debug_build() == 1, "liburg_debug.so is not the debug build"
+    return _lib_debug
+
+
+def _load(path):
+    if not os.path.exists(path):
+        raise RuntimeError(f"{path} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                           "(the CUDA path has no CPU fallback)")
+    if True:
         L = ct.CDLL(path)
         L.urg_create_workload.restype = ct.c_int
         L.urg_create_workload.argtypes = [ct.POINTER(WorkloadDesc), ct.POINTER(ct.c_void_p)]
@@ -115,13 +132,16 @@ def lib():
             L.urg_debug_stats.argtypes = [ct.c_void_p, ct.c_void_p]
         L.urg_debug_philox.restype = ct.c_int
         L.urg_debug_philox.argtypes = [ct.c_void_p, ct.c_void_p, ct.c_void_p, ct.c_int, ct.c_void_p]
-        _lib = L
-    return _lib
+        L.urg_debug_set_trace.restype = ct.c_int
+        L.urg_debug_set_trace.argtypes = [ct.c_void_p, ct.c_uint64, ct.c_uint64]
+        L.urg_debug_build.restype = ct.c_int
+        L.urg_debug_build.argtypes = []
+    return L
 
 
-def _check(status: int):
+def _check(status: int, L=None):
     if status != URG_OK:
-        raise UrgError(status, lib().urg_last_error().decode())
+        raise UrgError(status, (L or lib()).urg_last_error().decode())
 
 
 def policy_struct(p: Policy) -> PolicyS:
@@ -155,8 +175,10 @@ def _stream_handle(stream) -> Optional[int]:
 class DeviceWorkload:
     """urg_workload handle: the template resident in HBM (urg_create_workload)."""
 
-    def __init__(self, w: Workload):
+    def __init__(self, w: Workload, debug: bool = False):
+        """debug=True: the workload lives in liburg_debug.so (device invariant checks, event trace)."""
         self.spec = w
+        self.L = lib_debug() if debug else lib()
         keep = []
         chains = (ChainDesc * w.num_chains)()
         for ci, ch in enumerate(w.chains):
@@ -182,16 +204,19 @@ class DeviceWorkload:
                                  None if var is None else var.ctypes.data)
         self._keep = (keep, chains, inst, kern, var)
         h = ct.c_void_p()
-        _check(lib().urg_create_workload(ct.byref(self.desc), ct.byref(h)))
+        self._chk(self.L.urg_create_workload(ct.byref(self.desc), ct.byref(h)))
         self.handle = h
         self.device = _current_device()
         self.num_chains = w.num_chains
-        self.agg_words = int(lib().urg_agg_words(h))
-        self.template_bytes = int(lib().urg_template_bytes(h))
+        self.agg_words = int(self.L.urg_agg_words(h))
+        self.template_bytes = int(self.L.urg_template_bytes(h))
+
+    def _chk(self, status):
+        _check(status, self.L)
 
     def close(self):
         if getattr(self, "handle", None):
-            lib().urg_destroy_workload(self.handle)
+            self.L.urg_destroy_workload(self.handle)
             self.handle = None
 
     def __del__(self):
@@ -225,7 +250,7 @@ class DeviceWorkload:
         """urg_simulate_batch: asynchronous on `stream`; adds into `agg` (int64 device tensor)."""
         self._check_device_buffers(b, agg, records)
         o = OutputsS(None if records is None else records.data_ptr(), agg.data_ptr())
-        _check(lib().urg_simulate_batch(self.handle, ct.byref(policy_struct(p)), ct.byref(batch_struct(b)),
+        self._chk(self.L.urg_simulate_batch(self.handle, ct.byref(policy_struct(p)), ct.byref(batch_struct(b)),
                                         ct.byref(o), _stream_handle(stream)))
 
     # -- host buffers (numpy) --
@@ -241,7 +266,7 @@ class DeviceWorkload:
                     and records.flags.c_contiguous and records.size >= need):
                 raise ValueError(f"records must be a C-contiguous 32-bit array of >= {need} words")
         o = OutputsS(None if records is None else records.ctypes.data, agg.ctypes.data)
-        _check(lib().urg_simulate_batch_host(self.handle, ct.byref(policy_struct(p)), ct.byref(batch_struct(b)),
+        self._chk(self.L.urg_simulate_batch_host(self.handle, ct.byref(policy_struct(p)), ct.byref(batch_struct(b)),
                                              ct.byref(o), _stream_handle(stream)))
 
     def calibrate(self, p: Policy, b: Batch, window_ns: int = 30_000_000_000, stream=None):
@@ -249,10 +274,10 @@ class DeviceWorkload:
         Returns (L_th, number of samples, per-scenario sample lists)."""
         import torch
         bs = batch_struct(b)
-        words = int(lib().urg_calibration_words(self.handle, ct.byref(bs), window_ns))
+        words = int(self.L.urg_calibration_words(self.handle, ct.byref(bs), window_ns))
         scratch = torch.zeros(words, dtype=torch.int64, device="cuda")
         res = torch.zeros(2, dtype=torch.int64, device="cuda")
-        _check(lib().urg_calibrate(self.handle, ct.byref(policy_struct(p)), ct.byref(bs), window_ns,
+        self._chk(self.L.urg_calibrate(self.handle, ct.byref(policy_struct(p)), ct.byref(bs), window_ns,
                                    scratch.data_ptr(), words, res.data_ptr(), _stream_handle(stream)))
         self.check(stream)
         r = res.cpu().numpy()
@@ -262,15 +287,36 @@ class DeviceWorkload:
         rows = [sc[cnt + j * cap: cnt + j * cap + int(sc[j])] for j in range(cnt)]
         return int(r[0]), int(r[1]), rows
 
+    def trace(self, p: Policy, b: Batch, scenario: int, cap_rows: int = 1 << 20, stream=None):
+        """Debug build only: simulate batch b and return the event trace of global scenario
+        `scenario` as int64 rows (t, kind, lane, instance, a, b) (urg_debug_set_trace), with the
+        batch's aggregates.  Rows of one lane are in its program order; lanes interleave."""
+        import torch
+        if self.L.urg_debug_build() != 1:
+            raise RuntimeError("event traces need the debug build: DeviceWorkload(w, debug=True)")
+        buf = torch.zeros(1 + 6 * cap_rows, dtype=torch.int64, device="cuda")
+        agg = torch.zeros(self.agg_words, dtype=torch.int64, device="cuda")
+        self._chk(self.L.urg_debug_set_trace(buf.data_ptr(), cap_rows, scenario))
+        try:
+            self.simulate(p, b, agg, None, stream=stream)
+            self.check(stream)
+        finally:
+            self._chk(self.L.urg_debug_set_trace(None, 0, 0))
+        h = buf.cpu().numpy()
+        n = int(h[0])
+        if n > cap_rows:
+            raise RuntimeError(f"trace overflow: {n} rows > cap {cap_rows}")
+        return h[1: 1 + 6 * n].reshape(n, 6).copy(), agg.cpu().numpy()
+
     def check(self, stream=None) -> None:
         s = ct.c_int64(0)
-        _check(lib().urg_check(self.handle, _stream_handle(stream), ct.byref(s)))
+        self._chk(self.L.urg_check(self.handle, _stream_handle(stream), ct.byref(s)))
 
     def miss_ratios(self, agg_host: np.ndarray):
         per = np.zeros(self.num_chains, np.float64)
         ov = ct.c_double(0.0)
         a = np.ascontiguousarray(agg_host, np.int64)
-        _check(lib().urg_miss_ratios(self.handle, a.ctypes.data, per.ctypes.data, ct.byref(ov)))
+        self._chk(self.L.urg_miss_ratios(self.handle, a.ctypes.data, per.ctypes.data, ct.byref(ov)))
         return per, ov.value
 
 
