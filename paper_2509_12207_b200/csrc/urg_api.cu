@@ -410,13 +410,7 @@ static urg_status prepare_launch(const urg_workload *w, const urg_policy *p, con
     if (!fn) return fail(URG_EINTERNAL, "no kernel instantiation for kind %u flags %u", p->kind, p->flags);
     P.blob_bytes = (uint32_t)w->blob.size();
     P.mbar_offset = align16(P.blob_bytes);
-    P.hist_offset = align16(P.mbar_offset + 16);
-    // A10/A12: the response-time histogram in shared memory (one global flush per CTA) when it fits
-    // beside the template: core builds, num_chains x rt_bins x 8 B <= 96 KB (paper11: 88 KB)
-    const uint64_t hb = (uint64_t)w->num_chains * w->rt_bins * 8u;
-    P.hist_bytes = (!ext && !cal && hb <= 96u * 1024u) ? (uint32_t)hb : 0u;
-    if (const char *eh = getenv("URG_SMEM_HIST")) if (atoi(eh) == 0) P.hist_bytes = 0;   // test hook
-    P.snap_offset = align16(P.hist_offset + P.hist_bytes);
+    P.snap_offset = align16(P.mbar_offset + 16);
     uint32_t per_lane = URG_SNAP_BYTES_PER_LANE;
     if (p->kind >= URG_URGENGO && P.ma_w) {   // UrgenGo and the R27 policies estimate remaining work
         P.ma_max_tasks = w->max_tasks;

@@ -68,9 +68,6 @@ struct UrgSimParams {
     uint32_t nk_total, num_variants;
     // staging
     uint32_t blob_bytes, snap_offset, mbar_offset, smem_bytes;
-    // per-CTA response-time histogram in shared memory (A10/A12: [num_chains][rt_bins] u64, flushed
-    // to agg once per CTA), 0 = the kernel adds to agg directly
-    uint32_t hist_offset, hist_bytes;
     // estimation noise (R25) and CPU moving-average predictor (R26)
     uint32_t noise_pm, ma_w, ma_max_tasks, ma_slot, ma_offset;
     // cudaFree barriers (R28), CPU cores (R29)

@@ -229,12 +229,6 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
     T.kern_q = hdr->off_kern_q ? (const uint32_t *)(sm + hdr->off_kern_q) : nullptr;
     const uint32_t C = P.num_lanes;    // threads: chains, or tasks under per-task executors (R32)
     const uint32_t NC = P.num_chains;  // chains: records and aggregates
-    // A10: the CTA's response-time histogram [NC][rt_bins] in shared memory (flushed at the end)
-    unsigned long long *hist = P.hist_bytes ? (unsigned long long *)(sm + P.hist_offset) : nullptr;
-    if (hist) {
-        for (uint32_t i = threadIdx.x; i < NC * P.rt_bins; i += blockDim.x) hist[i] = 0ull;
-        __syncthreads();
-    }
 
     // per-warp Phase B snapshot (R21): last laxity of each lane, then its stream level
     // per-warp Phase B snapshot (R21), 1 KB: last laxity, two policy keys, stream level
@@ -592,10 +586,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                         hash = (hash ^ (uint32_t)((uint64_t)rt >> 32)) * 16777619u;
                         int64_t bin = rt / P.rt_bin_ns;
                         if (bin > (int64_t)P.rt_bins - 1) bin = P.rt_bins - 1;
-                        if (!CAL) {
-                            if (hist) atomicAdd(&hist[cid * P.rt_bins + (uint32_t)bin], 1ull);
-                            else atomicAdd(&agg[(uint64_t)cid * stride + 5 + bin], 1ull);
-                        }
+                        if (!CAL) atomicAdd(&agg[(uint64_t)cid * stride + 5 + bin], 1ull);
                         next_inst = true;
                     }
                 }
@@ -1162,13 +1153,6 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             if (n_total) atomicAdd(&a[5 + P.rt_bins + (uint64_t)100 * n_miss / n_total], 1ull);
         }
         my_launches += __reduce_add_sync(FULL, n_launch);
-    }
-    if (hist) {   // A12: the CTA's histogram, one global add per non-empty bin
-        __syncthreads();
-        for (uint32_t i = threadIdx.x; i < NC * P.rt_bins; i += blockDim.x) {
-            const unsigned long long v = hist[i];
-            if (v) atomicAdd(&agg[(uint64_t)(i / P.rt_bins) * stride + 5 + i % P.rt_bins], v);
-        }
     }
     if (PK) my_steps += __shfl_sync(FULL, my_steps, 16);   // the upper half's steps
     if (lane == 0) {
