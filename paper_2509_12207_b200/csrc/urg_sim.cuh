@@ -404,7 +404,9 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         int64_t head_end = INF64;              // end of the running kernel, INF64 when the stream runs nothing
         int64_t head_ready = 0;                // time the waiting head became head (R20 key)
         uint32_t head_util = 0;                // util of the running kernel
-        uint32_t head_u = 0xFFFFu;             // util of the waiting head (valid while one waits)
+        uint32_t head_u = 0xFFFFu;             // util of the waiting head; 0xFFFF while none waits (no head,
+                                               // the head runs, or the half's scenario ended), so the
+                                               // Phase C fit test alone excludes such a lane
         uint32_t head_nom = 0;                 // its nominal duration (read with the record)
         UrgKernRec nxt = {};                   // latency build: record of the next kernel to launch (kernel
                                                // `launched`), loaded one launch ahead (off the critical path;
@@ -506,6 +508,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             ++done;
             head_end = INF64;
             dh = D_INF;
+            head_u = 0xFFFFu;
             if (launched > done) {
                 head_ready = t;
                 const UrgKernRec kr = kern_rec(KR + done);
@@ -532,6 +535,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             d = d < 1 ? 1 : (d > 0xFFFFFFFFull ? 0xFFFFFFFFull : d);
             if (contend && !head_copy) d += d * (uint64_t)P.alpha_pm * u_run / 1000000ull;   // R30
             head_util = head_copy ? 0u : head_u;   // a memcpy uses the copy engine, not the SMs (R31)
+            head_u = 0xFFFFu;                       // no waiting head now
             head_end = t + (int64_t)d;
             dh = dsat((int64_t)d);
             URG_DASSERT(t >= head_ready && launched > done, INV_START_BEFORE_READY);
@@ -884,6 +888,14 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                             break;
                         }
                     }
+                    if (PK) {   // each half ends on its own (only here: a fast step cannot end one)
+                        if (bad && lane == hbase &&
+                            atomicCAS((unsigned long long *)err, 0ull, (unsigned long long)ERR_TIME) == 0ull)
+                            err[1] = s;
+                        fin = fin || t > H_stop || bad;
+                        if (fin) head_u = 0xFFFFu;   // an ended half dispatches nothing
+                        if (__all_sync(FULL, fin)) break;
+                    }
                 } else {
                     dc -= m;
                     dh -= m;
@@ -919,11 +931,12 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                 }
             }
             if (CAL && cal_next >= P.cal_end) break;   // no sample left to take
-            if (PK) {   // each half ends on its own; the warp goes on while one half runs
+            if (PK && URG_DIST_OFF) {   // each half ends on its own; the warp goes on while one half runs
                 if (bad && lane == hbase &&
                     atomicCAS((unsigned long long *)err, 0ull, (unsigned long long)ERR_TIME) == 0ull)
                     err[1] = s;
                 fin = fin || t > H_stop || bad;
+                if (fin) head_u = 0xFFFFu;
                 if (__all_sync(FULL, fin)) break;
             } else if (CAL) {
                 if (t > H_stop) break;
@@ -1052,10 +1065,10 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             // The greedy scan in key order starts, each time, the smallest-key head that
             // fits the capacity left (heads that do not fit stay unfit as `used` grows).
             if (PK && (c_always || __any_sync(FULL, dirty))) {
-                // both halves: a half that is not dirty has no head that fits (fit = 0)
-                bool waiting = !fin && launched > done && head_end == INF64;
+                // both halves: a half that is not dirty has no head that fits (fit = 0); a lane with no
+                // waiting head has head_u = 0xFFFF, which never fits
                 for (;;) {
-                    const uint32_t fitw = __ballot_sync(FULL, waiting && used + head_u <= 1000u);
+                    const uint32_t fitw = __ballot_sync(FULL, used + head_u <= 1000u);
                     if (!fitw) break;
                     const uint32_t fit = fitw & hmask;
                     const bool multi = (fit & (fit - 1)) != 0u;
@@ -1070,7 +1083,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                         if (fit) wl = (int)(ml & 31u);
                     }
                     const uint32_t uw = __shfl_sync(FULL, head_u, wl >= 0 ? wl : lane);
-                    if (lane == wl) { start_head(t, used); waiting = false; }
+                    if (lane == wl) start_head(t, used);
                     if (wl >= 0) used += uw;
                     URG_DASSERT(used <= 1000u, INV_CAPACITY);
                     if (!any_multi) break;   // each half started its only fitting head (others did not fit)
@@ -1079,15 +1092,15 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
 #ifdef URG_STATS
                 ++st_dispatch;
 #endif
-                bool waiting = launched > done && head_end == INF64;
+                bool waiting = true;   // head_u = 0xFFFF (never fits) unless a head waits
                 if (has_copy) {   // R31: the copy engine runs one memcpy at a time, (ready, chain) first
-                    const bool cw = waiting && head_copy;
+                    const bool cw = head_u != 0xFFFFu && head_copy;
                     if (__any_sync(FULL, cw) && !__any_sync(FULL, head_end != INF64 && head_copy)) {
                         const int64_t mr = warp_min_nonneg(cw ? head_ready : INF64);
                         const int wl = __ffs(__ballot_sync(FULL, cw && head_ready == mr)) - 1;
                         if (lane == wl) start_head(t, used);
                     }
-                    waiting = waiting && !head_copy;   // memcpys never take compute capacity
+                    waiting = !head_copy;   // memcpys never take compute capacity
                 }
                 for (;;) {
                     const uint32_t fit = __ballot_sync(FULL, waiting && used + head_u <= 1000u);
@@ -1105,7 +1118,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     const uint32_t u_run = used;
                     used += __shfl_sync(FULL, head_u, wl);
                     URG_DASSERT(used <= 1000u, INV_CAPACITY);
-                    if (lane == wl) { start_head(t, u_run); waiting = false; }
+                    if (lane == wl) start_head(t, u_run);
                     if ((fit & (fit - 1)) == 0) break;   // the others did not fit before; `used` only grew
                 }
             }
