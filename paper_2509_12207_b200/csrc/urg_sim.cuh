@@ -238,6 +238,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
     uint32_t *mbox = (uint32_t *)(snapL + 112);   // R32: message published to each lane this round
     UrgVarRec *myvar = (UrgVarRec *)(snapL + 128);  // R33: each lane's variant estimate totals
     uint4 *kqw = (uint4 *)(snapL + 192);            // R4: the lane's current block of four KERN words
+    uint4 *syw = (uint4 *)(snapL + 256);            // R5: the lane's current block of four SYNC words
     constexpr bool urg = KIND == K_URGENGO;
     constexpr bool cls = KIND >= K_EDF;        // classical policies (R27): AKB-tracking, no urgency
     constexpr bool akb_on = urg || cls;
@@ -597,8 +598,11 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                 if (pc == PC_ARRIVE) {   // frame arrival / instance start (R6; R32: the thread's task)
                     URG_TR(t, TR_INST_START, t_arr, 0);
                     if (!te) ++n_total;
-                    Fg = inst_factor(rng_word(P.seed, s, URG_TAG_INST, cid, inst, 0), CRF(gpu_sigma_ppm));
-                    Fc = inst_factor(rng_word(P.seed, s, URG_TAG_INST, cid, inst, 1), CRF(cpu_sigma_ppm));
+                    if (T.inst_q) {   // words 0 (GPU) and 1 (CPU) of one Philox block (R4)
+                        const uint4 w = rng_block(P.seed, s, URG_TAG_INST, cid, inst, 0);
+                        Fg = inst_factor(w.x, CRF(gpu_sigma_ppm));
+                        Fc = inst_factor(w.y, CRF(cpu_sigma_ppm));
+                    }
                     task = stage; launched = k_first; done = k_first; sync_ord = stage << 16;
                     if (!WIDE) nxt = kern_rec(KR + k_first);
                     rem_g = myvar[lane].gpu_est_total; rem_c = CRF(cpu_est_total);
@@ -736,9 +740,13 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     if (target >= 0) {
                         sync_target = (uint32_t)target;
                         sync_cost = P.sync_lo_ns;
-                        if (P.sync_hi_ns > P.sync_lo_ns)
-                            sync_cost += (int64_t)(rng_word(P.seed, s, URG_TAG_SYNC, cid, inst, sync_ord) %
+                        if (P.sync_hi_ns > P.sync_lo_ns) {
+                            // the sync ordinals of an instance are drawn in order from (stage << 16), a
+                            // multiple of 4: one Philox block serves four consecutive sync calls
+                            if ((sync_ord & 3u) == 0u) syw[lane] = rng_block(P.seed, s, URG_TAG_SYNC, cid, inst, sync_ord);
+                            sync_cost += (int64_t)(((const uint32_t *)&syw[lane])[sync_ord & 3u] %
                                                    (uint32_t)(P.sync_hi_ns - P.sync_lo_ns + 1));
+                        }
                         ++sync_ord;
                         URG_TR(t, TR_SYNC_CALL, sync_target, sync_cost);
                         if (done >= sync_target) {
