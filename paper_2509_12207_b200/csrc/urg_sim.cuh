@@ -408,7 +408,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         uint32_t head_u = 0xFFFFu;             // util of the waiting head; 0xFFFF while none waits (no head,
                                                // the head runs, or the half's scenario ended), so the
                                                // Phase C fit test alone excludes such a lane
-        uint32_t head_nom = 0;                 // its nominal duration (read with the record)
+        uint32_t head_dur = 0;                 // its actual duration (R4), drawn when it becomes head
         UrgKernRec nxt = {};                   // latency build: record of the next kernel to launch (kernel
                                                // `launched`), loaded one launch ahead (off the critical path;
                                                // the throughput builds reload it: registers)
@@ -502,6 +502,24 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
 
         // ---- lane-local pieces of a loop step (R21); used by the warp-wide
         //      step and by the single-lane ("solo") steps below ----
+        // R4: the actual duration of kernel `done` (the stream head) from its nominal duration -- drawn
+        // when the kernel becomes head (kernels become head in stream order), kept until it starts
+        auto head_duration = [&](uint32_t nom) -> uint32_t {
+            uint64_t G = 65536u;
+#ifdef URG_NO_KQCACHE
+            if (KQ) G = T.kern_q[rng_word(P.seed, s, URG_TAG_KERN, cid, inst, done) >> 20];
+#else
+            if (KQ) {
+                // kernel `done` follows `done` - 1 of the same instance, so the four words of a Philox
+                // block are drawn once and kept in the lane's shared-memory slot; a new block (or the
+                // instance's first kernel) refills it
+                if ((done & 3u) == 0u || done == k_first) kqw[lane] = rng_block(P.seed, s, URG_TAG_KERN, cid, inst, done);
+                G = T.kern_q[((const uint32_t *)&kqw[lane])[done & 3u] >> 20];
+            }
+#endif
+            const uint64_t d = ((((uint64_t)nom * Fg) >> 16) * G) >> 16;
+            return d < 1 ? 1u : (d > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)d);
+        };
         // Phase A for a lane whose running kernel ends at t (R19)
         auto retire = [&](int64_t t) {
             URG_DASSERT(head_end == t, INV_RETIRE_TIME);
@@ -513,27 +531,14 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             if (launched > done) {
                 head_ready = t;
                 const UrgKernRec kr = kern_rec(KR + done);
-                head_u = kr.util_permille; head_nom = kr.nominal_ns;
+                head_u = kr.util_permille; head_dur = head_duration(kr.nominal_ns);
                 if (has_copy) head_copy = kr.flags & 1u;
             }
             if (pc == PC_SYNC_WAIT && done >= sync_target) { pc = PC_SYNC_RET; cpu_busy(t, sync_cost); }
         };
         // Phase C start of this lane's waiting head: non-preemptive, exact duration (R4, R19, R20)
         auto start_head = [&](int64_t t, uint32_t u_run) {
-            uint64_t G = 65536u;
-#ifdef URG_NO_KQCACHE
-            if (KQ) G = T.kern_q[rng_word(P.seed, s, URG_TAG_KERN, cid, inst, done) >> 20];
-#else
-            if (KQ) {
-                // A lane starts its kernels in stream order: kernel `done` follows `done` - 1 of the
-                // same instance, so the four words of a Philox block are drawn once and kept in the
-                // lane's shared-memory slot; a new block (or the instance's first kernel) refills it.
-                if ((done & 3u) == 0u || done == k_first) kqw[lane] = rng_block(P.seed, s, URG_TAG_KERN, cid, inst, done);
-                G = T.kern_q[((const uint32_t *)&kqw[lane])[done & 3u] >> 20];
-            }
-#endif
-            uint64_t d = ((((uint64_t)head_nom * Fg) >> 16) * G) >> 16;
-            d = d < 1 ? 1 : (d > 0xFFFFFFFFull ? 0xFFFFFFFFull : d);
+            uint64_t d = head_dur;
             if (contend && !head_copy) d += d * (uint64_t)P.alpha_pm * u_run / 1000000ull;   // R30
             head_util = head_copy ? 0u : head_u;   // a memcpy uses the copy engine, not the SMs (R31)
             head_u = 0xFFFFu;                       // no waiting head now
@@ -678,7 +683,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     const UrgKernRec kr = WIDE ? kern_rec(KR + n) : nxt;
                     const int64_t est = kr.estimate_ns;
                     if (launched == done) {   // stream was empty: head now
-                        head_ready = t; head_u = kr.util_permille; head_nom = kr.nominal_ns; newhead = true;
+                        head_ready = t; head_u = kr.util_permille; head_dur = head_duration(kr.nominal_ns); newhead = true;
                         if (has_copy) head_copy = kr.flags & 1u;
                     }
                     URG_TR(t, TR_ENQUEUE, n, level);
@@ -861,6 +866,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         int64_t cal_next = 0;                   // CAL: next sampling time
         uint32_t cal_n = 0;                     // CAL: samples of this scenario
         bool fin = false;                       // PK: this half's scenario has ended
+        uint32_t nsteps = 0;                    // PK: loop steps since the last rare-path step
         // Core UrgenGo build: the Phase B snapshot (R21) is taken where it changes -- at the
         // end of the previous Phase B, beside that phase's new-head vote -- instead of on the
         // next phase's critical path (Phase A and Phase C touch neither the AKB nor L_last).
@@ -878,7 +884,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             bool bad = false;   // time did not advance (invariant)
             if constexpr (!URG_DIST_OFF) {   // (the 64-bit head below is kept for A/B: -DURG_NO_DIST)
                 const uint32_t m = hmin(fin ? D_INF : (dc < dh ? dc : dh));
-                t = t_prev + (int64_t)m;
+                t = (int64_t)((uint64_t)t_prev + m);   // (an ended half's t_prev may be INF64: wraps, unused)
                 const bool slow = !fin && ((m - 1u) >= D_SLOW - 1u || adv + m >= D_SLOW || t > H_stop);
                 if (PK ? __any_sync(FULL, slow) : slow) {
                     t = hmin64(fin ? INF64 : (head_end < cpu_next ? head_end : cpu_next));
@@ -897,6 +903,8 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                         }
                     }
                     if (PK) {   // each half ends on its own (only here: a fast step cannot end one)
+                        if (!fin && lane == hbase) my_steps += nsteps;   // this half's steps so far
+                        nsteps = 0;
                         if (bad && lane == hbase &&
                             atomicCAS((unsigned long long *)err, 0ull, (unsigned long long)ERR_TIME) == 0ull)
                             err[1] = s;
@@ -954,7 +962,16 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     break;
                 }
             }
-            if (!fin) {
+            if (PK && !URG_DIST_OFF) {
+                // every lane counts its half's loop steps in 32 bits; the count is moved into the
+                // 64-bit total on the rare path (at most 2^30 ns of simulated time, hence fewer than
+                // 2^30 steps, apart) while the half runs.  An ended half's t_prev is never read.
+                t_prev = t;
+                ++nsteps;
+#ifdef URG_DEBUG
+                if (!fin && lane == hbase) trace_row(t, TR_STEP, 0, 0);
+#endif
+            } else if (!fin) {
                 t_prev = t;
                 if (lane == hbase) ++my_steps;   // one loop step of this half's scenario
 #ifdef URG_DEBUG
