@@ -17,10 +17,10 @@ from dataclasses import replace
 import numpy as np
 import pytest
 
-from oracle import oracle as O
 from workloads import get_config
 
 from .gpu_helpers import agg_from_records, gpu_run
+from .oracle_pool import oracle_one
 
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
@@ -32,19 +32,11 @@ def _cuda():
         pytest.skip("no CUDA device")
 
 
-def _oracle_one(args):
-    name, pol, b, s = args
-    cfg = get_config(name)
-    r = O.run(cfg.workload(), cfg.policies[pol] if isinstance(pol, str) else pol,
-              replace(b, scenario_begin=s, scenario_count=1))
-    return s, r.records[0]
-
-
 def sampled_parity(name, pol, b, rec, sample):
     """Oracle records of `sample` (global indices inside b) equal the GPU's, one scenario per job."""
     # spawned workers: the parent holds a CUDA context; the children run only the C oracle
     with ProcessPoolExecutor(max_workers=min(16, len(sample)), mp_context=mp.get_context("spawn")) as ex:
-        res = list(ex.map(_oracle_one, [(name, pol, b, s) for s in sample]))
+        res = list(ex.map(oracle_one, [(name, pol, b, s) for s in sample]))
     bad = [s for s, r in res if not np.array_equal(r, rec[s - b.scenario_begin])]
     assert not bad, f"{name}/{pol}: scenarios {bad[:8]} differ from the oracle"
     return len(res)
