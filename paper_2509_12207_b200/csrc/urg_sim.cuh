@@ -402,8 +402,6 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         int64_t sync_cost = 0;
         uint32_t akb = 0;
         int64_t L_last = 0;
-        bool urg_last = false;                 // R10 of L_last: 0 <= L_last <= L_th (kept with L_last)
-        bool zwait = false;                    // waiting (PC_SYNC_WAIT) for a sync that costs 0 on return
         int64_t head_end = INF64;              // end of the running kernel, INF64 when the stream runs nothing
         int64_t head_ready = 0;                // time the waiting head became head (R20 key)
         uint32_t head_util = 0;                // util of the running kernel
@@ -536,7 +534,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                 head_u = kr.util_permille; head_dur = head_duration(kr.nominal_ns);
                 if (has_copy) head_copy = kr.flags & 1u;
             }
-            if (pc == PC_SYNC_WAIT && done >= sync_target) { pc = PC_SYNC_RET; zwait = false; cpu_busy(t, sync_cost); }
+            if (pc == PC_SYNC_WAIT && done >= sync_target) { pc = PC_SYNC_RET; cpu_busy(t, sync_cost); }
         };
         // Phase C start of this lane's waiting head: non-preemptive, exact duration (R4, R19, R20)
         auto start_head = [&](int64_t t, uint32_t u_run) {
@@ -640,7 +638,6 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                                            (2u * P.noise_pm + 1u)) - (int32_t)P.noise_pm;
                         const int64_t lax = laxity(t);   // Eq. 2 (R9)
                         L_last = lax;
-                        urg_last = lax >= 0 && lax <= P.lax_threshold_ns;
                         URG_TR(t, TR_EVAL, lax, launched);
                         if (f_early && lax < 0) {
                             URG_TR(t, TR_EARLY_EXIT, 0, 0);
@@ -694,7 +691,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     if (!WIDE && launched < CRF(num_kernels)) nxt = kern_rec(KR + launched);
                     rem_g -= est;
                     if (akb_on) ++akb;
-                    if (coll && urg_last) {
+                    if (coll && L_last >= 0 && L_last <= P.lax_threshold_ns) {
                         // R24: less urgent chains with a busy stream at the same or a higher priority
                         const int64_t own = urgency_key(L_last);
                         uint32_t mm = busy_m & ~(1u << lane), k = 0;
@@ -764,7 +761,6 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                             continue;
                         }
                         pc = PC_SYNC_WAIT;
-                        zwait = sync_cost == 0;
                         cpu_next = INF64; dc = D_INF;
                         break;
                     }
@@ -774,7 +770,6 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     int64_t lax = 0;
                     if (urg) { lax = laxity(t); L_last = lax; URG_TR(t, TR_EVAL, lax, launched); }
                     const bool own_urgent = lax >= 0 && lax <= P.lax_threshold_ns;
-                    if (urg) urg_last = own_urgent;
                     if (f_delay && !own_urgent && (urgent_m & ~(1u << lane)) &&
                         (WIDE ? kern_rec(KR + launched) : nxt).util_permille >= P.util_exempt) {
                         URG_TR(t, TR_DELAY, launched, 0);
@@ -833,7 +828,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         // binding snapshot is not needed).
         auto snapshot = [&](bool may_bind, uint32_t &urgent_m, uint32_t &active_m, uint32_t &busy_m) {
             urgent_m = 0; active_m = 0; busy_m = 0;
-            if (f_delay) urgent_m = __ballot_sync(FULL, akb > 0 && urg_last) & hmask;
+            if (f_delay) urgent_m = __ballot_sync(FULL, akb > 0 && L_last >= 0 && L_last <= P.lax_threshold_ns) & hmask;
             if (coll) {
                 busy_m = __ballot_sync(FULL, launched > done) & hmask;
                 active_m = __ballot_sync(FULL, akb > 0) & hmask;
@@ -988,7 +983,8 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             const bool ret = !fin && (URG_DIST_OFF ? head_end == t : dh == 0u);
             // The retire and due votes are issued together: a retirement makes its own lane due
             // at t only through a sync return of zero cost (retire(): cpu_busy(t, 0) sets cpu_next = t).
-            const bool due_pre = !fin && ((URG_DIST_OFF ? cpu_next == t : dc == 0u) || (ret && zwait && done + 1u >= sync_target));
+            const bool due_pre = !fin && ((URG_DIST_OFF ? cpu_next == t : dc == 0u) || (ret && pc == PC_SYNC_WAIT && done + 1u >= sync_target &&
+                                                            sync_cost == 0));
             const uint32_t retm = __ballot_sync(FULL, ret), duem = __ballot_sync(FULL, due_pre);
             bool dirty = (retm & hmask) != 0u;   // GPU state changed: Phase C must run
             if (retm) {
@@ -1016,7 +1012,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     }
                     const uint32_t nhm = c_always ? 0u : __ballot_sync(FULL, nh);
                     if (f_delay)
-                        urgent_nx = __ballot_sync(FULL, akb > 0 && urg_last) & hmask;
+                        urgent_nx = __ballot_sync(FULL, akb > 0 && L_last >= 0 && L_last <= P.lax_threshold_ns) & hmask;
                     if (f_bind) active_nx = __ballot_sync(FULL, akb > 0) & hmask;
                     dirty |= (nhm & hmask) != 0u;
                 } else if (!c_always)
