@@ -59,11 +59,13 @@ def main():
     from paper_2509_12207_b200.urg import DeviceWorkload
     from workloads import get_config
     from workloads.spec import RECORD_WORDS
+    from bench import Clocks
     names = a.configs.split(",")
     cores = len(os.sched_getaffinity(0))
     pool = mp.get_context("fork").Pool(cores, initializer=_init, initargs=(names,))
     out, md = [], ["| config | point | policy | scenarios | launch events | GPU s | G events/s | Eq. 3 miss ratio | "
-                   "oracle-checked scenarios | mismatches |", "|---|---|---|---|---|---|---|---|---|---|"]
+                   "oracle-checked scenarios | mismatches | SM MHz (median/max), throttle |",
+          "|---|---|---|---|---|---|---|---|---|---|---|"]
     for name in names:
         cfg = get_config(name)
         w = cfg.workload()
@@ -81,6 +83,7 @@ def main():
                     got = {}
                     t0 = time.perf_counter()
                     gpu_s = 0.0
+                    clk = Clocks(torch.cuda.current_device()).__enter__()   # SM clocks / throttle reasons
                     for lo in range(0, b.scenario_count, a.chunk):
                         n = min(a.chunk, b.scenario_count - lo)
                         cb = replace(b, scenario_begin=b.scenario_begin + lo, scenario_count=n)
@@ -97,6 +100,8 @@ def main():
                             for s, x in zip(sel, r.view(np.uint32)):
                                 got[s] = x
                         del rec
+                    clk.__exit__(None, None, None)
+                    clocks = clk.summary()
                     dw.check()
                     a_host = agg.cpu().numpy()
                     per, overall = dw.miss_ratios(a_host)
@@ -107,10 +112,11 @@ def main():
                            "loop_steps": int(a_host[-1]), "gpu_s": gpu_s, "wall_s": time.perf_counter() - t0,
                            "launch_events_per_s": launches / gpu_s, "eq3_miss_ratio": overall,
                            "per_chain_miss_ratio": [float(x) for x in per], "oracle_checked": len(want),
-                           "mismatches": mism[:16]}
+                           "mismatches": mism[:16], "clocks": clocks}
                     out.append(row)
                     md.append(f"| {name} | {bi} (f_a {b.fa_num}/{b.fa_den}) | {pol} | {b.scenario_count} | {launches:.4g} | "
-                              f"{gpu_s:.2f} | {launches / gpu_s / 1e9:.2f} | {overall:.4f} | {len(want)} | {len(mism)} |")
+                              f"{gpu_s:.2f} | {launches / gpu_s / 1e9:.2f} | {overall:.4f} | {len(want)} | {len(mism)} | "
+                              f"{clocks['sm_mhz']}/{clocks['sm_max_mhz']} {','.join(clocks['reasons']) or '-'} |")
                     print(md[-1], flush=True)
     pool.close()
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
@@ -120,7 +126,8 @@ def main():
         f.write(f"# BASELINE.json configurations at full size on one B200 ({a.tag})\n\n"
                 "GPU: `urg_simulate_batch` in chunks of at most 2M scenarios, device-timed.  Oracle: "
                 "configs[0]-[1] every scenario, configs[2]-[4] the first 256, the last 256 and every "
-                "9973rd scenario index, per-scenario records compared bit for bit (BASELINE.md).\n\n")
+                "9973rd scenario index, per-scenario records compared bit for bit (BASELINE.md).  SM clocks "
+                "sampled with nvidia-smi every 100 ms while each row's GPU runs were in flight.\n\n")
         f.write("\n".join(md) + "\n")
 
 
