@@ -348,6 +348,11 @@ static void fill_params(const urg_workload *w, const urg_policy *p, const urg_ba
     P.fa_num = b->fa_num; P.fa_den = b->fa_den; P.fd_num = b->fd_num; P.fd_den = b->fd_den;
     P.ftight_permille = b->ftight_permille; P.tight_explicit = b->tight_explicit; P.tight_mask = b->tight_mask;
     P.trace_buf = g_trace.buf; P.trace_cap = g_trace.cap; P.trace_scn = g_trace.scenario;
+    P.busy_launch_ns = w->launch_ns + (p->kind == URG_URGENGO ? w->launch_akb_ns : 0);
+    auto d32 = [](int64_t d) -> uint32_t { return d >= (int64_t)0x80000000LL ? 0x80000000u : (uint32_t)d; };
+    P.busy_launch_d32 = d32(P.busy_launch_ns);
+    P.sleep_d32 = d32(p->sleep_ns);
+    P.lth_excl = p->lax_threshold_ns < 0 ? 0ull : (uint64_t)p->lax_threshold_ns + 1ull;
 }
 
 // Launch geometry: one warp per scenario in flight, persistent CTAs pulling scenarios

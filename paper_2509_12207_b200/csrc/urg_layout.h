@@ -79,6 +79,12 @@ struct UrgSimParams {
     int64_t cal_end;
     int64_t *cal_buf;
     uint64_t cal_cap;
+    // host-derived constants of the step loop: the launch call's busy time (lambda, + lambda_akb for
+    // UrgenGo) and the delay sleep as saturated 32-bit distances, and R10 as one unsigned compare:
+    // urgent(L) <=> (uint64_t)L < lth_excl (= L_th + 1, or 0 when L_th < 0: never urgent)
+    int64_t busy_launch_ns;
+    uint32_t busy_launch_d32, sleep_d32;
+    uint64_t lth_excl;
     // debug build only (-DURG_DEBUG, liburg_debug.so): event trace of one scenario, [0] = row
     // counter, then rows (t, kind, chain, instance, a, b) in the oracle's trace schema
     int64_t *trace_buf;

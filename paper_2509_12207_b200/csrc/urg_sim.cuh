@@ -269,7 +269,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
     uint32_t *ma_ring = (uint32_t *)(sm + P.ma_offset) + (size_t)threadIdx.x * P.ma_slot;
     uint32_t *ma_cnt = ma_ring + P.ma_max_tasks * P.ma_w;
     uint32_t *ma_pred = ma_cnt + P.ma_max_tasks;
-    const int64_t busy_launch = P.launch_ns + (urg ? P.launch_akb_ns : 0);
+    const int64_t busy_launch = P.busy_launch_ns;   // lambda (+ lambda_akb for UrgenGo), host-derived
     const uint32_t stride = P.agg_stride;
     // lane -> (half, chain); masks and snapshot slots stay indexed by lane
     const int half = PK ? (lane >> 4) : 0;
@@ -392,6 +392,9 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         uint32_t task = 0, launched = 0, done = 0, level = 0;
         uint32_t task_first = 0, task_end = 0;
         int64_t rem_g = 0, rem_c = 0;          // sum of estimates of kernels / CPU segments not yet passed
+        // core UrgenGo build: Eq. 2 without its t, lb = t_arr + D' - rem_g - rem_c, kept instead of the two sums
+        constexpr bool lb_on = urg && !EXT;
+        int64_t lb = 0;
         int32_t nz = 0;                        // R25: estimation noise of the current task instance, per-mille
         int64_t free_req = 0;                  // R28: time of this chain's pending cudaFree request
         bool job = false, job_run = false;     // R29: a CPU job exists / it holds a core
@@ -444,6 +447,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         // Eq. 2 laxity (R9), with the remaining estimated work scaled by the task
         // instance's noise (R25; floor division, identity when noise is off)
         auto laxity = [&](int64_t t) -> int64_t {
+            if (lb_on) return lb - t;
             int64_t rem = rem_g + rem_c;
             if (noise) rem = rem * (1000 + nz) / 1000;
             return t_arr + Dp - rem - t;
@@ -543,7 +547,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             head_util = head_copy ? 0u : head_u;   // a memcpy uses the copy engine, not the SMs (R31)
             head_u = 0xFFFFu;                       // no waiting head now
             head_end = t + (int64_t)d;
-            dh = dsat((int64_t)d);
+            dh = contend ? dsat((int64_t)d) : ((uint32_t)d < D_FAR ? (uint32_t)d : D_FAR);   // d < 2^32 without R30
             URG_DASSERT(t >= head_ready && launched > done, INV_START_BEFORE_READY);
             URG_TR(t, TR_DISPATCH, done, head_end);
         };
@@ -611,6 +615,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     task = stage; launched = k_first; done = k_first; sync_ord = stage << 16;
                     if (!WIDE) nxt = kern_rec(KR + k_first);
                     rem_g = myvar[lane].gpu_est_total; rem_c = CRF(cpu_est_total);
+                    if (lb_on) lb = t_arr + Dp - rem_g - rem_c;
                     if (ma) {   // R26: this instance's ~E^cpu_j, floor mean of the last min(W, h_j) measurements
                         rem_c = 0;
                         for (uint32_t j = 0; j < CRF(num_tasks); ++j) {
@@ -690,8 +695,9 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     ++launched; ++n_launch;
                     if (!WIDE && launched < CRF(num_kernels)) nxt = kern_rec(KR + launched);
                     rem_g -= est;
+                    if (lb_on) lb += est;
                     if (akb_on) ++akb;
-                    if (coll && L_last >= 0 && L_last <= P.lax_threshold_ns) {
+                    if (coll && (uint64_t)L_last < P.lth_excl) {
                         // R24: less urgent chains with a busy stream at the same or a higher priority
                         const int64_t own = urgency_key(L_last);
                         uint32_t mm = busy_m & ~(1u << lane), k = 0;
@@ -704,7 +710,11 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                         if (k) URG_TR(t, TR_COLLISION, k + 1 > 32 ? 32 : k + 1, level);
                     }
                     const bool last = launched == task_end;
-                    if (last) rem_c -= ma ? ma_pred[task] : T.task[tbase + task].cpu_estimate_ns;
+                    if (last) {
+                        const uint32_t ce = ma ? ma_pred[task] : T.task[tbase + task].cpu_estimate_ns;
+                        rem_c -= ce;
+                        if (lb_on) lb += ce;
+                    }
                     const uint32_t sm = P.sync_mode;
                     int32_t target = -1;
                     if (r17_sel) {
@@ -769,13 +779,13 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                 if (pc == PC_CPU_DONE || pc == PC_ATTEMPT) {   // launch attempt for kernel n = launched (R14-R16)
                     int64_t lax = 0;
                     if (urg) { lax = laxity(t); L_last = lax; URG_TR(t, TR_EVAL, lax, launched); }
-                    const bool own_urgent = lax >= 0 && lax <= P.lax_threshold_ns;
+                    const bool own_urgent = (uint64_t)lax < P.lth_excl;   // R10: 0 <= L <= L_th
                     if (f_delay && !own_urgent && (urgent_m & ~(1u << lane)) &&
                         (WIDE ? kern_rec(KR + launched) : nxt).util_permille >= P.util_exempt) {
                         URG_TR(t, TR_DELAY, launched, 0);
                         pc = PC_ATTEMPT;
                         cpu_next = t + P.sleep_ns;
-                        dc = dsat(P.sleep_ns);
+                        dc = P.sleep_d32;
                         break;
                     }
                     if (launched == task_first) {   // task-level stream binding
@@ -815,7 +825,8 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                         URG_TR(t, TR_BIND, level, launched);
                     }
                     pc = PC_ENQUEUE;
-                    cpu_busy(t, busy_launch);
+                    if (!cores_on || busy_launch == 0) { cpu_next = t + busy_launch; dc = P.busy_launch_d32; }
+                    else cpu_busy(t, busy_launch);
                     if (busy_launch > 0) break;
                     continue;
                 }
@@ -828,7 +839,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         // binding snapshot is not needed).
         auto snapshot = [&](bool may_bind, uint32_t &urgent_m, uint32_t &active_m, uint32_t &busy_m) {
             urgent_m = 0; active_m = 0; busy_m = 0;
-            if (f_delay) urgent_m = __ballot_sync(FULL, akb > 0 && L_last >= 0 && L_last <= P.lax_threshold_ns) & hmask;
+            if (f_delay) urgent_m = __ballot_sync(FULL, akb > 0 && (uint64_t)L_last < P.lth_excl) & hmask;
             if (coll) {
                 busy_m = __ballot_sync(FULL, launched > done) & hmask;
                 active_m = __ballot_sync(FULL, akb > 0) & hmask;
@@ -1012,7 +1023,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     }
                     const uint32_t nhm = c_always ? 0u : __ballot_sync(FULL, nh);
                     if (f_delay)
-                        urgent_nx = __ballot_sync(FULL, akb > 0 && L_last >= 0 && L_last <= P.lax_threshold_ns) & hmask;
+                        urgent_nx = __ballot_sync(FULL, akb > 0 && (uint64_t)L_last < P.lth_excl) & hmask;
                     if (f_bind) active_nx = __ballot_sync(FULL, akb > 0) & hmask;
                     dirty |= (nhm & hmask) != 0u;
                 } else if (!c_always)
