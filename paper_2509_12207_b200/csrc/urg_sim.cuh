@@ -871,7 +871,10 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         // Warp-uniform: t_prev (time of the previous loop step) and `used`, the util
         // per-mille of the running kernels (kept incrementally).
         int64_t t_prev = -1;
-        uint32_t adv = 0;                       // sum of fast-path advances since the last exact refresh
+        // fast-step budget: a step of m ns stays on the fast path iff 0 < m < budget, where budget =
+        // min(2^30 - advance since the last exact refresh, H_stop - t_prev + 1) -- one compare covers
+        // "time did not advance", "a distance may be inexact" and "past the end of the horizon"
+        uint32_t budget = H_stop + 2 >= (int64_t)D_SLOW ? D_SLOW : (uint32_t)(H_stop + 2);   // t_prev = -1
         uint32_t used = 0;
         bool bar_prev = false;                  // R28: a barrier was pending at the previous step
         int64_t cal_next = 0;                   // CAL: next sampling time
@@ -896,7 +899,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             if constexpr (!URG_DIST_OFF) {   // (the 64-bit head below is kept for A/B: -DURG_NO_DIST)
                 const uint32_t m = hmin(fin ? D_INF : (dc < dh ? dc : dh));
                 t = (int64_t)((uint64_t)t_prev + m);   // (an ended half's t_prev may be INF64: wraps, unused)
-                const bool slow = !fin && ((m - 1u) >= D_SLOW - 1u || adv + m >= D_SLOW || t > H_stop);
+                const bool slow = !fin && (m - 1u) >= budget - 1u;
                 if (PK ? __any_sync(FULL, slow) : slow) {
                     t = hmin64(fin ? INF64 : (head_end < cpu_next ? head_end : cpu_next));
                     bad = !fin && t <= t_prev;
@@ -904,7 +907,10 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                         dc = cpu_next == INF64 ? D_INF : dsat(cpu_next - t);
                         dh = head_end == INF64 ? D_INF : dsat(head_end - t);
                     }
-                    adv = 0;
+                    {
+                        const int64_t hb = H_stop - t + 1;
+                        budget = hb >= (int64_t)D_SLOW ? D_SLOW : (hb < 1 ? 1u : (uint32_t)hb);
+                    }
                     if (!PK && !CAL) {
                         if (t > H_stop) break;
                         if (bad) {   // report and stop this scenario
@@ -926,7 +932,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                 } else {
                     dc -= m;
                     dh -= m;
-                    adv += m;
+                    budget -= m;
                 }
             } else {   // 64-bit next-event times; 32-bit distances from t_prev, saturated
                 const int64_t mine = fin ? INF64 : (head_end < cpu_next ? head_end : cpu_next);
