@@ -16,7 +16,6 @@
 #include "urg_layout.h"
 
 #define FULL 0xFFFFFFFFu
-#define URG_RARE(x) __builtin_expect(!!(x), 0)   // branch layout hint: the hot path falls through
 #define INF64 0x7FFFFFFFFFFFFFFFLL
 // 32-bit distances of a lane's next CPU event and kernel end from the last step time (see
 // the event loop): D_INF = none, D_FAR = at least 2^31 ns away (a lower bound), and every
@@ -560,12 +559,12 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             if (cores_on && job) { job = false; job_run = false; cpu_chg = true; }   // R29: the job completed
             if (te && pc == PC_WAIT_MSG) take_msg();   // woken by a delivered message (R32)
             for (uint32_t guard = 0;; ++guard) {
-                if (URG_RARE(guard > (1u << 24))) {
+                if (guard > (1u << 24)) {
                     if (atomicCAS((unsigned long long *)err, 0ull, (unsigned long long)ERR_GUARD) == 0ull) err[1] = s;
                     cpu_next = INF64; dc = D_INF;
                     break;
                 }
-                if (URG_RARE((uint32_t)(pc - PC_SYNC_RET) <= (uint32_t)(PC_TASK_START - PC_SYNC_RET))) {
+                if ((uint32_t)(pc - PC_SYNC_RET) <= (uint32_t)(PC_TASK_START - PC_SYNC_RET)) {
                 bool next_inst = false;
                 bool task_done = false;
                 if (pc == PC_SYNC_RET) {   // sync returned: covered kernels leave the AKB
@@ -645,7 +644,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                         const int64_t lax = laxity(t);   // Eq. 2 (R9)
                         L_last = lax;
                         URG_TR(t, TR_EVAL, lax, launched);
-                        if (URG_RARE(f_early && lax < 0)) {
+                        if (f_early && lax < 0) {
                             URG_TR(t, TR_EARLY_EXIT, 0, 0);
                             akb = 0;
                             ++n_early;
@@ -781,15 +780,15 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     int64_t lax = 0;
                     if (urg) { lax = laxity(t); L_last = lax; URG_TR(t, TR_EVAL, lax, launched); }
                     const bool own_urgent = (uint64_t)lax < P.lth_excl;   // R10: 0 <= L <= L_th
-                    if (URG_RARE(f_delay && !own_urgent && (urgent_m & ~(1u << lane)) &&
-                        (WIDE ? kern_rec(KR + launched) : nxt).util_permille >= P.util_exempt)) {
+                    if (f_delay && !own_urgent && (urgent_m & ~(1u << lane)) &&
+                        (WIDE ? kern_rec(KR + launched) : nxt).util_permille >= P.util_exempt) {
                         URG_TR(t, TR_DELAY, launched, 0);
                         pc = PC_ATTEMPT;
                         cpu_next = t + P.sleep_ns;
                         dc = P.sleep_d32;
                         break;
                     }
-                    if (URG_RARE(launched == task_first)) {   // task-level stream binding
+                    if (launched == task_first) {   // task-level stream binding
                         if (KIND == K_STATIC) level = static_level;
                         else if (cls) {   // R27: rank among itself and the AKB-active chains
                             uint32_t mm = active_m & ~(1u << lane);
@@ -901,7 +900,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                 const uint32_t m = hmin(fin ? D_INF : (dc < dh ? dc : dh));
                 t = (int64_t)((uint64_t)t_prev + m);   // (an ended half's t_prev may be INF64: wraps, unused)
                 const bool slow = !fin && (m - 1u) >= budget - 1u;
-                if (URG_RARE(PK ? __any_sync(FULL, slow) : slow)) {
+                if (PK ? __any_sync(FULL, slow) : slow) {
                     t = hmin64(fin ? INF64 : (head_end < cpu_next ? head_end : cpu_next));
                     bad = !fin && t <= t_prev;
                     if (!fin && t != INF64) {
