@@ -10,9 +10,11 @@
 #define URG_QTABLE 4096              // quantile-table entries (12-bit index)
 #define URG_MAX_BLOB_BYTES (160u * 1024u)
 #define URG_COLL_BINS 33             // aggregate: kernel-collision histogram bins (R24)
-#define URG_SNAP_BYTES_PER_LANE 80u  // per lane: laxity, two policy keys (8 B each), level, mailbox (4 B each),
+#define URG_SNAP_BYTES_PER_LANE 144u  // per lane: laxity, two policy keys (8 B each), level, mailbox (4 B each),
                                      // the template variant's two estimate totals (16 B), the lane's current
-                                     // blocks of four per-kernel (R4) and four sync-cost (R5) Philox words
+                                     // blocks of four per-kernel (R4) and four sync-cost (R5) Philox words,
+                                     // P' and H_stop (8 B each, read on the rare path), t_arr and D'
+                                     // (throughput UrgenGo build), the R22 record counters (32 B)
 
 enum { URG_TAG_ARR = 1, URG_TAG_TIGHT = 2, URG_TAG_INST = 3, URG_TAG_KERN = 4, URG_TAG_SYNC = 5, URG_TAG_NOISE = 6 };
 

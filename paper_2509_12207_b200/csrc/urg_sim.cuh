@@ -239,6 +239,14 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
     UrgVarRec *myvar = (UrgVarRec *)(snapL + 128);  // R33: each lane's variant estimate totals
     uint4 *kqw = (uint4 *)(snapL + 192);            // R4: the lane's current block of four KERN words
     uint4 *syw = (uint4 *)(snapL + 256);            // R5: the lane's current block of four SYNC words
+    // cold per-lane scalars kept in shared memory (read once per instance / on the rare path), so the
+    // packed build's registers hold the per-step state: P' and the half's H_stop
+    volatile int64_t *cold_Pp = snapL + 320, *cold_Hs = snapL + 352;
+    // ... the throughput UrgenGo build's t_arr and D' (read per instance), and every build's per-scenario
+    // record counters of R22 (updated once per instance)
+    volatile int64_t *cold_Ta = snapL + 384, *cold_Dp = snapL + 416;
+    struct UrgAcc { uint32_t total, miss, early, unfin, hash, pad; unsigned long long sum_rt; };   // 32 B
+    volatile UrgAcc *rac = (volatile UrgAcc *)(snapL + 448) + lane;
     constexpr bool urg = KIND == K_URGENGO;
     constexpr bool cls = KIND >= K_EDF;        // classical policies (R27): AKB-tracking, no urgency
     constexpr bool akb_on = urg || cls;
@@ -297,7 +305,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         const uint32_t ml = hmin(hi == mh ? lo : 0xFFFFFFFFu);
         return (int64_t)(((uint64_t)mh << 32) | ml);
     };
-    unsigned long long my_launches = 0, my_steps = 0;
+    unsigned long long my_steps = 0;
 #ifdef URG_STATS
     unsigned long long st_single = 0, st_multi = 0, st_dispatch = 0, st_rebase = 0;   // profiling build only
 #endif
@@ -366,6 +374,8 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             maxD = x > maxD ? x : maxD;
         }
         const int64_t H = P.horizon_ns, H_stop = H + maxD;
+        cold_Pp[lane] = Pp;
+        cold_Hs[lane] = H_stop;
         uint32_t static_level = 0;
         {
             uint32_t r = 1;
@@ -416,8 +426,8 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                                                // `launched`), loaded one launch ahead (off the critical path;
                                                // the throughput builds reload it: registers)
         bool head_copy = false;                // R31: the head is a memcpy (copy engine)
-        uint32_t n_total = 0, n_miss = 0, n_early = 0, n_unfin = 0, n_launch = 0, hash = 2166136261u;
-        uint64_t sum_rt = 0;
+        uint32_t n_launch = 0;
+        rac->total = 0; rac->miss = 0; rac->early = 0; rac->unfin = 0; rac->hash = 2166136261u; rac->sum_rt = 0ull;
         uint32_t msg = 0;                      // R32: delivered, untaken message (instance + 1), 0 = none
         uint32_t expect = 0;                   // R32, last stage: next instance to record
 #ifdef URG_DEBUG
@@ -436,7 +446,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             int64_t jit = 0;
             if (P.jitter_ns > 0)
                 jit = (int64_t)(rng_word(P.seed, s, URG_TAG_ARR, cid, i, 0) % (uint32_t)(P.jitter_ns + 1));
-            return CRF(offset_ns) + (int64_t)i * Pp + jit;
+            return CRF(offset_ns) + (int64_t)i * (WIDE ? cold_Pp[lane] : Pp) + jit;
         };
         auto inst_factor = [&](uint32_t w, uint32_t sigma) -> uint32_t {
             if (!T.inst_q) return 65536u;
@@ -483,8 +493,10 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             return o < sl;
         };
 
+        if (lb_on) cold_Dp[lane] = Dp;
         if (valid) {
             t_arr = arrival(0);
+            if (lb_on) cold_Ta[lane] = t_arr;
             if (te && stage > 0) pc = PC_WAIT_MSG;   // R32: waits for the previous task's message
             else if (t_arr < H) { pc = PC_ARRIVE; cpu_next = t_arr; dc = dsat(t_arr + 1); }   // t_prev = -1
         }
@@ -495,9 +507,8 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             msg = 0;
             if (last_stage)
                 for (; expect < i; ++expect) {
-                    ++n_miss;
-                    hash = (hash ^ 0xFFFFFFFFu) * 16777619u;
-                    hash = (hash ^ 0xFFFFFFFFu) * 16777619u;
+                    rac->miss = rac->miss + 1u;
+                    rac->hash = (((rac->hash ^ 0xFFFFFFFFu) * 16777619u) ^ 0xFFFFFFFFu) * 16777619u;
                 }
             inst = i;
             t_arr = arrival(i);
@@ -591,13 +602,13 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                         next_inst = true;
                     } else {   // instance complete (R18, R22)
                         expect = inst + 1u;
-                        const int64_t rt = t - t_arr;
+                        const int64_t rt = t - (lb_on ? cold_Ta[lane] : t_arr);
+                        const int64_t Dpc = lb_on ? cold_Dp[lane] : Dp;
                         URG_DASSERT(te || (done == launched && launched == CRF(num_kernels)), INV_CONSERVATION);
-                        URG_TR(t, TR_INST_DONE, rt, rt > Dp ? 1 : 0);
-                        if (rt > Dp) ++n_miss;
-                        sum_rt += (uint64_t)rt;
-                        hash = (hash ^ (uint32_t)rt) * 16777619u;
-                        hash = (hash ^ (uint32_t)((uint64_t)rt >> 32)) * 16777619u;
+                        URG_TR(t, TR_INST_DONE, rt, rt > Dpc ? 1 : 0);
+                        if (rt > Dpc) rac->miss = rac->miss + 1u;
+                        rac->sum_rt = rac->sum_rt + (uint64_t)rt;
+                        rac->hash = (((rac->hash ^ (uint32_t)rt) * 16777619u) ^ (uint32_t)((uint64_t)rt >> 32)) * 16777619u;
                         int64_t bin = rt / P.rt_bin_ns;
                         if (bin > (int64_t)P.rt_bins - 1) bin = P.rt_bins - 1;
                         if (!CAL) atomicAdd(&agg[(uint64_t)cid * stride + 5 + bin], 1ull);
@@ -605,8 +616,8 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     }
                 }
                 if (pc == PC_ARRIVE) {   // frame arrival / instance start (R6; R32: the thread's task)
-                    URG_TR(t, TR_INST_START, t_arr, 0);
-                    if (!te) ++n_total;
+                    URG_TR(t, TR_INST_START, lb_on ? cold_Ta[lane] : t_arr, 0);
+                    if (!te) rac->total = rac->total + 1u;
                     if (T.inst_q) {   // words 0 (GPU) and 1 (CPU) of one Philox block (R4)
                         const uint4 w = rng_block(P.seed, s, URG_TAG_INST, cid, inst, 0);
                         Fg = inst_factor(w.x, CRF(gpu_sigma_ppm));
@@ -615,7 +626,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     task = stage; launched = k_first; done = k_first; sync_ord = stage << 16;
                     if (!WIDE) nxt = kern_rec(KR + k_first);
                     rem_g = myvar[lane].gpu_est_total; rem_c = CRF(cpu_est_total);
-                    if (lb_on) lb = t_arr + Dp - rem_g - rem_c;
+                    if (lb_on) lb = cold_Ta[lane] + cold_Dp[lane] - rem_g - rem_c;
                     if (ma) {   // R26: this instance's ~E^cpu_j, floor mean of the last min(W, h_j) measurements
                         rem_c = 0;
                         for (uint32_t j = 0; j < CRF(num_tasks); ++j) {
@@ -647,11 +658,10 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                         if (f_early && lax < 0) {
                             URG_TR(t, TR_EARLY_EXIT, 0, 0);
                             akb = 0;
-                            ++n_early;
+                            rac->early = rac->early + 1u;
                             if (last_stage) {   // R32: an earlier task's exit is a gap the last task records
-                                ++n_miss;
-                                hash = (hash ^ 0xFFFFFFFFu) * 16777619u;
-                                hash = (hash ^ 0xFFFFFFFFu) * 16777619u;
+                                rac->miss = rac->miss + 1u;
+                                rac->hash = (((rac->hash ^ 0xFFFFFFFFu) * 16777619u) ^ 0xFFFFFFFFu) * 16777619u;
                                 expect = inst + 1u;
                             }
                             pc = PC_DONE;
@@ -675,11 +685,12 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                         break;
                     }
                     ++inst;
-                    t_arr = arrival(inst);
-                    if (t_arr >= H) { pc = PC_DONE; cpu_next = INF64; dc = D_INF; break; }   // not admitted
+                    const int64_t ta = arrival(inst);
+                    if (lb_on) cold_Ta[lane] = ta; else t_arr = ta;
+                    if (ta >= H) { pc = PC_DONE; cpu_next = INF64; dc = D_INF; break; }   // not admitted
                     pc = PC_ARRIVE;
-                    cpu_next = t_arr;
-                    if (t_arr > t) { dc = dsat(t_arr - t); break; }
+                    cpu_next = ta;
+                    if (ta > t) { dc = dsat(ta - t); break; }
                     continue;
                 }
                 }
@@ -908,7 +919,8 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                         dh = head_end == INF64 ? D_INF : dsat(head_end - t);
                     }
                     {
-                        const int64_t hb = H_stop - t + 1;
+                        const int64_t hs = WIDE ? cold_Hs[lane] : H_stop;
+                        const int64_t hb = hs - t + 1;
                         budget = hb >= (int64_t)D_SLOW ? D_SLOW : (hb < 1 ? 1u : (uint32_t)hb);
                     }
                     if (!PK && !CAL) {
@@ -925,7 +937,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                         if (bad && lane == hbase &&
                             atomicCAS((unsigned long long *)err, 0ull, (unsigned long long)ERR_TIME) == 0ull)
                             err[1] = s;
-                        fin = fin || t > H_stop || bad;
+                        fin = fin || t > cold_Hs[lane] || bad;
                         if (fin) head_u = 0xFFFFu;   // an ended half dispatches nothing
                         if (__all_sync(FULL, fin)) break;
                     }
@@ -1171,6 +1183,9 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             continue;
         }
         // ---- A11: end of horizon accounting (R7) and per-scenario records ----
+        uint32_t n_total = rac->total, n_miss = rac->miss, n_early = rac->early, n_unfin = rac->unfin,
+                 hash = rac->hash;
+        const uint64_t sum_rt = rac->sum_rt;
         if (te) {   // R32: the chain's early exits and launches, summed over its threads
             uint32_t e_sum = 0, l_sum = 0;
             for (uint32_t o = 0; o < C; ++o) {
@@ -1207,12 +1222,14 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             atomicAdd(&a[4], (unsigned long long)sum_rt);
             if (n_total) atomicAdd(&a[5 + P.rt_bins + (uint64_t)100 * n_miss / n_total], 1ull);
         }
-        my_launches += __reduce_add_sync(FULL, n_launch);
+        {   // the warp's launch events of this scenario (pair): one global add
+            const uint32_t nl = __reduce_add_sync(FULL, n_launch);
+            if (lane == 0 && nl) atomicAdd(&agg[(uint64_t)NC * stride + URG_COLL_BINS + 0], (unsigned long long)nl);
+        }
     }
     if (PK) my_steps += __shfl_sync(FULL, my_steps, 16);   // the upper half's steps
     if (lane == 0) {
         if (CAL) return;
-        atomicAdd(&agg[(uint64_t)NC * stride + URG_COLL_BINS + 0], my_launches);
         atomicAdd(&agg[(uint64_t)NC * stride + URG_COLL_BINS + 1], my_steps);
 #ifdef URG_STATS
         atomicAdd(&work[4], st_single); atomicAdd(&work[5], st_multi);
