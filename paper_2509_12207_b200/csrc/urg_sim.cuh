@@ -204,13 +204,19 @@ __device__ __forceinline__ uint64_t work_offset(uint64_t j, uint64_t S, uint32_t
 // than the 128-register cap of the 512-thread build).
 template <int KIND, int FLAGS, bool KQ, bool WIDE, bool CAL = false, bool EXT = true, bool PK = false,
           bool SMALL = false>
+// packed-build CTA size per policy: with the cold per-lane state in shared memory, UrgenGo takes 832
+// threads (72 registers, 26 warps/SM; configs[3] slice 2.517 -> 2.535 G/s against 640 / 96) and the
+// ASYNC policies 768 (80 registers; configs[2] FIFO 4.51 -> 4.80 G/s), profiles/r02_ab_i_cold_smem.txt
 #ifndef URG_PK_THREADS
-#define URG_PK_THREADS 640   // measured: 96 registers (20 warps/SM) beat 80 at 768 threads with the kept distances
+#define URG_PK_THREADS 832
+#endif
+#ifndef URG_PK_THREADS_ASYNC
+#define URG_PK_THREADS_ASYNC 768
 #endif
 #ifndef URG_LAT_THREADS
 #define URG_LAT_THREADS 512
 #endif
-__global__ void __launch_bounds__(WIDE ? (PK ? URG_PK_THREADS : 1024) : (SMALL ? 256 : URG_LAT_THREADS), 1)
+__global__ void __launch_bounds__(WIDE ? (PK ? (KIND == K_URGENGO ? URG_PK_THREADS : URG_PK_THREADS_ASYNC) : 1024) : (SMALL ? 256 : URG_LAT_THREADS), 1)
 urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t *__restrict__ records,
                unsigned long long *__restrict__ agg, unsigned long long *__restrict__ work,
                long long *__restrict__ err)
