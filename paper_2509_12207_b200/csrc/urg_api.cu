@@ -394,7 +394,7 @@ static urg_status geometry(const urg_workload *w, const void *fn, uint64_t count
 }
 
 // Parameters, kernel instantiation and geometry of one simulation launch.  Shared memory:
-// the template blob, its mbarrier, then per lane the slot fields (urg_layout.h) and, with the
+// the template blob, its mbarrier, then per lane the Phase B snapshot (16 B) and, with the
 // CPU predictor (R26), max_tasks x (W + 2) words of predictor state.
 static urg_status prepare_launch(const urg_workload *w, const urg_policy *p, const urg_batch *b, bool wide, bool cal,
                                  UrgSimParams &P, urg_sim_fn &fn, int &warps, int &ctas)
@@ -416,12 +416,7 @@ static urg_status prepare_launch(const urg_workload *w, const urg_policy *p, con
     P.blob_bytes = (uint32_t)w->blob.size();
     P.mbar_offset = align16(P.blob_bytes);
     P.snap_offset = align16(P.mbar_offset + 16);
-    // the per-lane slot fields the instantiation uses (urg_layout.h): the extra policy-key, level /
-    // mailbox and LCUF fields for the classical policies, the collision metric and the extended and
-    // calibration builds
-    const bool extra_slots = p->kind >= URG_EDF || (p->kind == URG_URGENGO && (p->flags & URG_F_COLLISIONS)) || ext || cal;
-    const uint32_t snap_lane = 8u * urg_snap_fields(extra_slots);
-    uint32_t per_lane = snap_lane;
+    uint32_t per_lane = URG_SNAP_BYTES_PER_LANE;
     if (p->kind >= URG_URGENGO && P.ma_w) {   // UrgenGo and the R27 policies estimate remaining work
         P.ma_max_tasks = w->max_tasks;
         P.ma_slot = w->max_tasks * (P.ma_w + 2);
@@ -430,7 +425,7 @@ static urg_status prepare_launch(const urg_workload *w, const urg_policy *p, con
     urg_status st = geometry(w, (const void *)fn, pk ? (b->scenario_count + 1) / 2 : b->scenario_count,
                              P.snap_offset, per_lane, warps, ctas, P.smem_bytes);
     if (st != URG_OK) return st;
-    P.ma_offset = P.snap_offset + (uint32_t)warps * 32u * snap_lane;
+    P.ma_offset = P.snap_offset + (uint32_t)warps * 32u * URG_SNAP_BYTES_PER_LANE;
     return URG_OK;
 }
 

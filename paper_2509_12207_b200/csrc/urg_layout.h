@@ -10,32 +10,11 @@
 #define URG_QTABLE 4096              // quantile-table entries (12-bit index)
 #define URG_MAX_BLOB_BYTES (160u * 1024u)
 #define URG_COLL_BINS 33             // aggregate: kernel-collision histogram bins (R24)
-// Per-lane shared-memory slots of the simulation kernel: field f of lane l in warp w
-// is the 8-byte word at snap_offset + (w * nf + f) * 256 + l * 8 -- every field of a lane sits at
-// one base register plus an immediate offset, and another lane's field is in the same array.
-// nf = URG_SNAP_FIELDS for the core builds of FIFO / STATIC / UrgenGo without the collision
-// metric, URG_SNAP_FIELDS_EXTRA for the builds that also rank by policy keys, count collisions or
-// run the extended model (urg_snap_fields).
-enum {
-    URG_SL_L = 0,                                  // last laxity: the Phase B snapshot (R21)
-    URG_SL_VT,                                     // the variant's Eq. 2 GPU estimate total (R33)
-    URG_SL_KQ0, URG_SL_KQ1,                        // the lane's current block of four KERN words (R4)
-    URG_SL_SY0, URG_SL_SY1,                        // ... and of four SYNC words (R5)
-    URG_SL_PP, URG_SL_HS, URG_SL_TA, URG_SL_DP,    // P', the half's H_stop, t_arr, D' (cold)
-    URG_SL_R0, URG_SL_R1, URG_SL_R2, URG_SL_R3,    // R22 counters: total|miss, early|unfin, hash, sum rt
-    // kept here instead of registers by the packed build (read on the rare path or once per event):
-    // next CPU event, kernel end, last laxity, batch estimate sum, sync cost, work index, loop steps
-    URG_SL_CN, URG_SL_HE, URG_SL_LL, URG_SL_ACC, URG_SL_SC, URG_SL_JW, URG_SL_ST,
-    URG_SNAP_FIELDS,
-    URG_SL_A = URG_SNAP_FIELDS, URG_SL_B,          // two policy keys (R27; R29 priorities)
-    URG_SL_LM,                                     // stream level (R24) | mailbox (R32), 4 B each
-    URG_SL_VC,                                     // all kernel estimates of the chain (LCUF key, R27)
-    URG_SNAP_FIELDS_EXTRA
-};
-static inline __host__ __device__ unsigned urg_snap_fields(bool extra)
-{
-    return extra ? (unsigned)URG_SNAP_FIELDS_EXTRA : (unsigned)URG_SNAP_FIELDS;
-}
+#define URG_SNAP_BYTES_PER_LANE 144u  // per lane: laxity, two policy keys (8 B each), level, mailbox (4 B each),
+                                     // the template variant's two estimate totals (16 B), the lane's current
+                                     // blocks of four per-kernel (R4) and four sync-cost (R5) Philox words,
+                                     // P' and H_stop (8 B each, read on the rare path), t_arr and D'
+                                     // (throughput UrgenGo build), the R22 record counters (32 B)
 
 enum { URG_TAG_ARR = 1, URG_TAG_TIGHT = 2, URG_TAG_INST = 3, URG_TAG_KERN = 4, URG_TAG_SYNC = 5, URG_TAG_NOISE = 6 };
 

@@ -109,20 +109,6 @@ __device__ __forceinline__ int64_t shfl64(int64_t v, int src)
     return (int64_t)__shfl_sync(FULL, (unsigned long long)v, src);
 }
 
-// A 64-bit per-lane value held in its shared-memory slot (COLD: the packed build, whose registers
-// hold the per-step state) or in a register.  The slot is volatile so the compiler does not keep
-// a register copy of it across the event loop.
-template <bool COLD>
-struct Lane64 {
-    int64_t r;
-    volatile int64_t *p;
-    __device__ __forceinline__ Lane64(volatile int64_t *q, int64_t v) : r(v), p(q) { if (COLD) *p = v; }
-    __device__ __forceinline__ Lane64 &operator=(int64_t v) { if (COLD) *p = v; else r = v; return *this; }
-    __device__ __forceinline__ Lane64 &operator+=(int64_t v) { return *this = (int64_t)*this + v; }
-    __device__ __forceinline__ Lane64 &operator-=(int64_t v) { return *this = (int64_t)*this - v; }
-    __device__ __forceinline__ operator int64_t() const { return COLD ? (int64_t)*p : r; }
-};
-
 // urgency key: orders as 1/L, L = 0 saturating (R9)
 __device__ __forceinline__ int64_t urgency_key(int64_t L)
 {
@@ -250,40 +236,29 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
     const uint32_t C = P.num_lanes;    // threads: chains, or tasks under per-task executors (R32)
     const uint32_t NC = P.num_chains;  // chains: records and aggregates
 
+    // per-warp Phase B snapshot (R21): last laxity of each lane, then its stream level
+    // per-warp Phase B snapshot (R21), 1 KB: last laxity, two policy keys, stream level
+    int64_t *snapL = (int64_t *)(sm + P.snap_offset) + warp * (URG_SNAP_BYTES_PER_LANE * 32 / 8);
+    int64_t *snapA = snapL + 32, *snapB = snapL + 64;
+    uint32_t *snapLev = (uint32_t *)(snapL + 96);
+    uint32_t *mbox = (uint32_t *)(snapL + 112);   // R32: message published to each lane this round
+    UrgVarRec *myvar = (UrgVarRec *)(snapL + 128);  // R33: each lane's variant estimate totals
+    uint4 *kqw = (uint4 *)(snapL + 192);            // R4: the lane's current block of four KERN words
+    uint4 *syw = (uint4 *)(snapL + 256);            // R5: the lane's current block of four SYNC words
+    // cold per-lane scalars kept in shared memory (read once per instance / on the rare path), so the
+    // packed build's registers hold the per-step state: P' and the half's H_stop
+    volatile int64_t *cold_Pp = snapL + 320, *cold_Hs = snapL + 352;
+    // ... the throughput UrgenGo build's t_arr and D' (read per instance), and every build's per-scenario
+    // record counters of R22 (updated once per instance)
+    volatile int64_t *cold_Ta = snapL + 384, *cold_Dp = snapL + 416;
+    struct UrgAcc { uint32_t total, miss, early, unfin, hash, pad; unsigned long long sum_rt; };   // 32 B
+    volatile UrgAcc *rac = (volatile UrgAcc *)(snapL + 448) + lane;
     constexpr bool urg = KIND == K_URGENGO;
     constexpr bool cls = KIND >= K_EDF;        // classical policies (R27): AKB-tracking, no urgency
     constexpr bool akb_on = urg || cls;
     constexpr bool f_bind = urg && (FLAGS & F_BIND), f_delay = urg && (FLAGS & F_DELAY),
                    f_early = urg && (FLAGS & F_EARLY);
     constexpr bool coll = urg && (FLAGS & F_COLL);   // collision metric (R24): not in the schedule
-
-    // Per-lane shared-memory slots (urg_layout.h): field f of this lane is my[f * 32], of lane o
-    // wslot[f * 32 + o]; one base register reaches all of a lane's fields.
-    constexpr uint32_t NF = (cls || coll || EXT) ? URG_SNAP_FIELDS_EXTRA : URG_SNAP_FIELDS;
-    int64_t *wslot = (int64_t *)(sm + P.snap_offset) + warp * (NF * 32);
-    volatile int64_t *my = wslot + lane;
-    int64_t *snapL = wslot + URG_SL_L * 32;               // Phase B snapshot of the last laxities (R21)
-    int64_t *snapA = wslot + URG_SL_A * 32, *snapB = wslot + URG_SL_B * 32;   // policy keys (R27, R29)
-    uint32_t *snapLM = (uint32_t *)(wslot + URG_SL_LM * 32);   // [2o] stream level (R24), [2o+1] mailbox (R32)
-#define SNAP_LEV(o) snapLM[2 * (o)]
-#define MBOX(o) snapLM[2 * (o) + 1]
-    // the lane's current blocks of four KERN (R4) and SYNC (R5) Philox words, two 8-byte fields each
-    int64_t *my_nv = wslot + lane;   // (non-volatile view: the Philox word blocks)
-    auto kq_store = [&](uint4 b) { *(uint2 *)&my_nv[URG_SL_KQ0 * 32] = make_uint2(b.x, b.y);
-                                   *(uint2 *)&my_nv[URG_SL_KQ1 * 32] = make_uint2(b.z, b.w); };
-    auto kq_word = [&](uint32_t q) -> uint32_t { return ((const uint32_t *)&my_nv[(URG_SL_KQ0 + (q >> 1)) * 32])[q & 1u]; };
-    auto sy_store = [&](uint4 b) { *(uint2 *)&my_nv[URG_SL_SY0 * 32] = make_uint2(b.x, b.y);
-                                   *(uint2 *)&my_nv[URG_SL_SY1 * 32] = make_uint2(b.z, b.w); };
-    auto sy_word = [&](uint32_t q) -> uint32_t { return ((const uint32_t *)&my_nv[(URG_SL_SY0 + (q >> 1)) * 32])[q & 1u]; };
-    // cold per-lane scalars (read once per instance / on the rare path): P', the half's H_stop, t_arr
-    // and D' (throughput UrgenGo build)
-    volatile int64_t &cold_Pp = my[URG_SL_PP * 32], &cold_Hs = my[URG_SL_HS * 32];
-    volatile int64_t &cold_Ta = my[URG_SL_TA * 32], &cold_Dp = my[URG_SL_DP * 32];
-    // the per-scenario record counters of R22 (updated once per instance)
-    volatile uint32_t *rc0 = (volatile uint32_t *)&my[URG_SL_R0 * 32], *rc1 = (volatile uint32_t *)&my[URG_SL_R1 * 32];
-    volatile uint32_t &R_total = rc0[0], &R_miss = rc0[1], &R_early = rc1[0], &R_unfin = rc1[1];
-    volatile uint32_t &R_hash = *(volatile uint32_t *)&my[URG_SL_R2 * 32];
-    volatile uint64_t &R_sumrt = *(volatile uint64_t *)&my[URG_SL_R3 * 32];
     // Core build: Phase C's fit ballot runs at every step and is itself the test, so no "new
     // stream head" vote sits between Phase B and Phase C (a head that did not fit at an earlier
     // Phase C still does not: `used` only falls at a retirement).
@@ -336,7 +311,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         const uint32_t ml = hmin(hi == mh ? lo : 0xFFFFFFFFu);
         return (int64_t)(((uint64_t)mh << 32) | ml);
     };
-    Lane64<PK> my_steps(&my[URG_SL_ST * 32], 0);   // loop steps (the lane at the half's base counts)
+    unsigned long long my_steps = 0;
 #ifdef URG_STATS
     unsigned long long st_single = 0, st_multi = 0, st_dispatch = 0, st_rebase = 0;   // profiling build only
 #endif
@@ -370,16 +345,10 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         const bool valid = valid_c && jw < P.scenario_count;
         if (jw < P.scenario_count) jw = work_offset(jw, P.scenario_count, P.num_variants);
         const uint32_t s = (uint32_t)(P.scenario_begin + jw);
-        if (PK) my[URG_SL_JW * 32] = (int64_t)jw;   // read back by the epilogue (registers: the event loop)
         // R33: this scenario's template variant -- its kernel records and estimate totals
         const uint32_t vidx = P.num_variants > 1 ? s % P.num_variants : 0u;
-        const uint32_t kro = vidx * P.nk_total + kbase;   // the lane's records: P.kern[kro + k] (host: V * sum N < 2^31)
-#define KREC(n) kern_rec(P.kern + kro + (n))
-        if (valid_c) {   // the variant's estimate totals, per lane
-            const UrgVarRec vr = P.var[(size_t)vidx * C + c];
-            my[URG_SL_VT * 32] = vr.gpu_est_total;
-            if (NF > URG_SNAP_FIELDS) my[URG_SL_VC * 32] = vr.gpu_est_chain;
-        }
+        const UrgKernRec *KR = P.kern + (size_t)vidx * P.nk_total + kbase;
+        if (valid_c) myvar[lane] = P.var[(size_t)vidx * C + c];   // the variant's estimate totals, per lane
 
         // ---- A1: scenario init (R3, R15 STATIC) ----
         int64_t Pp = 0, Dp = 0;
@@ -411,8 +380,8 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             maxD = x > maxD ? x : maxD;
         }
         const int64_t H = P.horizon_ns, H_stop = H + maxD;
-        cold_Pp = Pp;
-        cold_Hs = H_stop;
+        cold_Pp[lane] = Pp;
+        cold_Hs[lane] = H_stop;
         uint32_t static_level = 0;
         {
             uint32_t r = 1;
@@ -426,11 +395,11 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         }
 
         // ---- per-lane dynamic state ----
-        if (te) { MBOX(lane) = 0u; __syncwarp(); }   // R32: no message published yet
+        if (te) { mbox[lane] = 0u; __syncwarp(); }   // R32: no message published yet
         if (ma)
             for (uint32_t j = 0; j < P.ma_max_tasks; ++j) ma_cnt[j] = 0;
         int pc = PC_DONE;
-        Lane64<PK> cpu_next(&my[URG_SL_CN * 32], INF64);
+        int64_t cpu_next = INF64;
         uint32_t dc = D_INF, dh = D_INF;       // distances of cpu_next and head_end from the last step time
         auto dsat = [](int64_t d) -> uint32_t { return d >= (int64_t)D_FAR ? D_FAR : (uint32_t)d; };
         uint32_t inst = 0;
@@ -447,16 +416,12 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         bool job = false, job_run = false;     // R29: a CPU job exists / it holds a core
         bool cpu_chg = false, rerank_req = false;
         int64_t job_rem = 0, job_ready = 0, run_start = 0, cpu_prio = 0;
-        Lane64<PK> acc(&my[URG_SL_ACC * 32], 0);
+        int64_t acc = 0;
         uint32_t batch_start = 0, sync_target = 0, sync_ord = 0;
-        Lane64<PK> sync_cost(&my[URG_SL_SC * 32], 0);
-        uint32_t zwake = 0xFFFFFFFFu;          // SYNC_WAIT on a zero-cost sync: the retirement of kernel
-                                               // zwake (= sync_target - 1) makes the lane due at once
+        int64_t sync_cost = 0;
         uint32_t akb = 0;
-        Lane64<PK> L_last(&my[URG_SL_LL * 32], 0);
-        bool lurg = 0 < P.lth_excl;            // R10 of L_last: (uint64_t)L_last < lth_excl
-        auto set_L = [&](int64_t v) { L_last = v; lurg = (uint64_t)v < P.lth_excl; };
-        Lane64<PK> head_end(&my[URG_SL_HE * 32], INF64);   // end of the running kernel, INF64 when none runs
+        int64_t L_last = 0;
+        int64_t head_end = INF64;              // end of the running kernel, INF64 when the stream runs nothing
         int64_t head_ready = 0;                // time the waiting head became head (R20 key)
         uint32_t head_util = 0;                // util of the running kernel
         uint32_t head_u = 0xFFFFu;             // util of the waiting head; 0xFFFF while none waits (no head,
@@ -468,7 +433,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                                                // the throughput builds reload it: registers)
         bool head_copy = false;                // R31: the head is a memcpy (copy engine)
         uint32_t n_launch = 0;
-        R_total = 0; R_miss = 0; R_early = 0; R_unfin = 0; R_hash = 2166136261u; R_sumrt = 0ull;
+        rac->total = 0; rac->miss = 0; rac->early = 0; rac->unfin = 0; rac->hash = 2166136261u; rac->sum_rt = 0ull;
         uint32_t msg = 0;                      // R32: delivered, untaken message (instance + 1), 0 = none
         uint32_t expect = 0;                   // R32, last stage: next instance to record
 #ifdef URG_DEBUG
@@ -487,7 +452,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             int64_t jit = 0;
             if (P.jitter_ns > 0)
                 jit = (int64_t)(rng_word(P.seed, s, URG_TAG_ARR, cid, i, 0) % (uint32_t)(P.jitter_ns + 1));
-            return CRF(offset_ns) + (int64_t)i * (WIDE ? cold_Pp : Pp) + jit;
+            return CRF(offset_ns) + (int64_t)i * (WIDE ? cold_Pp[lane] : Pp) + jit;
         };
         auto inst_factor = [&](uint32_t w, uint32_t sigma) -> uint32_t {
             if (!T.inst_q) return 65536u;
@@ -513,7 +478,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         auto cls_key_a = [&]() -> int64_t {
             return KIND == K_EDF ? t_arr + Dp : KIND == K_HRRN ? t_arr : KIND == K_LCUF ? Pp : 0;
         };
-        auto cls_key_b = [&]() -> int64_t { return KIND == K_LCUF ? (int64_t)my[URG_SL_VC * 32] : rem_g + rem_c; };
+        auto cls_key_b = [&]() -> int64_t { return KIND == K_LCUF ? myvar[lane].gpu_est_chain : rem_g + rem_c; };
         // "chain o ranks before chain s" (ties by smaller chain id; exact 128-bit ratios)
         auto cls_before = [&](int64_t oA, int64_t oB, int o, int64_t sA, int64_t sB, int sl, int64_t t) -> bool {
             if (KIND == K_EDF || KIND == K_SJF) {
@@ -534,10 +499,10 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             return o < sl;
         };
 
-        if (lb_on) cold_Dp = Dp;
+        if (lb_on) cold_Dp[lane] = Dp;
         if (valid) {
             t_arr = arrival(0);
-            if (lb_on) cold_Ta = t_arr;
+            if (lb_on) cold_Ta[lane] = t_arr;
             if (te && stage > 0) pc = PC_WAIT_MSG;   // R32: waits for the previous task's message
             else if (t_arr < H) { pc = PC_ARRIVE; cpu_next = t_arr; dc = dsat(t_arr + 1); }   // t_prev = -1
         }
@@ -548,8 +513,8 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             msg = 0;
             if (last_stage)
                 for (; expect < i; ++expect) {
-                    R_miss = R_miss + 1u;
-                    R_hash = (((R_hash ^ 0xFFFFFFFFu) * 16777619u) ^ 0xFFFFFFFFu) * 16777619u;
+                    rac->miss = rac->miss + 1u;
+                    rac->hash = (((rac->hash ^ 0xFFFFFFFFu) * 16777619u) ^ 0xFFFFFFFFu) * 16777619u;
                 }
             inst = i;
             t_arr = arrival(i);
@@ -569,8 +534,8 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                 // kernel `done` follows `done` - 1 of the same instance, so the four words of a Philox
                 // block are drawn once and kept in the lane's shared-memory slot; a new block (or the
                 // instance's first kernel) refills it
-                if ((done & 3u) == 0u || done == k_first) kq_store(rng_block(P.seed, s, URG_TAG_KERN, cid, inst, done));
-                G = T.kern_q[kq_word(done & 3u) >> 20];
+                if ((done & 3u) == 0u || done == k_first) kqw[lane] = rng_block(P.seed, s, URG_TAG_KERN, cid, inst, done);
+                G = T.kern_q[((const uint32_t *)&kqw[lane])[done & 3u] >> 20];
             }
 #endif
             const uint64_t d = ((((uint64_t)nom * Fg) >> 16) * G) >> 16;
@@ -586,11 +551,11 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             head_u = 0xFFFFu;
             if (launched > done) {
                 head_ready = t;
-                const UrgKernRec kr = KREC(done);
+                const UrgKernRec kr = kern_rec(KR + done);
                 head_u = kr.util_permille; head_dur = head_duration(kr.nominal_ns);
                 if (has_copy) head_copy = kr.flags & 1u;
             }
-            if (pc == PC_SYNC_WAIT && done >= sync_target) { pc = PC_SYNC_RET; zwake = 0xFFFFFFFFu; cpu_busy(t, sync_cost); }
+            if (pc == PC_SYNC_WAIT && done >= sync_target) { pc = PC_SYNC_RET; cpu_busy(t, sync_cost); }
         };
         // Phase C start of this lane's waiting head: non-preemptive, exact duration (R4, R19, R20)
         auto start_head = [&](int64_t t, uint32_t u_run) {
@@ -639,17 +604,17 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                         task_end += T.task[tbase + task].num_kernels;
                         pc = PC_TASK_START;
                     } else if (!last_stage) {   // R32: publish instance inst to the next task's thread
-                        MBOX(lane + 1) = inst + 1u;
+                        mbox[lane + 1] = inst + 1u;
                         next_inst = true;
                     } else {   // instance complete (R18, R22)
                         expect = inst + 1u;
-                        const int64_t rt = t - (lb_on ? cold_Ta : t_arr);
-                        const int64_t Dpc = lb_on ? cold_Dp : Dp;
+                        const int64_t rt = t - (lb_on ? cold_Ta[lane] : t_arr);
+                        const int64_t Dpc = lb_on ? cold_Dp[lane] : Dp;
                         URG_DASSERT(te || (done == launched && launched == CRF(num_kernels)), INV_CONSERVATION);
                         URG_TR(t, TR_INST_DONE, rt, rt > Dpc ? 1 : 0);
-                        if (rt > Dpc) R_miss = R_miss + 1u;
-                        R_sumrt = R_sumrt + (uint64_t)rt;
-                        R_hash = (((R_hash ^ (uint32_t)rt) * 16777619u) ^ (uint32_t)((uint64_t)rt >> 32)) * 16777619u;
+                        if (rt > Dpc) rac->miss = rac->miss + 1u;
+                        rac->sum_rt = rac->sum_rt + (uint64_t)rt;
+                        rac->hash = (((rac->hash ^ (uint32_t)rt) * 16777619u) ^ (uint32_t)((uint64_t)rt >> 32)) * 16777619u;
                         int64_t bin = rt / P.rt_bin_ns;
                         if (bin > (int64_t)P.rt_bins - 1) bin = P.rt_bins - 1;
                         if (!CAL) atomicAdd(&agg[(uint64_t)cid * stride + 5 + bin], 1ull);
@@ -657,17 +622,17 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     }
                 }
                 if (pc == PC_ARRIVE) {   // frame arrival / instance start (R6; R32: the thread's task)
-                    URG_TR(t, TR_INST_START, lb_on ? cold_Ta : t_arr, 0);
-                    if (!te) R_total = R_total + 1u;
+                    URG_TR(t, TR_INST_START, lb_on ? cold_Ta[lane] : t_arr, 0);
+                    if (!te) rac->total = rac->total + 1u;
                     if (T.inst_q) {   // words 0 (GPU) and 1 (CPU) of one Philox block (R4)
                         const uint4 w = rng_block(P.seed, s, URG_TAG_INST, cid, inst, 0);
                         Fg = inst_factor(w.x, CRF(gpu_sigma_ppm));
                         Fc = inst_factor(w.y, CRF(cpu_sigma_ppm));
                     }
                     task = stage; launched = k_first; done = k_first; sync_ord = stage << 16;
-                    if (!WIDE) nxt = KREC(k_first);
-                    rem_g = my[URG_SL_VT * 32]; rem_c = CRF(cpu_est_total);
-                    if (lb_on) lb = cold_Ta + cold_Dp - rem_g - rem_c;
+                    if (!WIDE) nxt = kern_rec(KR + k_first);
+                    rem_g = myvar[lane].gpu_est_total; rem_c = CRF(cpu_est_total);
+                    if (lb_on) lb = cold_Ta[lane] + cold_Dp[lane] - rem_g - rem_c;
                     if (ma) {   // R26: this instance's ~E^cpu_j, floor mean of the last min(W, h_j) measurements
                         rem_c = 0;
                         for (uint32_t j = 0; j < CRF(num_tasks); ++j) {
@@ -694,15 +659,15 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                             nz = (int32_t)(rng_word(P.seed, s, URG_TAG_NOISE, cid, inst, task) %
                                            (2u * P.noise_pm + 1u)) - (int32_t)P.noise_pm;
                         const int64_t lax = laxity(t);   // Eq. 2 (R9)
-                        set_L(lax);
+                        L_last = lax;
                         URG_TR(t, TR_EVAL, lax, launched);
                         if (f_early && lax < 0) {
                             URG_TR(t, TR_EARLY_EXIT, 0, 0);
                             akb = 0;
-                            R_early = R_early + 1u;
+                            rac->early = rac->early + 1u;
                             if (last_stage) {   // R32: an earlier task's exit is a gap the last task records
-                                R_miss = R_miss + 1u;
-                                R_hash = (((R_hash ^ 0xFFFFFFFFu) * 16777619u) ^ 0xFFFFFFFFu) * 16777619u;
+                                rac->miss = rac->miss + 1u;
+                                rac->hash = (((rac->hash ^ 0xFFFFFFFFu) * 16777619u) ^ 0xFFFFFFFFu) * 16777619u;
                                 expect = inst + 1u;
                             }
                             pc = PC_DONE;
@@ -727,7 +692,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     }
                     ++inst;
                     const int64_t ta = arrival(inst);
-                    if (lb_on) cold_Ta = ta; else t_arr = ta;
+                    if (lb_on) cold_Ta[lane] = ta; else t_arr = ta;
                     if (ta >= H) { pc = PC_DONE; cpu_next = INF64; dc = D_INF; break; }   // not admitted
                     pc = PC_ARRIVE;
                     cpu_next = ta;
@@ -737,7 +702,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                 }
                 if (pc == PC_ENQUEUE) {   // the kernel reaches its stream (R16) + sync decision (R17)
                     const uint32_t n = launched;
-                    const UrgKernRec kr = WIDE ? KREC(n) : nxt;
+                    const UrgKernRec kr = WIDE ? kern_rec(KR + n) : nxt;
                     const int64_t est = kr.estimate_ns;
                     if (launched == done) {   // stream was empty: head now
                         head_ready = t; head_u = kr.util_permille; head_dur = head_duration(kr.nominal_ns); newhead = true;
@@ -745,18 +710,18 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     }
                     URG_TR(t, TR_ENQUEUE, n, level);
                     ++launched; ++n_launch;
-                    if (!WIDE && launched < CRF(num_kernels)) nxt = KREC(launched);
+                    if (!WIDE && launched < CRF(num_kernels)) nxt = kern_rec(KR + launched);
                     rem_g -= est;
                     if (lb_on) lb += est;
                     if (akb_on) ++akb;
-                    if (coll && lurg) {
+                    if (coll && (uint64_t)L_last < P.lth_excl) {
                         // R24: less urgent chains with a busy stream at the same or a higher priority
                         const int64_t own = urgency_key(L_last);
                         uint32_t mm = busy_m & ~(1u << lane), k = 0;
                         while (mm) {
                             const int o = __ffs(mm) - 1;
                             mm &= mm - 1;
-                            k += (SNAP_LEV(o) <= level && urgency_key(snapL[o]) < own) ? 1u : 0u;
+                            k += (snapLev[o] <= level && urgency_key(snapL[o]) < own) ? 1u : 0u;
                         }
                         if (k && !CAL) atomicAdd(&agg[(uint64_t)NC * stride + (k + 1 > 32 ? 32 : k + 1)], 1ull);
                         if (k) URG_TR(t, TR_COLLISION, k + 1 > 32 ? 32 : k + 1, level);
@@ -773,7 +738,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                         // R17 with selects (one rare branch): the estimate sum only matters in the
                         // batched modes; a batch closes when it reaches Delta_eval, crossing kernel included
                         if (n == task_first) batch_start = task_first;
-                        const int64_t acc2 = (n == task_first ? 0 : (int64_t)acc) + est;
+                        const int64_t acc2 = (n == task_first ? 0 : acc) + est;
                         const bool closes = sm >= S_BATCHED && acc2 >= P.delta_eval_ns;
                         acc = (closes || last) ? 0 : acc2;
                         target = (last || sm == S_EACH || (closes && sm == S_BATCHED)) ? (int32_t)launched : -1;
@@ -790,10 +755,10 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     } else if (sm == S_EACH) {
                         target = (int32_t)launched;
                     } else {
-                        if (n == task_first) batch_start = task_first;
-                        const int64_t acc2 = (n == task_first ? 0 : (int64_t)acc) + est;
-                        const bool closes = acc2 >= P.delta_eval_ns;
-                        acc = (closes || last) ? 0 : acc2;
+                        if (n == task_first) { acc = 0; batch_start = task_first; }
+                        acc += est;
+                        const bool closes = acc >= P.delta_eval_ns;
+                        if (closes || last) acc = 0;
                         if (last || (closes && sm == S_BATCHED)) target = (int32_t)launched;
                         else if (closes) {   // OVERLAP: wait for the previous batch
                             const uint32_t prev = batch_start;
@@ -806,23 +771,22 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     }
                     if (target >= 0) {
                         sync_target = (uint32_t)target;
-                        int64_t sc = P.sync_lo_ns;
+                        sync_cost = P.sync_lo_ns;
                         if (P.sync_hi_ns > P.sync_lo_ns) {
                             // the sync ordinals of an instance are drawn in order from (stage << 16), a
                             // multiple of 4: one Philox block serves four consecutive sync calls
-                            if ((sync_ord & 3u) == 0u) sy_store(rng_block(P.seed, s, URG_TAG_SYNC, cid, inst, sync_ord));
-                            sc += (int64_t)(sy_word(sync_ord & 3u) % (uint32_t)(P.sync_hi_ns - P.sync_lo_ns + 1));
+                            if ((sync_ord & 3u) == 0u) syw[lane] = rng_block(P.seed, s, URG_TAG_SYNC, cid, inst, sync_ord);
+                            sync_cost += (int64_t)(((const uint32_t *)&syw[lane])[sync_ord & 3u] %
+                                                   (uint32_t)(P.sync_hi_ns - P.sync_lo_ns + 1));
                         }
                         ++sync_ord;
-                        URG_TR(t, TR_SYNC_CALL, sync_target, sc);
+                        URG_TR(t, TR_SYNC_CALL, sync_target, sync_cost);
                         if (done >= sync_target) {
                             pc = PC_SYNC_RET;
-                            cpu_busy(t, sc);
-                            if (sc > 0) break;
+                            cpu_busy(t, sync_cost);
+                            if (sync_cost > 0) break;
                             continue;
                         }
-                        sync_cost = sc;
-                        zwake = sc == 0 ? sync_target - 1u : 0xFFFFFFFFu;
                         pc = PC_SYNC_WAIT;
                         cpu_next = INF64; dc = D_INF;
                         break;
@@ -831,10 +795,10 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                 }
                 if (pc == PC_CPU_DONE || pc == PC_ATTEMPT) {   // launch attempt for kernel n = launched (R14-R16)
                     int64_t lax = 0;
-                    if (urg) { lax = laxity(t); set_L(lax); URG_TR(t, TR_EVAL, lax, launched); }
+                    if (urg) { lax = laxity(t); L_last = lax; URG_TR(t, TR_EVAL, lax, launched); }
                     const bool own_urgent = (uint64_t)lax < P.lth_excl;   // R10: 0 <= L <= L_th
                     if (f_delay && !own_urgent && (urgent_m & ~(1u << lane)) &&
-                        (WIDE ? KREC(launched) : nxt).util_permille >= P.util_exempt) {
+                        (WIDE ? kern_rec(KR + launched) : nxt).util_permille >= P.util_exempt) {
                         URG_TR(t, TR_DELAY, launched, 0);
                         pc = PC_ATTEMPT;
                         cpu_next = t + P.sleep_ns;
@@ -892,13 +856,13 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         // binding snapshot is not needed).
         auto snapshot = [&](bool may_bind, uint32_t &urgent_m, uint32_t &active_m, uint32_t &busy_m) {
             urgent_m = 0; active_m = 0; busy_m = 0;
-            if (f_delay) urgent_m = __ballot_sync(FULL, akb > 0 && lurg) & hmask;
+            if (f_delay) urgent_m = __ballot_sync(FULL, akb > 0 && (uint64_t)L_last < P.lth_excl) & hmask;
             if (coll) {
                 busy_m = __ballot_sync(FULL, launched > done) & hmask;
                 active_m = __ballot_sync(FULL, akb > 0) & hmask;
                 __syncwarp();   // the previous phase's reads of the snapshot are done
                 snapL[lane] = L_last;
-                SNAP_LEV(lane) = level;
+                snapLev[lane] = level;
                 __syncwarp();
             } else if (f_bind && __any_sync(FULL, may_bind)) {
                 active_m = __ballot_sync(FULL, akb > 0) & hmask;
@@ -954,20 +918,14 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                 t = (int64_t)((uint64_t)t_prev + m);   // (an ended half's t_prev may be INF64: wraps, unused)
                 const bool slow = !fin && (m - 1u) >= budget - 1u;
                 if (PK ? __any_sync(FULL, slow) : slow) {
-                    const int64_t he = head_end, cn = cpu_next;
-                    t = hmin64(fin ? INF64 : (he < cn ? he : cn));
+                    t = hmin64(fin ? INF64 : (head_end < cpu_next ? head_end : cpu_next));
                     bad = !fin && t <= t_prev;
                     if (!fin && t != INF64) {
-                        dc = cn == INF64 ? D_INF : dsat(cn - t);
-                        dh = he == INF64 ? D_INF : dsat(he - t);
+                        dc = cpu_next == INF64 ? D_INF : dsat(cpu_next - t);
+                        dh = head_end == INF64 ? D_INF : dsat(head_end - t);
                     }
-                    // every build counts loop steps in 32 bits (all lanes of a half alike) and moves the
-                    // count into the 64-bit total here: at most 2^30 ns of simulated time, hence fewer
-                    // than 2^30 steps, pass between two rare-path steps while the scenario runs
-                    if (!fin && lane == hbase) my_steps += nsteps;
-                    nsteps = 0;
                     {
-                        const int64_t hs = WIDE ? cold_Hs : H_stop;
+                        const int64_t hs = WIDE ? cold_Hs[lane] : H_stop;
                         const int64_t hb = hs - t + 1;
                         budget = hb >= (int64_t)D_SLOW ? D_SLOW : (hb < 1 ? 1u : (uint32_t)hb);
                     }
@@ -980,10 +938,12 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                         }
                     }
                     if (PK) {   // each half ends on its own (only here: a fast step cannot end one)
+                        if (!fin && lane == hbase) my_steps += nsteps;   // this half's steps so far
+                        nsteps = 0;
                         if (bad && lane == hbase &&
                             atomicCAS((unsigned long long *)err, 0ull, (unsigned long long)ERR_TIME) == 0ull)
                             err[1] = s;
-                        fin = fin || t > cold_Hs || bad;
+                        fin = fin || t > cold_Hs[lane] || bad;
                         if (fin) head_u = 0xFFFFu;   // an ended half dispatches nothing
                         if (__all_sync(FULL, fin)) break;
                     }
@@ -1037,9 +997,10 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     break;
                 }
             }
-            if (!URG_DIST_OFF && !CAL) {
-                // loop steps counted in 32 bits, flushed on the rare path (above).  An ended half's
-                // t_prev is never read.
+            if (PK && !URG_DIST_OFF) {
+                // every lane counts its half's loop steps in 32 bits; the count is moved into the
+                // 64-bit total on the rare path (at most 2^30 ns of simulated time, hence fewer than
+                // 2^30 steps, apart) while the half runs.  An ended half's t_prev is never read.
                 t_prev = t;
                 ++nsteps;
 #ifdef URG_DEBUG
@@ -1047,7 +1008,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
 #endif
             } else if (!fin) {
                 t_prev = t;
-                if (lane == hbase) my_steps += 1;   // one loop step (the 64-bit head and the calibration build)
+                if (lane == hbase) ++my_steps;   // one loop step of this half's scenario
 #ifdef URG_DEBUG
                 if (lane == hbase) trace_row(t, TR_STEP, 0, 0);
 #endif
@@ -1057,8 +1018,8 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             const bool ret = !fin && (URG_DIST_OFF ? head_end == t : dh == 0u);
             // The retire and due votes are issued together: a retirement makes its own lane due
             // at t only through a sync return of zero cost (retire(): cpu_busy(t, 0) sets cpu_next = t).
-            // (SYNC_WAIT on a zero-cost sync whose last awaited kernel, number zwake, retires now)
-            const bool due_pre = !fin && ((URG_DIST_OFF ? cpu_next == t : dc == 0u) || (ret && done == zwake));
+            const bool due_pre = !fin && ((URG_DIST_OFF ? cpu_next == t : dc == 0u) || (ret && pc == PC_SYNC_WAIT && done + 1u >= sync_target &&
+                                                            sync_cost == 0));
             const uint32_t retm = __ballot_sync(FULL, ret), duem = __ballot_sync(FULL, due_pre);
             bool dirty = (retm & hmask) != 0u;   // GPU state changed: Phase C must run
             if (retm) {
@@ -1086,7 +1047,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     }
                     const uint32_t nhm = c_always ? 0u : __ballot_sync(FULL, nh);
                     if (f_delay)
-                        urgent_nx = __ballot_sync(FULL, akb > 0 && lurg) & hmask;
+                        urgent_nx = __ballot_sync(FULL, akb > 0 && (uint64_t)L_last < P.lth_excl) & hmask;
                     if (f_bind) active_nx = __ballot_sync(FULL, akb > 0) & hmask;
                     dirty |= (nhm & hmask) != 0u;
                 } else if (!c_always)
@@ -1095,8 +1056,8 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                 // an untaken one); threads waiting for one run in the next round, same t and read view
                 while (te) {
                     __syncwarp();
-                    const uint32_t pub = MBOX(lane);
-                    if (pub) { msg = pub; MBOX(lane) = 0u; }
+                    const uint32_t pub = mbox[lane];
+                    if (pub) { msg = pub; mbox[lane] = 0u; }
                     __syncwarp();
                     const bool wake = !fin && pc == PC_WAIT_MSG && msg != 0u;
                     if (!__any_sync(FULL, wake)) break;
@@ -1228,9 +1189,9 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             continue;
         }
         // ---- A11: end of horizon accounting (R7) and per-scenario records ----
-        uint32_t n_total = R_total, n_miss = R_miss, n_early = R_early, n_unfin = R_unfin,
-                 hash = R_hash;
-        const uint64_t sum_rt = R_sumrt;
+        uint32_t n_total = rac->total, n_miss = rac->miss, n_early = rac->early, n_unfin = rac->unfin,
+                 hash = rac->hash;
+        const uint64_t sum_rt = rac->sum_rt;
         if (te) {   // R32: the chain's early exits and launches, summed over its threads
             uint32_t e_sum = 0, l_sum = 0;
             for (uint32_t o = 0; o < C; ++o) {
@@ -1254,8 +1215,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             n_miss += n_unfin;
             URG_DASSERT(n_miss <= n_total && n_early + n_unfin <= n_miss, INV_COUNTS);
             if (records) {
-                const uint64_t jr = PK ? (uint64_t)my[URG_SL_JW * 32] : (uint64_t)jw;
-                uint4 *r = (uint4 *)(records + (jr * NC + cid) * 8);
+                uint4 *r = (uint4 *)(records + ((uint64_t)jw * NC + cid) * 8);
                 r[0] = make_uint4(n_total, n_miss, n_early, n_unfin);
                 r[1] = make_uint4(n_launch, hash, (uint32_t)sum_rt, (uint32_t)(sum_rt >> 32));
             }
@@ -1273,10 +1233,10 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             if (lane == 0 && nl) atomicAdd(&agg[(uint64_t)NC * stride + URG_COLL_BINS + 0], (unsigned long long)nl);
         }
     }
-    if (PK) my_steps += (int64_t)__shfl_sync(FULL, (unsigned long long)(int64_t)my_steps, 16);   // the upper half's steps
+    if (PK) my_steps += __shfl_sync(FULL, my_steps, 16);   // the upper half's steps
     if (lane == 0) {
         if (CAL) return;
-        atomicAdd(&agg[(uint64_t)NC * stride + URG_COLL_BINS + 1], (unsigned long long)(int64_t)my_steps);
+        atomicAdd(&agg[(uint64_t)NC * stride + URG_COLL_BINS + 1], my_steps);
 #ifdef URG_STATS
         atomicAdd(&work[4], st_single); atomicAdd(&work[5], st_multi);
         atomicAdd(&work[6], st_dispatch); atomicAdd(&work[7], st_rebase);
