@@ -204,14 +204,16 @@ __device__ __forceinline__ uint64_t work_offset(uint64_t j, uint64_t S, uint32_t
 // than the 128-register cap of the 512-thread build).
 template <int KIND, int FLAGS, bool KQ, bool WIDE, bool CAL = false, bool EXT = true, bool PK = false,
           bool SMALL = false>
-// packed-build CTA size per policy: with the cold per-lane state in shared memory, UrgenGo takes 832
-// threads (72 registers, 26 warps/SM; configs[3] slice 2.517 -> 2.535 G/s against 640 / 96) and the
-// ASYNC policies 768 (80 registers; configs[2] FIFO 4.51 -> 4.80 G/s), profiles/r02_ab_i_cold_smem.txt
+// packed-build CTA size per policy: the packed loop's throughput grows with resident warps (22 -> 26
+// warps per SM: 2.36 -> 2.53 G launch events/s on a configs[3] slice), so UrgenGo takes the largest
+// CTA, 1024 threads (64 registers, a few spilled values: 2.55 -> 2.63 G/s against 832 / 72), and the
+// ASYNC policies 896 (72 registers: configs[2] FIFO 4.91 -> 5.04, STATIC 4.69 -> 4.85 G/s against
+// 768 / 80) -- profiles/r02_ab_m_dp_pre2_cta.txt
 #ifndef URG_PK_THREADS
-#define URG_PK_THREADS 832
+#define URG_PK_THREADS 1024
 #endif
 #ifndef URG_PK_THREADS_ASYNC
-#define URG_PK_THREADS_ASYNC 768
+#define URG_PK_THREADS_ASYNC 896
 #endif
 #ifndef URG_LAT_THREADS
 #define URG_LAT_THREADS 512
@@ -428,13 +430,6 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                                                // the head runs, or the half's scenario ended), so the
                                                // Phase C fit test alone excludes such a lane
         uint32_t head_dur = 0;                 // its actual duration (R4), drawn when it becomes head
-        // latency core build: util and duration of kernel done + 1 while it waits right behind the head
-        // (drawn when it gets there), so a retirement hands the next head to Phase C without a load
-#ifndef URG_PRE2
-#define URG_PRE2 1
-#endif
-        constexpr bool pre2 = URG_PRE2 && !EXT && !WIDE && !CAL;
-        uint32_t nx2_u = 0, nx2_dur = 0;
         UrgKernRec nxt = {};                   // latency build: record of the next kernel to launch (kernel
                                                // `launched`), loaded one launch ahead (off the critical path;
                                                // the throughput builds reload it: registers)
@@ -530,9 +525,10 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
 
         // ---- lane-local pieces of a loop step (R21); used by the warp-wide
         //      step and by the single-lane ("solo") steps below ----
-        // R4: the actual duration of kernel k from its nominal duration -- drawn when the kernel
-        // becomes stream head (or, latency core build, when it becomes the kernel right behind the
-        // head): either way in stream order, kept until it starts
+        // R4: the actual duration of kernel k (the stream head) from its nominal duration -- drawn when
+        // the kernel becomes head (kernels become head in stream order), kept until it starts.  (Drawing
+        // the kernel behind the head ahead, so a retirement issues no load, measured 6 % slower on
+        // configs[1]: profiles/r02_ab_m_dp_pre2_cta.txt)
         auto head_duration = [&](uint32_t nom, uint32_t k) -> uint32_t {
             uint64_t G = 65536u;
 #ifdef URG_NO_KQCACHE
@@ -559,17 +555,9 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             head_u = 0xFFFFu;
             if (launched > done) {
                 head_ready = t;
-                if (pre2) {   // the kernel behind the head was drawn already: no load or draw before Phase C
-                    head_u = nx2_u; head_dur = nx2_dur;
-                    if (launched > done + 1u) {
-                        const UrgKernRec kr = kern_rec(KR + done + 1u);
-                        nx2_u = kr.util_permille; nx2_dur = head_duration(kr.nominal_ns, done + 1u);
-                    }
-                } else {
-                    const UrgKernRec kr = kern_rec(KR + done);
-                    head_u = kr.util_permille; head_dur = head_duration(kr.nominal_ns, done);
-                    if (has_copy) head_copy = kr.flags & 1u;
-                }
+                const UrgKernRec kr = kern_rec(KR + done);
+                head_u = kr.util_permille; head_dur = head_duration(kr.nominal_ns, done);
+                if (has_copy) head_copy = kr.flags & 1u;
             }
             if (pc == PC_SYNC_WAIT && done >= sync_target) { pc = PC_SYNC_RET; cpu_busy(t, sync_cost); }
         };
@@ -723,8 +711,6 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     if (launched == done) {   // stream was empty: head now
                         head_ready = t; head_u = kr.util_permille; head_dur = head_duration(kr.nominal_ns, n); newhead = true;
                         if (has_copy) head_copy = kr.flags & 1u;
-                    } else if (pre2 && launched == done + 1u) {   // right behind the head: drawn now
-                        nx2_u = kr.util_permille; nx2_dur = head_duration(kr.nominal_ns, n);
                     }
                     URG_TR(t, TR_ENQUEUE, n, level);
                     ++launched; ++n_launch;
