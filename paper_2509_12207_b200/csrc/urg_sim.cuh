@@ -96,6 +96,18 @@ static __device__ __noinline__ uint4 rng_block(uint64_t seed, uint32_t s, uint32
 // ---------------------------------------------------------------------------
 // small warp helpers
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t lane_id()
+{
+    uint32_t r;
+    asm("mov.u32 %0, %%laneid;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t lane_bit()   // 1 << lane_id()
+{
+    uint32_t r;
+    asm("mov.u32 %0, %%lanemask_eq;" : "=r"(r));
+    return r;
+}
 __device__ __forceinline__ int64_t warp_min_nonneg(int64_t v)    // v >= 0 for every lane
 {
     const uint32_t hi = (uint32_t)((uint64_t)v >> 32), lo = (uint32_t)v;
@@ -224,7 +236,13 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                long long *__restrict__ err)
 {
     extern __shared__ __align__(128) uint8_t sm[];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // packed UrgenGo build: lane index and lane bit from the special registers (one S2R each when the
+    // compiler rematerialises them at 64 registers, instead of S2R TID + logic): configs[3] slice
+    // 2.630 -> 2.730 G/s, configs[4] 3.290 -> 3.398; the other builds measured 0.6-0.8 % slower with it
+    // (profiles/r02_ab_p_laneid.txt)
+    constexpr bool sreg_lane = PK && KIND == K_URGENGO;
+    const int lane = sreg_lane ? (int)lane_id() : (int)(threadIdx.x & 31);
+    const int warp = threadIdx.x >> 5;
 
     // ---- A0: template staging (once per CTA) ----
     stage_blob(sm, blob, P.blob_bytes, (uint64_t *)(sm + P.mbar_offset));
@@ -289,7 +307,8 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
     const uint32_t stride = P.agg_stride;
     // lane -> (half, chain); masks and snapshot slots stay indexed by lane
     const int half = PK ? (lane >> 4) : 0;
-    const uint32_t hmask = PK ? (0xFFFFu << (16 * half)) : FULL;
+    const uint32_t hmask = PK ? (0xFFFFu << (lane & 16)) : FULL;
+    auto lbit = [&]() -> uint32_t { return sreg_lane ? lane_bit() : (1u << lane); };
     const int hbase = PK ? (lane & 16) : 0;
     const uint32_t c = PK ? (uint32_t)(lane & 15) : (uint32_t)lane;
     const bool valid_c = c < C;
@@ -543,7 +562,9 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             }
 #endif
             const uint64_t d = ((((uint64_t)nom * Fg) >> 16) * G) >> 16;
-            return d < 1 ? 1u : (d > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)d);
+            // clamp to [1, 2^32 - 1] on the two 32-bit halves (one test of the high word, one max)
+            const uint32_t lo = (uint32_t)d, lo1 = lo > 1u ? lo : 1u;
+            return (uint32_t)(d >> 32) ? 0xFFFFFFFFu : lo1;
         };
         // Phase A for a lane whose running kernel ends at t (R19)
         auto retire = [&](int64_t t) {
@@ -721,7 +742,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     if (coll && (uint64_t)L_last < P.lth_excl) {
                         // R24: less urgent chains with a busy stream at the same or a higher priority
                         const int64_t own = urgency_key(L_last);
-                        uint32_t mm = busy_m & ~(1u << lane), k = 0;
+                        uint32_t mm = busy_m & ~lbit(), k = 0;
                         while (mm) {
                             const int o = __ffs(mm) - 1;
                             mm &= mm - 1;
@@ -801,7 +822,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     int64_t lax = 0;
                     if (urg) { lax = laxity(t); L_last = lax; URG_TR(t, TR_EVAL, lax, launched); }
                     const bool own_urgent = (uint64_t)lax < P.lth_excl;   // R10: 0 <= L <= L_th
-                    if (f_delay && !own_urgent && (urgent_m & ~(1u << lane)) &&
+                    if (f_delay && !own_urgent && (urgent_m & ~lbit()) &&
                         (WIDE ? kern_rec(KR + launched) : nxt).util_permille >= P.util_exempt) {
                         URG_TR(t, TR_DELAY, launched, 0);
                         pc = PC_ATTEMPT;
@@ -812,7 +833,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     if (launched == task_first) {   // task-level stream binding
                         if (KIND == K_STATIC) level = static_level;
                         else if (cls) {   // R27: rank among itself and the AKB-active chains
-                            uint32_t mm = active_m & ~(1u << lane);
+                            uint32_t mm = active_m & ~lbit();
                             const uint32_t n_r = 1 + __popc(mm);
                             const int64_t ownA = cls_key_a(), ownB = cls_key_b();
                             uint32_t r = 1;
@@ -829,7 +850,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                         else if (own_urgent) level = 0;
                         else {
                             const int64_t own = urgency_key(lax);
-                            uint32_t mm = active_m & ~(1u << lane);
+                            uint32_t mm = active_m & ~lbit();
                             const uint32_t n_r = 1 + __popc(mm);
                             uint32_t r = 1;
                             while (mm) {
@@ -1091,7 +1112,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                         snapA[lane] = prio;
                         snapB[lane] = job_ready;
                         __syncwarp();
-                        uint32_t better = 0, mm = jm & ~(1u << lane);
+                        uint32_t better = 0, mm = jm & ~lbit();
                         while (mm) {
                             const int o = __ffs(mm) - 1;
                             mm &= mm - 1;
