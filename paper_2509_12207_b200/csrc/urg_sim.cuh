@@ -271,7 +271,9 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
     // ... the throughput UrgenGo build's t_arr and D' (read per instance), and every build's per-scenario
     // record counters of R22 (updated once per instance)
     volatile int64_t *cold_Ta = snapL + 384, *cold_Dp = snapL + 416;
-    struct UrgAcc { uint32_t total, miss, early, unfin, hash, pad; unsigned long long sum_rt; };   // 32 B
+    // (launches: the kernels launched by the lane's finished instances; the current instance's are
+    // launched - k_first, so the per-launch path keeps no launch counter)
+    struct UrgAcc { uint32_t total, miss, early, unfin, hash, launches; unsigned long long sum_rt; };   // 32 B
     volatile UrgAcc *rac = (volatile UrgAcc *)(snapL + 448) + lane;
     constexpr bool urg = KIND == K_URGENGO;
     constexpr bool cls = KIND >= K_EDF;        // classical policies (R27): AKB-tracking, no urgency
@@ -426,7 +428,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         uint32_t inst = 0;
         int64_t t_arr = 0;
         uint32_t Fg = 65536u, Fc = 65536u;
-        uint32_t task = 0, launched = 0, done = 0, level = 0;
+        uint32_t task = 0, launched = k_first, done = k_first, level = 0;
         uint32_t task_first = 0, task_end = 0;
         int64_t rem_g = 0, rem_c = 0;          // sum of estimates of kernels / CPU segments not yet passed
         // core UrgenGo build: Eq. 2 without its t, lb = t_arr + D' - rem_g - rem_c, kept instead of the two sums
@@ -453,8 +455,8 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                                                // `launched`), loaded one launch ahead (off the critical path;
                                                // the throughput builds reload it: registers)
         bool head_copy = false;                // R31: the head is a memcpy (copy engine)
-        uint32_t n_launch = 0;
         rac->total = 0; rac->miss = 0; rac->early = 0; rac->unfin = 0; rac->hash = 2166136261u; rac->sum_rt = 0ull;
+        rac->launches = 0;
         uint32_t msg = 0;                      // R32: delivered, untaken message (instance + 1), 0 = none
         uint32_t expect = 0;                   // R32, last stage: next instance to record
 #ifdef URG_DEBUG
@@ -654,6 +656,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                         Fg = inst_factor(w.x, CRF(gpu_sigma_ppm));
                         Fc = inst_factor(w.y, CRF(cpu_sigma_ppm));
                     }
+                    rac->launches = rac->launches + (launched - k_first);   // the previous instance's launches
                     task = stage; launched = k_first; done = k_first; sync_ord = stage << 16;
                     if (!WIDE) nxt = kern_rec(KR + k_first);
                     rem_g = myvar[lane].gpu_est_total; rem_c = CRF(cpu_est_total);
@@ -734,7 +737,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                         if (has_copy) head_copy = kr.flags & 1u;
                     }
                     URG_TR(t, TR_ENQUEUE, n, level);
-                    ++launched; ++n_launch;
+                    ++launched;
                     if (!WIDE && launched < CRF(num_kernels)) nxt = kern_rec(KR + launched);
                     rem_g -= est;
                     if (lb_on) lb += est;
@@ -916,7 +919,9 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         // fast-step budget: a step of m ns stays on the fast path iff 0 < m < budget, where budget =
         // min(2^30 - advance since the last exact refresh, H_stop - t_prev + 1) -- one compare covers
         // "time did not advance", "a distance may be inexact" and "past the end of the horizon"
-        uint32_t budget = H_stop + 2 >= (int64_t)D_SLOW ? D_SLOW : (uint32_t)(H_stop + 2);   // t_prev = -1
+        // kept as its end point lim = low 32 bits of (t_prev + budget), fixed between rare-path steps
+        // (budget <= 2^30, so budget = lim - low 32 bits of t_prev): nothing to update on a fast step
+        uint32_t lim = (uint32_t)-1 + (H_stop + 2 >= (int64_t)D_SLOW ? D_SLOW : (uint32_t)(H_stop + 2));   // t_prev = -1
         uint32_t used = 0;
         bool bar_prev = false;                  // R28: a barrier was pending at the previous step
         int64_t cal_next = 0;                   // CAL: next sampling time
@@ -941,7 +946,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
             if constexpr (!URG_DIST_OFF) {   // (the 64-bit head below is kept for A/B: -DURG_NO_DIST)
                 const uint32_t m = hmin(fin ? D_INF : (dc < dh ? dc : dh));
                 t = (int64_t)((uint64_t)t_prev + m);   // (an ended half's t_prev may be INF64: wraps, unused)
-                const bool slow = !fin && (m - 1u) >= budget - 1u;
+                const bool slow = !fin && (m - 1u) >= (lim - (uint32_t)t_prev) - 1u;
                 if (PK ? __any_sync(FULL, slow) : slow) {
                     t = hmin64(fin ? INF64 : (head_end < cpu_next ? head_end : cpu_next));
                     bad = !fin && t <= t_prev;
@@ -952,7 +957,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     {
                         const int64_t hs = WIDE ? cold_Hs[lane] : H_stop;
                         const int64_t hb = hs - t + 1;
-                        budget = hb >= (int64_t)D_SLOW ? D_SLOW : (hb < 1 ? 1u : (uint32_t)hb);
+                        lim = (uint32_t)t + (hb >= (int64_t)D_SLOW ? D_SLOW : (hb < 1 ? 1u : (uint32_t)hb));
                     }
                     if (!PK && !CAL) {
                         if (t > H_stop) break;
@@ -975,7 +980,6 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                 } else {
                     dc -= m;
                     dh -= m;
-                    budget -= m;
                 }
             } else {   // 64-bit next-event times; 32-bit distances from t_prev, saturated
                 const int64_t mine = fin ? INF64 : (head_end < cpu_next ? head_end : cpu_next);
@@ -1158,8 +1162,9 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     const uint32_t fitw = __ballot_sync(FULL, used + head_u <= 1000u);
                     if (!fitw) break;
                     const uint32_t fit = fitw & hmask;
-                    const bool multi = (fit & (fit - 1)) != 0u;
-                    const bool any_multi = __any_sync(FULL, multi);
+                    // some half has two or more fitting heads: read off the (warp-uniform) ballot, no vote
+                    const uint32_t f0 = fitw & 0xFFFFu, f1 = fitw >> 16;
+                    const bool any_multi = ((f0 & (f0 - 1u)) | (f1 & (f1 - 1u))) != 0u;
                     int wl = fit ? __ffs(fit) - 1 : -1;
                     if (any_multi) {
                         const bool in = (fit >> lane) & 1u;
@@ -1218,6 +1223,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         // ---- A11: end of horizon accounting (R7) and per-scenario records ----
         uint32_t n_total = rac->total, n_miss = rac->miss, n_early = rac->early, n_unfin = rac->unfin,
                  hash = rac->hash;
+        uint32_t n_launch = rac->launches + (launched - k_first);   // + the current instance's
         const uint64_t sum_rt = rac->sum_rt;
         if (te) {   // R32: the chain's early exits and launches, summed over its threads
             uint32_t e_sum = 0, l_sum = 0;
