@@ -242,7 +242,15 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
     // (profiles/r02_ab_p_laneid.txt)
     constexpr bool sreg_lane = PK && KIND == K_URGENGO;
     const int lane = sreg_lane ? (int)lane_id() : (int)(threadIdx.x & 31);
-    const int warp = threadIdx.x >> 5;
+    // packed UrgenGo build: the warp index through a shuffle from lane 0, warp-uniform by construction,
+    // so the compiler keeps the warp's slot base in a uniform register instead of rematerialising it
+    // (S2R TID + the shared-window base + multiply) at every use: configs[3] slice 2.868 -> 2.965 G/s,
+    // configs[4] 3.516 -> 3.544; FIFO measured 3 % slower with it (profiles/r02_ab_w_uniform_warp.txt)
+#ifndef URG_UW_ALL
+#define URG_UW_ALL 0
+#endif
+    constexpr bool uw_on = URG_UW_ALL || sreg_lane;
+    const int warp = uw_on ? __shfl_sync(FULL, (int)(threadIdx.x >> 5), 0) : (int)(threadIdx.x >> 5);
 
     // ---- A0: template staging (once per CTA) ----
     stage_blob(sm, blob, P.blob_bytes, (uint64_t *)(sm + P.mbar_offset));
