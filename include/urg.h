@@ -76,7 +76,7 @@ typedef struct {
     uint32_t num_prio;                    /* NUM_PRI stream priorities, 1..8 (6) */
     int64_t launch_ns;                    /* lambda, CPU cost of a launch */
     int64_t launch_akb_ns;                /* extra UrgenGo cost per launch: AKB update */
-    int64_t sync_lo_ns, sync_hi_ns;       /* sigma range per sync call */
+    int64_t sync_lo_ns, sync_hi_ns;       /* sigma range per sync call; 0 <= lo <= hi < 2^32 - 1 */
     int64_t jitter_ns;                    /* arrival jitter J; must be < every P' */
     const int32_t *inst_quantiles_q16;    /* host, 4096 truncated-normal z quantiles (Q16.16) or NULL */
     const uint32_t *kern_quantiles_q16;   /* host, 4096 per-kernel factor quantiles (Q16.16) or NULL */

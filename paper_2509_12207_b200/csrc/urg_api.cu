@@ -102,7 +102,7 @@ extern "C" urg_status urg_create_workload(const urg_workload_desc *d, urg_worklo
     if (d->launch_akb_ns < 0) return fail(URG_EINVAL, "launch_akb_ns must be >= 0");
     if (d->sync_lo_ns < 0 || d->sync_hi_ns < d->sync_lo_ns)
         return fail(URG_EINVAL, "sync range must satisfy 0 <= sync_lo_ns <= sync_hi_ns");
-    if (d->sync_hi_ns - d->sync_lo_ns >= 0xFFFFFFFFLL) return fail(URG_ERANGE, "sync_hi_ns - sync_lo_ns must be < 2^32 - 1");
+    if (d->sync_hi_ns >= 0xFFFFFFFFLL) return fail(URG_ERANGE, "sync_hi_ns must be < 2^32 - 1 (the kernel keeps sync costs in 32 bits)");
     if (d->jitter_ns < 0 || d->jitter_ns >= 0xFFFFFFFFLL) return fail(URG_EINVAL, "jitter_ns must be in [0, 2^32 - 1)");
     if (d->rt_bin_ns <= 0) return fail(URG_EINVAL, "rt_bin_ns must be > 0");
     if (d->rt_bins < 1 || d->rt_bins > (1u << 20)) return fail(URG_EINVAL, "rt_bins must be in 1..2^20");

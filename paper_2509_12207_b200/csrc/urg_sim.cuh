@@ -449,7 +449,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         int64_t job_rem = 0, job_ready = 0, run_start = 0, cpu_prio = 0;
         int64_t acc = 0;
         uint32_t batch_start = 0, sync_target = 0, sync_ord = 0;
-        int64_t sync_cost = 0;
+        uint32_t sync_cost = 0;                // sigma of the pending sync call (host: < 2^32 - 1 ns)
         uint32_t akb = 0;
         int64_t L_last = 0;
         int64_t head_end = INF64;              // end of the running kernel, INF64 when the stream runs nothing
@@ -807,12 +807,12 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     }
                     if (target >= 0) {
                         sync_target = (uint32_t)target;
-                        sync_cost = P.sync_lo_ns;
+                        sync_cost = (uint32_t)P.sync_lo_ns;
                         if (P.sync_hi_ns > P.sync_lo_ns) {
                             // the sync ordinals of an instance are drawn in order from (stage << 16), a
                             // multiple of 4: one Philox block serves four consecutive sync calls
                             if ((sync_ord & 3u) == 0u) syw[lane] = rng_block(P.seed, s, URG_TAG_SYNC, cid, inst, sync_ord);
-                            sync_cost += (int64_t)(((const uint32_t *)&syw[lane])[sync_ord & 3u] %
+                            sync_cost += (((const uint32_t *)&syw[lane])[sync_ord & 3u] %
                                                    (uint32_t)(P.sync_hi_ns - P.sync_lo_ns + 1));
                         }
                         ++sync_ord;
