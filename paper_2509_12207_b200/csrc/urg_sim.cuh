@@ -313,7 +313,13 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
     uint32_t *ma_ring = (uint32_t *)(sm + P.ma_offset) + (size_t)threadIdx.x * P.ma_slot;
     uint32_t *ma_cnt = ma_ring + P.ma_max_tasks * P.ma_w;
     uint32_t *ma_pred = ma_cnt + P.ma_max_tasks;
-    const int64_t busy_launch = P.busy_launch_ns;   // lambda (+ lambda_akb for UrgenGo), host-derived
+    // lambda (+ lambda_akb for UrgenGo), host-derived.  The packed builds of the other policies read it
+    // from the parameter bank at each use (a constant operand) instead of holding it in registers:
+    // configs[2] FIFO 5.07 -> 5.22 G/s; the packed UrgenGo build was 1 % slower that way and keeps the
+    // register (profiles/r02_ab_aa_lambda_param.txt).  busy_launch_d32 != 0 <=> busy_launch_ns > 0.
+    constexpr bool bl_param = PK && !urg;
+    const int64_t busy_launch_r = P.busy_launch_ns;
+#define busy_launch (bl_param ? P.busy_launch_ns : busy_launch_r)
     const uint32_t stride = P.agg_stride;
     // lane -> (half, chain); masks and snapshot slots stay indexed by lane
     const int half = PK ? (lane >> 4) : 0;
@@ -880,7 +886,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
                     pc = PC_ENQUEUE;
                     if (!cores_on || busy_launch == 0) { cpu_next = t + busy_launch; dc = P.busy_launch_d32; }
                     else cpu_busy(t, busy_launch);
-                    if (busy_launch > 0) break;
+                    if (bl_param ? P.busy_launch_d32 != 0u : busy_launch > 0) break;
                     continue;
                 }
                 break;   // PC_SYNC_WAIT / PC_DONE: nothing to do at t
@@ -916,7 +922,7 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
         // a due lane can bind in this phase unless it is mid-task and the launch cost
         // makes it yield before reaching the next task's first kernel
         auto can_bind = [&]() -> bool {
-            return !(busy_launch > 0 && ((pc == PC_ENQUEUE && launched + 1 < task_end) ||
+            return !((bl_param ? P.busy_launch_d32 != 0u : busy_launch > 0) && ((pc == PC_ENQUEUE && launched + 1 < task_end) ||
                                          (pc == PC_ATTEMPT && launched != task_first)));
         };
 
@@ -1285,6 +1291,8 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
     }
 }
 
+
+#undef busy_launch
 
 // ---------------------------------------------------------------------------
 // instantiation rows: 0 FIFO, 1 STATIC, 2 + f UrgenGo with flags f (0..15);
