@@ -292,8 +292,9 @@ urg_sim_kernel(const uint8_t *__restrict__ blob, const UrgSimParams P, uint32_t 
     // Core build: Phase C's fit ballot runs at every step and is itself the test, so no "new
     // stream head" vote sits between Phase B and Phase C (a head that did not fit at an earlier
     // Phase C still does not: `used` only falls at a retirement).
-    // Measured: +1-2 % on UrgenGo packed; the latency build ran 3x slower; the ASYNC policies
-    // (FIFO / STATIC) lost 13 % with it (configs[2]) and keep the new-head vote.
+    // Measured: +1-2 % on UrgenGo packed in round 1, +8 % on the round-2 build (configs[3] slice 2.772 ->
+    // 2.993 G/s, profiles/r02_ab_ac_newhead_vote_rejected.txt); the latency build ran 3x slower; the
+    // ASYNC policies (FIFO / STATIC) lost 13 % with it (configs[2]) and keep the new-head vote.
 #ifdef URG_OLD_CALWAYS
     constexpr bool c_always = PK && !EXT && !CAL;
     constexpr bool r17_sel = true;
